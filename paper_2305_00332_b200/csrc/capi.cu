@@ -1,0 +1,508 @@
+// capi.cu -- host dispatch behind include/mmlttb.h (extern "C", no torch).
+//
+// Each entry validates its O(1) arguments defensively (the Python layer has
+// already raised the reference's exception classes in the reference's order),
+// carves the caller's workspace, and enqueues 1-4 kernels on the caller's
+// stream.  Nothing here synchronises the host.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/mmlttb.h"
+#include "kernels.cuh"
+
+using namespace mm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return MM_OK;
+}
+
+constexpr int64_t ALIGN = 256;
+inline int64_t up(int64_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int esize(int dt) { return (dt == MM_F32 || dt == MM_I32) ? 4 : 8; }
+inline bool ydt_ok(int dt) { return dt == MM_F32 || dt == MM_F64; }
+inline bool xdt_ok(int dt) { return dt >= MM_F32 && dt <= MM_I32; }
+
+// workspace bump allocator over the caller's buffer
+struct Carve {
+  char* p;
+  int64_t left;
+  bool ok = true;
+  template <typename T> T* take(int64_t count) {
+    const int64_t bytes = up(count * (int64_t)sizeof(T));
+    if (bytes > left) { ok = false; return nullptr; }
+    T* r = reinterpret_cast<T*>(p);
+    p += bytes;
+    left -= bytes;
+    return r;
+  }
+};
+
+// ---- K1 planning --------------------------------------------------------
+struct ExPlan {
+  int64_t C, chunk;
+};
+
+// Chunk length per warp: big enough to amortise the per-warp setup, small
+// enough that the grid has many waves over 148 SMs x 64 resident warps.
+ExPlan plan_extrema(int64_t total_elems, int64_t max_bucket, int ydt) {
+  const int64_t target_max = ydt == MM_F32 ? 8192 : 4096;
+  const int64_t want_warps = 148LL * 64 * 6;
+  int64_t target = total_elems / want_warps;
+  target = std::max<int64_t>(1024, std::min<int64_t>(target_max, target));
+  ExPlan p;
+  p.C = std::max<int64_t>(1, cdiv(max_bucket, target));
+  p.chunk = cdiv(max_bucket, p.C);
+  return p;
+}
+
+int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
+  const int64_t warps = a.B * a.nb * a.C;
+  const int64_t blocks = cdiv(warps, 8);
+  if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
+  if (ydt == MM_F32)
+    k_extrema<float, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else
+    k_extrema<double, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
+  return check_launch("k_extrema");
+}
+
+bool mul_ok(int64_t a, int64_t b) { return a == 0 || b <= INT64_MAX / a; }
+
+// ---- K3 planning --------------------------------------------------------
+constexpr int NBB = 32;  // buckets per k_lttb_tables block
+
+int smax_for(int64_t s) {
+  if (s <= 4) return 4;
+  if (s <= 8) return 8;
+  if (s <= 16) return 16;
+  if (s <= 32) return 32;
+  if (s <= 64) return 64;
+  return 0;
+}
+
+int64_t jump_smem(int64_t k3, int smax) { return 2 * ((k3 * smax + 15) / 16 * 16); }
+constexpr int64_t JUMP_SMEM_MAX = 200 * 1024;
+
+// Which LTTB kernel pair runs for bucket-size bound `s` and k3 buckets.
+bool use_tables(int64_t s, int64_t k3) {
+  const int sm = smax_for(s);
+  return sm > 0 && jump_smem(k3, sm) <= JUMP_SMEM_MAX;
+}
+
+int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s) {
+  const int64_t k3 = n_out - 2;
+  if (use_tables(s, k3)) return up(B * ((k3 * smax_for(s) + 15) / 16 * 16));
+  return up(B * k3 * (int64_t)sizeof(double2));
+}
+
+template <int SMAX> int jump_attr() {
+  static bool done = false;
+  if (!done) {
+    if (cudaFuncSetAttribute(k_lttb_jump<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JUMP_SMEM_MAX) != cudaSuccess)
+      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_lttb_jump)");
+    done = true;
+  }
+  return MM_OK;
+}
+
+template <typename XT, typename YT, int SMAX>
+int launch_tables_jump(LttbArgs a, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  a.tab_ld = (k3 * SMAX + 15) / 16 * 16;
+  dim3 g((unsigned)cdiv(k3, NBB), (unsigned)a.B);
+  constexpr int NT = NBB * SMAX < 1024 ? NBB * SMAX : 1024;
+  k_lttb_tables<XT, YT, SMAX, NBB><<<g, NT, 0, st>>>(a);
+  int rc = check_launch("k_lttb_tables");
+  if (rc) return rc;
+  if ((rc = jump_attr<SMAX>())) return rc;
+  k_lttb_jump<SMAX><<<(unsigned)a.B, 1024, (size_t)jump_smem(k3, SMAX), st>>>(a);
+  return check_launch("k_lttb_jump");
+}
+
+template <typename XT, typename YT>
+int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  if (a.B > 65535 && use_tables(s, k3)) return fail(MM_ERANGE, "batch > 65535 series");
+  if (use_tables(s, k3)) {
+    switch (smax_for(s)) {
+      case 4: return launch_tables_jump<XT, YT, 4>(a, st);
+      case 8: return launch_tables_jump<XT, YT, 8>(a, st);
+      case 16: return launch_tables_jump<XT, YT, 16>(a, st);
+      case 32: return launch_tables_jump<XT, YT, 32>(a, st);
+      default: return launch_tables_jump<XT, YT, 64>(a, st);
+    }
+  }
+  a.means = reinterpret_cast<double2*>(a.tables);
+  a.means_ld = k3;
+  const int64_t n = a.B * k3;
+  k_lttb_means<XT, YT><<<(unsigned)cdiv(n, 128), 128, 0, st>>>(a);
+  int rc = check_launch("k_lttb_means");
+  if (rc) return rc;
+  k_lttb_chain<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
+  return check_launch("k_lttb_chain");
+}
+
+template <typename XT>
+int launch_lttb_x(LttbArgs a, int ydt, int64_t s, cudaStream_t st) {
+  if (ydt == MM_F32) return launch_lttb_t<XT, float>(a, s, st);
+  if (ydt == MM_F64) return launch_lttb_t<XT, double>(a, s, st);
+  return fail(MM_EINVAL, "y dtype");
+}
+
+// a.tables must point at lttb_ws(B, n_out, s) bytes of workspace
+int launch_lttb(LttbArgs a, int xdt, int ydt, int64_t s, cudaStream_t st) {
+  switch (xdt) {
+    case MM_F32: return launch_lttb_x<float>(a, ydt, s, st);
+    case MM_F64: return launch_lttb_x<double>(a, ydt, s, st);
+    case MM_I64: return launch_lttb_x<long long>(a, ydt, s, st);
+    case MM_I32: return launch_lttb_x<int>(a, ydt, s, st);
+  }
+  return fail(MM_EINVAL, "x dtype");
+}
+
+// ---- shared pieces of the fused entries ----------------------------------
+// sizes for minmaxlttb / preselect on B series
+int64_t preselect_ws(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt, bool with_lttb) {
+  const int64_t k = (n_out - 2) * (r_ps / 2);
+  const int64_t S = cdiv(N - 2, k);
+  const ExPlan p = plan_extrema(B * (N - 2), S, ydt);
+  const int64_t cap = 2 + 2 * k;
+  int64_t bytes = up(B * k * p.C * (int64_t)sizeof(Partial)) + up(B * 8);
+  if (with_lttb) bytes += 3 * up(B * cap * 8) + lttb_ws(B, n_out, r_ps);
+  return bytes;
+}
+
+int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
+  if (!y) return fail(MM_EINVAL, "y is null");
+  if (!ydt_ok(ydt)) return fail(MM_EINVAL, "y dtype must be f32 or f64");
+  if (B < 1 || N < 2) return fail(MM_EINVAL, "need B >= 1 and N >= 2");
+  if (n_out < 3 || n_out > N) return fail(MM_EINVAL, "n_out must be in [3, %lld]", (long long)N);
+  return MM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mmlttb_version(void) { return 1; }
+const char* mmlttb_last_error(void) { return g_err.c_str(); }
+
+int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int y_dtype) {
+  if (B < 1 || N < 3 || n_out < 3 || n_out > N) return 0;
+  switch (op) {
+    case MM_OP_MINMAXLTTB:
+      if (r_ps == 1) return mmlttb_workspace_bytes(MM_OP_MINMAX, B, N, n_out, 0, y_dtype);
+      if (r_ps < 2 || r_ps % 2) return 0;
+      return preselect_ws(B, N, n_out, r_ps, y_dtype, true);
+    case MM_OP_PRESELECT:
+      if (r_ps < 2 || r_ps % 2) return 0;
+      return preselect_ws(B, N, n_out, r_ps, y_dtype, false);
+    case MM_OP_LTTB:
+      return lttb_ws(B, n_out, cdiv(N - 2, n_out - 2));
+    case MM_OP_MINMAX:
+    case MM_OP_M4: {
+      const int64_t k = op == MM_OP_MINMAX ? n_out / 2 : n_out / 4;
+      if (k < 1) return 0;
+      const ExPlan p = plan_extrema(B * N, cdiv(N, k), y_dtype);
+      return up(B * k * p.C * (int64_t)sizeof(Partial));
+    }
+  }
+  return 0;
+}
+
+int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out,
+                            int64_t r_ps, int64_t* out, int64_t out_ld, int64_t* out_count, void* workspace,
+                            int64_t workspace_bytes, void* stream) {
+  int rc = check_common(y, y_dtype, B, N, n_out);
+  if (rc) return rc;
+  if (r_ps < 2 || r_ps % 2) return fail(MM_EINVAL, "r_ps must be even >= 2");
+  const int64_t k = (n_out - 2) * (r_ps / 2);
+  if (k > N - 2) return fail(MM_EINVAL, "sub-buckets exceed interior");
+  if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
+  if (out_ld < 2 + 2 * k) return fail(MM_EINVAL, "out_ld < 2 + 2k");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t S = cdiv(N - 2, k);
+  const ExPlan p = plan_extrema(B * (N - 2), S, y_dtype);
+  Carve cv{(char*)workspace, workspace_bytes};
+  Partial* part = cv.take<Partial>(B * k * p.C);
+  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
+  ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk, part};
+  if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
+  CompactArgs ca{};
+  ca.part = part; ca.nb = k; ca.C = p.C; ca.mode = 0;
+  ca.emit_first = 0; ca.emit_last = N - 1; ca.force_n_out = 0; ca.last_index = N - 1;
+  ca.start = 1; ca.len = N - 2; ca.k = k; ca.b0 = 0;
+  ca.out_idx = out; ca.out_ld = out_ld; ca.out_count = out_count;
+  k_compact<512><<<(unsigned)B, 512, 0, st>>>(ca);
+  return check_launch("k_compact");
+}
+
+static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int m4,
+                       int64_t force_n_out, int64_t* out, int64_t* out_count, void* ws, int64_t wsb,
+                       cudaStream_t st) {
+  int rc = check_common(y, ydt, B, N, n_out);
+  if (rc) return rc;
+  const int64_t k = m4 ? n_out / 4 : n_out / 2;
+  if ((m4 && n_out % 4) || (!m4 && n_out % 2)) return fail(MM_EINVAL, "n_out divisibility");
+  if (!mul_ok(k + 1, N)) return fail(MM_ERANGE, "k*N overflows int64");
+  const ExPlan p = plan_extrema(B * N, cdiv(N, k), ydt);
+  Carve cv{(char*)ws, wsb};
+  Partial* part = cv.take<Partial>(B * k * p.C);
+  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
+  ExArgs ea{y, y_ld, B, 0, N, k, nullptr, 0, k, p.C, p.chunk, part};
+  if ((rc = launch_extrema(ea, ydt, st))) return rc;
+  CompactArgs ca{};
+  ca.part = part; ca.nb = k; ca.C = p.C; ca.mode = m4 ? 1 : 0;
+  ca.emit_first = -1; ca.emit_last = -1; ca.force_n_out = force_n_out; ca.last_index = N - 1;
+  ca.start = 0; ca.len = N; ca.k = k; ca.b0 = 0;
+  ca.out_idx = out; ca.out_ld = n_out; ca.out_count = out_count;
+  k_compact<512><<<(unsigned)B, 512, 0, st>>>(ca);
+  return check_launch("k_compact");
+}
+
+int mmlttb_minmax(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int64_t* out,
+                  int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream) {
+  return minmax_impl(y, y_dtype, y_ld, B, N, n_out, 0, 0, out, out_count, workspace, workspace_bytes,
+                            (cudaStream_t)stream);
+}
+
+int mmlttb_m4(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int64_t* out,
+              int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream) {
+  return minmax_impl(y, y_dtype, y_ld, B, N, n_out, 1, 0, out, out_count, workspace, workspace_bytes,
+                            (cudaStream_t)stream);
+}
+
+int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
+                      int64_t N, int64_t n_out, int64_t r_ps, int64_t* out, int64_t* out_count, void* workspace,
+                      int64_t workspace_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r_ps == 1) {  // downsamplers.py:204-205
+    if (n_out % 2) return fail(MM_EINVAL, "r_ps=1 needs an even n_out");
+    return minmax_impl(y, y_dtype, y_ld, B, N, n_out, 0, n_out, out, out_count, workspace, workspace_bytes, st);
+  }
+  int rc = check_common(y, y_dtype, B, N, n_out);
+  if (rc) return rc;
+  if (!x || !xdt_ok(x_dtype)) return fail(MM_EINVAL, "x missing or bad dtype");
+  if (r_ps < 2 || r_ps % 2) return fail(MM_EINVAL, "r_ps must be 1 or even >= 2");
+  const int64_t k = (n_out - 2) * (r_ps / 2);
+  if (k > N - 2) return fail(MM_EINVAL, "sub-buckets exceed interior");
+  if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
+  const int64_t S = cdiv(N - 2, k);
+  const ExPlan p = plan_extrema(B * (N - 2), S, y_dtype);
+  const int64_t cap = 2 + 2 * k;
+  Carve cv{(char*)workspace, workspace_bytes};
+  Partial* part = cv.take<Partial>(B * k * p.C);
+  int64_t* cnt = cv.take<int64_t>(B);
+  int64_t* pre = cv.take<int64_t>(B * cap);
+  double* px = cv.take<double>(B * cap);
+  double* py = cv.take<double>(B * cap);
+  unsigned char* lt = cv.take<unsigned char>(lttb_ws(B, n_out, r_ps));
+  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small (%lld bytes)", (long long)workspace_bytes);
+  // K1: sub-bucket extrema over partition(1, N-1, k)  (downsamplers.py:149-155)
+  ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk, part};
+  if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
+  // K2: [0] + interleaved pairs + [N-1], gathered as f64 (:156-160, :207)
+  CompactArgs ca{};
+  ca.part = part; ca.nb = k; ca.C = p.C; ca.mode = 0;
+  ca.emit_first = 0; ca.emit_last = N - 1; ca.force_n_out = 0; ca.last_index = N - 1;
+  ca.start = 1; ca.len = N - 2; ca.k = k; ca.b0 = 0;
+  ca.out_idx = pre; ca.out_ld = cap; ca.out_count = cnt;
+  ca.x = x; ca.xdt = x_dtype; ca.x_ld = x_ld; ca.x_off = 0;
+  ca.y = y; ca.ydt = y_dtype; ca.y_ld = y_ld; ca.y_off = 0;
+  ca.out_x = px; ca.out_y = py;
+  k_compact<512><<<(unsigned)B, 512, 0, st>>>(ca);
+  if ((rc = check_launch("k_compact"))) return rc;
+  // K3: LTTB over the compacted sub-series, mapped back (:208-209)
+  LttbArgs la{};
+  la.x = px; la.x_ld = cap; la.y = py; la.y_ld = cap;
+  la.m_dev = cnt; la.n = 0; la.bounds = nullptr; la.map = pre; la.map_ld = cap;
+  la.B = B; la.n_out = n_out; la.out = out; la.tables = lt;
+  if ((rc = launch_lttb(la, MM_F64, MM_F64, r_ps, st))) return rc;
+  if (out_count) {  // every series yields exactly n_out (P9)
+    k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
+    return check_launch("k_fill");
+  }
+  return MM_OK;
+}
+
+int mmlttb_lttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
+                int64_t N, int64_t n_out, int64_t* out, void* workspace, int64_t workspace_bytes, void* stream) {
+  int rc = check_common(y, y_dtype, B, N, n_out);
+  if (rc) return rc;
+  if (!x || !xdt_ok(x_dtype)) return fail(MM_EINVAL, "x missing or bad dtype");
+  if (!mul_ok(n_out, N)) return fail(MM_ERANGE, "n_out*N overflows int64");
+  const int64_t s = cdiv(N - 2, n_out - 2);
+  if (workspace_bytes < lttb_ws(B, n_out, s)) return fail(MM_EWORKSPACE, "workspace too small");
+  LttbArgs la{};
+  la.x = x; la.x_ld = x_ld; la.y = y; la.y_ld = y_ld;
+  la.m_dev = nullptr; la.n = N; la.bounds = nullptr; la.map = nullptr;
+  la.B = B; la.n_out = n_out; la.out = out; la.tables = (unsigned char*)workspace;
+  return launch_lttb(la, x_dtype, y_dtype, s, (cudaStream_t)stream);
+}
+
+int mmlttb_every_nth(int64_t N, int64_t n_out, int64_t* out, void* stream) {
+  if (n_out < 1 || !mul_ok(n_out, N)) return fail(MM_EINVAL, "bad n_out");
+  k_every_nth<<<(unsigned)cdiv(n_out, 256), 256, 0, (cudaStream_t)stream>>>(N, n_out, out);
+  return check_launch("k_every_nth");
+}
+
+int64_t mmlttb_extrema_workspace_bytes(int64_t k, int64_t max_bucket_len) {
+  const ExPlan p = plan_extrema(k * max_bucket_len, max_bucket_len, MM_F64);
+  return up(k * p.C * (int64_t)sizeof(Partial));
+}
+
+int mmlttb_extrema_by_bucket(const void* y, int y_dtype, const int64_t* bounds, int64_t k, int64_t max_bucket_len,
+                             int64_t* out_min, int64_t* out_max, void* workspace, int64_t workspace_bytes,
+                             void* stream) {
+  if (!y || !bounds || !ydt_ok(y_dtype) || k < 1 || max_bucket_len < 1) return fail(MM_EINVAL, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const ExPlan p = plan_extrema(k * max_bucket_len, max_bucket_len, MM_F64);
+  Carve cv{(char*)workspace, workspace_bytes};
+  Partial* part = cv.take<Partial>(k * p.C);
+  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
+  ExArgs ea{y, 0, 1, 0, 1, 1, bounds, 0, k, p.C, p.chunk, part};
+  int rc = launch_extrema(ea, y_dtype, st);
+  if (rc) return rc;
+  k_finalize_extrema<<<(unsigned)cdiv(k, 256), 256, 0, st>>>(part, k, p.C, out_min, out_max);
+  return check_launch("k_finalize_extrema");
+}
+
+int64_t mmlttb_lttb_select_workspace_bytes(int64_t n, int64_t nb) {
+  (void)n;
+  return up((nb - 1) * (int64_t)sizeof(double2));
+}
+
+int mmlttb_lttb_select(const void* xs, int x_dtype, const void* ys, int y_dtype, int64_t n, const int64_t* bounds,
+                       int64_t nb, int64_t* out, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!xs || !ys || !bounds || !xdt_ok(x_dtype) || !ydt_ok(y_dtype) || nb < 2 || n < 2)
+    return fail(MM_EINVAL, "bad arguments");
+  if (workspace_bytes < mmlttb_lttb_select_workspace_bytes(n, nb)) return fail(MM_EWORKSPACE, "workspace too small");
+  LttbArgs la{};
+  la.x = xs; la.y = ys; la.n = n; la.bounds = bounds; la.B = 1; la.n_out = nb + 1; la.out = out;
+  la.tables = (unsigned char*)workspace;
+  // explicit bounds: always the chain pair (bucket sizes are the caller's)
+  return launch_lttb(la, x_dtype, y_dtype, INT64_MAX / 4, (cudaStream_t)stream);
+}
+
+int64_t mmlttb_shard_workspace_bytes(int64_t N, int64_t n_out, int64_t r_ps, int64_t b0, int64_t b1) {
+  const int64_t k = (n_out - 2) * (r_ps / 2);
+  if (k < 1 || b1 <= b0) return ALIGN;
+  const int64_t S = cdiv(N - 2, k);
+  const int64_t lo = 1 + (b0 * (N - 2)) / k, hi = 1 + (b1 * (N - 2)) / k;
+  const ExPlan p = plan_extrema(hi - lo, S, MM_F32);
+  const ExPlan q = plan_extrema(hi - lo, S, MM_F64);
+  return up((b1 - b0) * std::max(p.C, q.C) * (int64_t)sizeof(Partial));
+}
+
+int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard, int y_dtype, int64_t lo, int64_t N,
+                           int64_t n_out, int64_t r_ps, int64_t b0, int64_t b1, int emit_first, int emit_last,
+                           int64_t* out_idx, double* out_x, double* out_y, int64_t* out_count, void* workspace,
+                           int64_t workspace_bytes, void* stream) {
+  int rc = check_common(y_shard, y_dtype, 1, N, n_out);
+  if (rc) return rc;
+  if (!x_shard || !xdt_ok(x_dtype)) return fail(MM_EINVAL, "x missing or bad dtype");
+  if (r_ps < 2 || r_ps % 2) return fail(MM_EINVAL, "r_ps must be even >= 2");
+  const int64_t k = (n_out - 2) * (r_ps / 2);
+  if (k > N - 2 || b0 < 0 || b1 > k || b1 < b0) return fail(MM_EINVAL, "bad bucket range");
+  if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nb = b1 - b0;
+  const int64_t S = cdiv(N - 2, k);
+  const int64_t elo = 1 + (b0 * (N - 2)) / k, ehi = 1 + (b1 * (N - 2)) / k;
+  const ExPlan p = plan_extrema(ehi - elo, S, y_dtype);
+  Carve cv{(char*)workspace, workspace_bytes};
+  Partial* part = cv.take<Partial>(std::max<int64_t>(nb, 1) * p.C);
+  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
+  // virtual base: element i of the global series lives at y_shard[i - lo]
+  const void* ybase = (const char*)y_shard - lo * esize(y_dtype);
+  if (nb > 0) {
+    ExArgs ea{ybase, 0, 1, 1, N - 2, k, nullptr, b0, nb, p.C, p.chunk, part};
+    if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
+  }
+  CompactArgs ca{};
+  ca.part = part; ca.nb = nb; ca.C = p.C; ca.mode = 0;
+  ca.emit_first = emit_first ? 0 : -1; ca.emit_last = emit_last ? N - 1 : -1;
+  ca.force_n_out = 0; ca.last_index = N - 1;
+  ca.start = 1; ca.len = N - 2; ca.k = k; ca.b0 = b0;
+  ca.out_idx = out_idx; ca.out_ld = 0; ca.out_count = out_count;
+  ca.x = x_shard; ca.xdt = x_dtype; ca.x_ld = 0; ca.x_off = lo;
+  ca.y = y_shard; ca.ydt = y_dtype; ca.y_ld = 0; ca.y_off = lo;
+  ca.out_x = out_x; ca.out_y = out_y;
+  k_compact<512><<<1, 512, 0, st>>>(ca);
+  return check_launch("k_compact(shard)");
+}
+
+int mmlttb_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts, int64_t G,
+                        int64_t cap, int64_t* out_idx, double* out_x, double* out_y, int64_t* out_m, void* stream) {
+  if (G < 1 || cap < 1) return fail(MM_EINVAL, "bad arguments");
+  k_merge_shards<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>(idx, xs, ys, counts, G, cap, out_idx, out_x, out_y,
+                                                                 out_m);
+  return check_launch("k_merge_shards");
+}
+
+int64_t mmlttb_lttb_preselected_workspace_bytes(int64_t B, int64_t n_out, int64_t r_ps) {
+  return lttb_ws(B, n_out, r_ps);
+}
+
+int mmlttb_lttb_preselected(const int64_t* pre_idx, const double* pre_x, const double* pre_y, const int64_t* m,
+                            int64_t B, int64_t ld, int64_t n_out, int64_t r_ps, int64_t* out, void* workspace,
+                            int64_t workspace_bytes, void* stream) {
+  if (!pre_idx || !pre_x || !pre_y || !m || B < 1 || n_out < 3 || r_ps < 1) return fail(MM_EINVAL, "bad arguments");
+  if (workspace_bytes < lttb_ws(B, n_out, r_ps)) return fail(MM_EWORKSPACE, "workspace too small");
+  LttbArgs la{};
+  la.x = pre_x; la.x_ld = ld; la.y = pre_y; la.y_ld = ld;
+  la.m_dev = m; la.map = pre_idx; la.map_ld = ld;
+  la.B = B; la.n_out = n_out; la.out = out; la.tables = (unsigned char*)workspace;
+  return launch_lttb(la, MM_F64, MM_F64, r_ps, (cudaStream_t)stream);
+}
+
+int mmlttb_validate(const void* x, int x_dtype, const void* y, int y_dtype, int64_t N, int32_t* flags, void* stream) {
+  if (!x || !y || !flags || N < 1 || !xdt_ok(x_dtype) || !ydt_ok(y_dtype)) return fail(MM_EINVAL, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(flags, 0, sizeof(int32_t), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(N, 256), 148 * 16);
+#define MM_V(XT, YT) k_validate<XT, YT><<<blocks, 256, 0, st>>>((const XT*)x, (const YT*)y, N, (int*)flags)
+  if (y_dtype == MM_F32) {
+    switch (x_dtype) {
+      case MM_F32: MM_V(float, float); break;
+      case MM_F64: MM_V(double, float); break;
+      case MM_I64: MM_V(long long, float); break;
+      default: MM_V(int, float); break;
+    }
+  } else {
+    switch (x_dtype) {
+      case MM_F32: MM_V(float, double); break;
+      case MM_F64: MM_V(double, double); break;
+      case MM_I64: MM_V(long long, double); break;
+      default: MM_V(int, double); break;
+    }
+  }
+#undef MM_V
+  return check_launch("k_validate");
+}
+
+}  // extern "C"

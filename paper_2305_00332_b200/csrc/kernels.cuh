@@ -1,0 +1,620 @@
+// kernels.cuh -- sm_100a device code for the MinMaxLTTB path.
+//
+// K1  k_extrema        streaming first-occurrence argmin/argmax per
+//                      (series, sub-bucket, chunk): _kernels.py:22-78
+// K2  k_compact        per-series combine of K1 partials, (lo,hi) emission
+//                      with dedup, endpoints, exclusive scan, gather of the
+//                      preselected (x,y) as f64: downsamplers.py:60-69,
+//                      135-161, 164-179, 95-112; core.py:103-105
+// K3a k_lttb_tables +  LTTB over small buckets as transition tables
+//     k_lttb_jump      T_b[p] = argmax_j area(P_p, P_j, C_{b+1}) built in
+//                      parallel, the bucket chain resolved by pointer
+//                      jumping in shared memory: _kernels.py:81-119
+// K3b k_lttb_means +   LTTB over large buckets: parallel in-order means,
+//     k_lttb_chain     then one CTA walks the chain, threads evaluating the
+//                      bucket's triangle areas: _kernels.py:81-119
+//
+// Arithmetic parity: extrema compare IEEE total-order
+// integer keys (-0.0 < +0.0; f32 keys order exactly like the f64 keys the
+// reference builds); LTTB is strict IEEE fp64 through __dadd_rn / __dsub_rn /
+// __dmul_rn / __ddiv_rn (never contracted to FMA), bucket sums in index
+// order, strict '>' with lowest index on ties and NaN never winning.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mm {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- keys ----
+// _kernels.py:22-25 restated for the storage width: bits ^ ((bits>>63)&MAG).
+// `b` must be SIGNED so that >> is arithmetic (SURVEY §7 hard part 2).
+__device__ __forceinline__ int32_t key32(uint32_t u) {
+  const int32_t b = (int32_t)u;
+  return b ^ ((b >> 31) & 0x7fffffff);
+}
+__device__ __forceinline__ long long key64(unsigned long long u) {
+  const long long b = (long long)u;
+  return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <typename T> struct YTr;
+template <> struct YTr<float> {
+  typedef int32_t K;
+  static constexpr int VEC = 4;
+  static __device__ __forceinline__ K kmax() { return 0x7fffffff; }
+  static __device__ __forceinline__ K kmin() { return (K)0x80000000; }
+  static __device__ __forceinline__ K key(const float* p) { return key32(__float_as_uint(__ldg(p))); }
+  static __device__ __forceinline__ void keys(const uint4& v, K* k) {
+    k[0] = key32(v.x); k[1] = key32(v.y); k[2] = key32(v.z); k[3] = key32(v.w);
+  }
+};
+template <> struct YTr<double> {
+  typedef long long K;
+  static constexpr int VEC = 2;
+  static __device__ __forceinline__ K kmax() { return 0x7fffffffffffffffLL; }
+  static __device__ __forceinline__ K kmin() { return (K)0x8000000000000000ULL; }
+  static __device__ __forceinline__ K key(const double* p) {
+    return key64((unsigned long long)__double_as_longlong(__ldg(p)));
+  }
+  static __device__ __forceinline__ void keys(const uint4& v, K* k) {
+    k[0] = key64(((unsigned long long)v.y << 32) | v.x);
+    k[1] = key64(((unsigned long long)v.w << 32) | v.z);
+  }
+};
+
+// element -> f64 exactly as np.array(values, dtype=float64) (core.py:49)
+template <typename T> __device__ __forceinline__ double to_f64(const T* p, int64_t i);
+template <> __device__ __forceinline__ double to_f64<float>(const float* p, int64_t i) { return (double)__ldg(p + i); }
+template <> __device__ __forceinline__ double to_f64<double>(const double* p, int64_t i) { return __ldg(p + i); }
+template <> __device__ __forceinline__ double to_f64<long long>(const long long* p, int64_t i) {
+  return __ll2double_rn(__ldg(p + i));
+}
+template <> __device__ __forceinline__ double to_f64<int>(const int* p, int64_t i) { return (double)__ldg(p + i); }
+
+// ------------------------------------------------------- K1 partials ----
+struct Partial {
+  long long kmin, kmax;  // total-order keys (sign-extended for f32)
+  long long imin, imax;  // element index (INT64_MAX = none)
+};
+
+struct ExArgs {
+  const void* y;
+  int64_t y_ld;
+  int64_t B;
+  int64_t start, len, k;   // closed-form partition(start, start+len, k) (core.py:173)
+  const int64_t* bounds;   // or explicit bounds (k+1 entries), shared by all series
+  int64_t b0, nb;          // buckets [b0, b0+nb) of every series
+  int64_t C, chunk;        // chunks per bucket, chunk length (elements)
+  Partial* part;           // [B][nb][C]
+};
+
+__device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k, int64_t b) {
+  return start + (b * len) / k;  // core.py:173 (host guarantees k*len < 2^63)
+}
+
+// One warp per (series, bucket, chunk).  Lanes stream 16-byte vectors
+// (U in flight per lane), keep a per-lane running min/max KEY plus the
+// position of the vector that first reached it (strict < / >, lane order is
+// index order => lane-local first occurrence), recover the exact element
+// from that vector at the end, then reduce (key, index) lexicographically
+// across the warp -- the same first-occurrence argmin/argmax as
+// _argminmax_range (_kernels.py:28-60) independent of evaluation order.
+template <typename T, int U>
+__global__ void __launch_bounds__(256) k_extrema(ExArgs a) {
+  typedef YTr<T> Tr;
+  typedef typename Tr::K K;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t total = a.B * a.nb * a.C;
+  if (w >= total) return;  // warp-uniform
+  const int64_t c = w % a.C;
+  const int64_t t = w / a.C;
+  const int64_t b = a.b0 + t % a.nb;
+  const int64_t s = t / a.nb;
+  int64_t blo, bhi;
+  if (a.bounds) {
+    blo = a.bounds[b];
+    bhi = a.bounds[b + 1];
+  } else {
+    blo = pbound(a.start, a.len, a.k, b);
+    bhi = pbound(a.start, a.len, a.k, b + 1);
+  }
+  const int64_t lo = blo + c * a.chunk;
+  const int64_t hi = min(bhi, lo + a.chunk);
+  const T* y = (const T*)a.y + s * a.y_ld;
+
+  K mn = Tr::kmax(), mx = Tr::kmin();
+  int64_t pmn = INT64_MAX, pmx = INT64_MAX;
+  bool vmn = false, vmx = false;
+  if (lo < hi) {
+    const int n = (int)(hi - lo);
+    const uintptr_t addr = (uintptr_t)(y + lo);
+    int head = (int)(((16u - (unsigned)(addr & 15u)) & 15u) / sizeof(T));
+    if (head > n) head = n;
+    if (lane < head) {
+      const K kk = Tr::key(y + lo + lane);
+      mn = kk; mx = kk; pmn = pmx = lo + lane;
+    }
+    const int64_t vstart = lo + head;
+    const int nvec = (n - head) / Tr::VEC;
+    const uint4* vp = reinterpret_cast<const uint4*>(y + vstart);
+    for (int v0 = 0; v0 < nvec; v0 += 32 * U) {
+      uint4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nvec) r[u] = ld_stream(vp + v);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nvec) {
+          K kk[Tr::VEC];
+          Tr::keys(r[u], kk);
+          K vl = kk[0], vh = kk[0];
+#pragma unroll
+          for (int e = 1; e < Tr::VEC; ++e) { vl = min(vl, kk[e]); vh = max(vh, kk[e]); }
+          if (vl < mn) { mn = vl; pmn = vstart + (int64_t)v * Tr::VEC; vmn = true; }
+          if (vh > mx) { mx = vh; pmx = vstart + (int64_t)v * Tr::VEC; vmx = true; }
+        }
+      }
+    }
+    const int64_t tp = vstart + (int64_t)nvec * Tr::VEC + lane;
+    if (tp < hi) {
+      const K kk = Tr::key(y + tp);
+      if (kk < mn) { mn = kk; pmn = tp; vmn = false; }
+      if (kk > mx) { mx = kk; pmx = tp; vmx = false; }
+    }
+    // exact element inside the winning vector: first component with the key
+    if (vmn) {
+      K kk[Tr::VEC];
+      Tr::keys(__ldg(reinterpret_cast<const uint4*>(y + pmn)), kk);
+      int e = Tr::VEC - 1;
+#pragma unroll
+      for (int q = Tr::VEC - 1; q >= 0; --q) if (kk[q] == mn) e = q;
+      pmn += e;
+    }
+    if (vmx) {
+      K kk[Tr::VEC];
+      Tr::keys(__ldg(reinterpret_cast<const uint4*>(y + pmx)), kk);
+      int e = Tr::VEC - 1;
+#pragma unroll
+      for (int q = Tr::VEC - 1; q >= 0; --q) if (kk[q] == mx) e = q;
+      pmx += e;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const K omn = __shfl_xor_sync(FULL, mn, off);
+    const int64_t opmn = __shfl_xor_sync(FULL, pmn, off);
+    if (omn < mn || (omn == mn && opmn < pmn)) { mn = omn; pmn = opmn; }
+    const K omx = __shfl_xor_sync(FULL, mx, off);
+    const int64_t opmx = __shfl_xor_sync(FULL, pmx, off);
+    if (omx > mx || (omx == mx && opmx < pmx)) { mx = omx; pmx = opmx; }
+  }
+  if (lane == 0) {
+    Partial p;
+    p.kmin = (long long)mn; p.kmax = (long long)mx; p.imin = pmn; p.imax = pmx;
+    a.part[w] = p;
+  }
+}
+
+// combine the C chunk partials of one bucket (lexicographic, order-free)
+__device__ __forceinline__ void combine(const Partial* p, int64_t C, int64_t& imin, int64_t& imax) {
+  Partial r = p[0];
+  for (int64_t c = 1; c < C; ++c) {
+    const Partial q = p[c];
+    if (q.kmin < r.kmin || (q.kmin == r.kmin && q.imin < r.imin)) { r.kmin = q.kmin; r.imin = q.imin; }
+    if (q.kmax > r.kmax || (q.kmax == r.kmax && q.imax < r.imax)) { r.kmax = q.kmax; r.imax = q.imax; }
+  }
+  imin = r.imin;
+  imax = r.imax;
+}
+
+// ---------------------------------------------------- block scan helper --
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int& total, int* sh /* >= NT/32+1 ints */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < NT / 32 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < NT / 32) sh[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const int before = wid ? sh[wid - 1] : 0;
+  total = sh[NT / 32 - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+// ---------------------------------------------------------- K2 compact ---
+struct CompactArgs {
+  const Partial* part;
+  int64_t nb, C;            // per series: nb buckets x C chunks
+  int mode;                 // 0: minmax pairs, 1: m4 quads
+  int64_t emit_first;       // index emitted before everything (-1: none)
+  int64_t emit_last;        // index emitted after everything (-1: none)
+  int64_t force_n_out;      // > 0: _minmax_with_endpoints (downsamplers.py:164-179)
+  int64_t last_index;       // N-1 for force mode
+  int64_t start, len, k, b0;  // bucket bounds (m4 first/last)
+  int64_t* out_idx;
+  int64_t out_ld;
+  int64_t* out_count;
+  const void* x; int xdt; int64_t x_ld; int64_t x_off;  // gather x[i - x_off] (x may be null)
+  const void* y; int ydt; int64_t y_ld; int64_t y_off;
+  double* out_x;            // may be null
+  double* out_y;
+};
+
+__device__ __forceinline__ double load_any(const void* p, int dt, int64_t i) {
+  switch (dt) {
+    case 0: return (double)__ldg((const float*)p + i);
+    case 1: return __ldg((const double*)p + i);
+    case 2: return __ll2double_rn(__ldg((const long long*)p + i));
+    default: return (double)__ldg((const int*)p + i);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_compact(CompactArgs a) {
+  __shared__ int sh[NT / 32 + 1];
+  __shared__ long long s_first, s_last, s_m;
+  const int64_t s = blockIdx.x;
+  const Partial* part = a.part + s * a.nb * a.C;
+  int64_t* out = a.out_idx + s * a.out_ld;
+  double* ox = a.out_x ? a.out_x + s * a.out_ld : nullptr;
+  double* oy = a.out_y ? a.out_y + s * a.out_ld : nullptr;
+  const void* xs = a.x ? (const void*)((const char*)a.x + s * a.x_ld * (a.xdt == 0 || a.xdt == 3 ? 4 : 8)) : nullptr;
+  const void* ys = a.y ? (const void*)((const char*)a.y + s * a.y_ld * (a.ydt == 0 || a.ydt == 3 ? 4 : 8)) : nullptr;
+
+  auto put = [&](int64_t pos, int64_t idx) {
+    out[pos] = idx;
+    if (ox) ox[pos] = load_any(xs, a.xdt, idx - a.x_off);
+    if (oy) oy[pos] = load_any(ys, a.ydt, idx - a.y_off);
+  };
+  auto items_of = [&](int64_t bl, int64_t* it) -> int {
+    int64_t imin, imax;
+    combine(part + bl * a.C, a.C, imin, imax);
+    const int64_t lo = min(imin, imax), hi = max(imin, imax);
+    if (a.mode == 0) {  // downsamplers.py:60-69
+      it[0] = lo; it[1] = hi;
+      return hi != lo ? 2 : 1;
+    }
+    // m4: {first, argmin, argmax, last} sorted, adjacent duplicates dropped (:95-112)
+    const int64_t b = a.b0 + bl;
+    int64_t q[4] = {pbound(a.start, a.len, a.k, b), lo, hi, pbound(a.start, a.len, a.k, b + 1) - 1};
+    // q[0] <= lo <= hi <= q[3] already (extrema lie inside the bucket)
+    int n = 0;
+    it[n++] = q[0];
+#pragma unroll
+    for (int i = 1; i < 4; ++i) if (q[i] != q[i - 1]) it[n++] = q[i];
+    return n;
+  };
+
+  // r_ps == 1 endpoint forcing needs the count before placement
+  int prepend = 0, replace_first = 0, append = 0, replace_last = 0;
+  int64_t m_total = 0;
+  if (a.force_n_out > 0) {
+    int64_t acc = 0;
+    for (int64_t t0 = 0; t0 < a.nb; t0 += NT) {
+      const int64_t bl = t0 + threadIdx.x;
+      int cnt = 0;
+      if (bl < a.nb) { int64_t it[4]; cnt = items_of(bl, it); }
+      int tot;
+      block_excl_scan<NT>(cnt, tot, sh);
+      acc += tot;
+    }
+    if (threadIdx.x == 0) {
+      int64_t it[4];
+      items_of(0, it);
+      s_first = it[0];
+      const int n = items_of(a.nb - 1, it);
+      s_last = it[n - 1];
+      s_m = acc;
+    }
+    __syncthreads();
+    m_total = s_m;
+    if (s_first != 0) { if (m_total < a.force_n_out) prepend = 1; else replace_first = 1; }
+    if (s_last != a.last_index) {
+      if (m_total + prepend < a.force_n_out) append = 1; else replace_last = 1;
+    }
+  }
+
+  int64_t carry = (a.emit_first >= 0 ? 1 : 0) + prepend;
+  for (int64_t t0 = 0; t0 < a.nb; t0 += NT) {
+    const int64_t bl = t0 + threadIdx.x;
+    int64_t it[4];
+    int cnt = 0;
+    if (bl < a.nb) cnt = items_of(bl, it);
+    int tot;
+    const int ex = block_excl_scan<NT>(cnt, tot, sh);
+    for (int i = 0; i < cnt; ++i) put(carry + ex + i, it[i]);
+    carry += tot;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (a.emit_first >= 0) put(0, a.emit_first);
+    if (a.emit_last >= 0) put(carry++, a.emit_last);
+    if (prepend || replace_first) put(0, 0);
+    if (append) put(carry++, a.last_index);
+    if (replace_last) put(carry - 1, a.last_index);
+    a.out_count[s] = carry;
+  }
+}
+
+// extrema-only finalize for the _extrema_by_bucket entry point
+__global__ void k_finalize_extrema(const Partial* part, int64_t k, int64_t C, int64_t* out_min, int64_t* out_max) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= k) return;
+  int64_t a, c;
+  combine(part + b * C, C, a, c);
+  out_min[b] = a;
+  out_max[b] = c;
+}
+
+// -------------------------------------------------------------- LTTB -----
+// Points of series s: x/y typed (XT/YT), count m (device per series or
+// fixed), optional map position -> output index (the preselected indices).
+struct LttbArgs {
+  const void* x; int64_t x_ld;
+  const void* y; int64_t y_ld;
+  const int64_t* m_dev; int64_t n;   // m_dev ? m_dev[s] : n
+  const int64_t* bounds;             // explicit LTTB bounds (B == 1 only) or null
+  const int64_t* map; int64_t map_ld;
+  int64_t B, n_out;
+  int64_t* out;                      // [B][n_out]
+  unsigned char* tables; int64_t tab_ld;  // K3a: [B][k3*SMAX]
+  double2* means; int64_t means_ld;       // K3b: [B][k3]
+};
+
+__device__ __forceinline__ double lttb_area(double ax, double ay, double cx, double cy, double xj, double yj) {
+  // _kernels.py:114: abs((ax - cx) * (ys[j] - ay) - (ax - xs[j]) * (cy - ay)), every op rounded
+  return fabs(__dsub_rn(__dmul_rn(__dsub_rn(ax, cx), __dsub_rn(yj, ay)),
+                        __dmul_rn(__dsub_rn(ax, xj), __dsub_rn(cy, ay))));
+}
+
+__device__ __forceinline__ int64_t lbound(const LttbArgs& a, int64_t m, int64_t b) {
+  if (a.bounds) return a.bounds[b];
+  return 1 + (b * (m - 2)) / (a.n_out - 2);  // partition(1, m-1, n_out-2), downsamplers.py:129
+}
+
+// mean point of bucket b+1 (in-order fp64 sums, _kernels.py:95-104), or the
+// last point for the final bucket (:105-107)
+template <typename XT, typename YT>
+__device__ __forceinline__ double2 lttb_next_mean(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b) {
+  const int64_t k3 = a.n_out - 2;
+  double2 c;
+  if (b + 1 < k3) {
+    const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
+    double sx = 0.0, sy = 0.0;
+    for (int64_t j = nlo; j < nhi; ++j) {
+      sx = __dadd_rn(sx, to_f64(xs, j));
+      sy = __dadd_rn(sy, to_f64(ys, j));
+    }
+    const double cnt = (double)(nhi - nlo);
+    c.x = __ddiv_rn(sx, cnt);
+    c.y = __ddiv_rn(sy, cnt);
+  } else {
+    c.x = to_f64(xs, m - 1);
+    c.y = to_f64(ys, m - 1);
+  }
+  return c;
+}
+
+// K3a, part 1: T_b[p] for every bucket b and every predecessor candidate p
+// (bucket b-1's points; bucket 0's only predecessor is point 0).
+// Block = NBB consecutive buckets of one series.
+template <typename XT, typename YT, int SMAX, int NBB>
+__global__ void __launch_bounds__(NBB * SMAX < 1024 ? NBB * SMAX : 1024) k_lttb_tables(LttbArgs a) {
+  __shared__ double2 s_mean[NBB];
+  __shared__ int64_t s_bnd[NBB + 2];
+  const int64_t s = blockIdx.y;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t bb = (int64_t)blockIdx.x * NBB;
+  if (bb >= k3) return;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int nbk = (int)(k3 - bb < NBB ? k3 - bb : (int64_t)NBB);
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x) s_mean[i] = lttb_next_mean(a, xs, ys, m, bb + i);
+  for (int i = threadIdx.x; i <= nbk; i += blockDim.x) s_bnd[i + 1] = lbound(a, m, bb + i);
+  if (threadIdx.x == 0) s_bnd[0] = bb > 0 ? lbound(a, m, bb - 1) : 0;
+  __syncthreads();
+  unsigned char* tab = a.tables + s * a.tab_ld + bb * SMAX;
+  for (int it = threadIdx.x; it < nbk * SMAX; it += blockDim.x) {
+    const int bi = it / SMAX, p = it % SMAX;
+    const int64_t b = bb + bi;
+    const int64_t blo = s_bnd[bi + 1], bhi = s_bnd[bi + 2];
+    int64_t ap;
+    bool valid;
+    if (b == 0) { valid = (p == 0); ap = 0; }
+    else { const int64_t plo = s_bnd[bi]; valid = p < s_bnd[bi + 1] - plo; ap = plo + p; }
+    unsigned char r = 0;
+    if (valid) {
+      const double ax = to_f64(xs, ap), ay = to_f64(ys, ap);
+      const double2 c = s_mean[bi];
+      double best = -1.0;
+      for (int64_t j = blo; j < bhi; ++j) {
+        const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+        if (ar > best) { best = ar; r = (unsigned char)(j - blo); }  // strict '>' (:115)
+      }
+    }
+    tab[it] = r;
+  }
+}
+
+// K3a, part 2: one CTA per series loads its tables into shared memory and
+// composes them by pointer jumping: after level w, G_b maps bucket
+// (b-w)'s points to bucket b; ceil(log2 k3) levels leave G_b[0] = the LTTB
+// pick of bucket b (the chain out[b+1] = T_b[out[b]] of :108-119).
+template <int SMAX>
+__global__ void __launch_bounds__(1024) k_lttb_jump(LttbArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int64_t s = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const int64_t nent = k3 * SMAX;
+  unsigned char* A = sm;
+  unsigned char* Bf = sm + ((nent + 15) & ~(int64_t)15);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.tables + s * a.tab_ld);
+    uint4* dst = reinterpret_cast<uint4*>(A);
+    const int64_t nv = (nent + 15) / 16;
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  for (int64_t w = 1; w < k3; w <<= 1) {
+    for (int64_t it = threadIdx.x; it < nent; it += blockDim.x) {
+      const int64_t b = it / SMAX;
+      const int p = (int)(it % SMAX);
+      unsigned char v = A[it];
+      if (b >= w) v = A[b * SMAX + A[(b - w) * SMAX + p]];
+      Bf[it] = v;
+    }
+    __syncthreads();
+    unsigned char* t = A; A = Bf; Bf = t;
+  }
+  int64_t* out = a.out + s * a.n_out;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  for (int64_t b = threadIdx.x; b < k3; b += blockDim.x) {
+    const int64_t pos = lbound(a, m, b) + A[b * SMAX];
+    out[b + 1] = map ? map[pos] : pos;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = map ? map[0] : 0;
+    out[k3 + 1] = map ? map[m - 1] : m - 1;
+  }
+}
+
+// K3b, part 1: next-bucket means for every (series, bucket), one thread each.
+template <typename XT, typename YT>
+__global__ void k_lttb_means(LttbArgs a) {
+  const int64_t k3 = a.n_out - 2;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.B * k3) return;
+  const int64_t s = g / k3, b = g % k3;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  a.means[s * a.means_ld + b] =
+      lttb_next_mean(a, (const XT*)a.x + s * a.x_ld, (const YT*)a.y + s * a.y_ld, m, b);
+}
+
+// K3b, part 2: one CTA per series carries the bucket-to-bucket dependency.
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
+  __shared__ double s_area[NT / 32];
+  __shared__ long long s_idx[NT / 32];
+  __shared__ long long s_prev;
+  const int64_t s = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const double2* means = a.means + s * a.means_ld;
+  int64_t* out = a.out + s * a.n_out;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t prev = 0;
+  int64_t blo = lbound(a, m, 0);
+  for (int64_t b = 0; b < k3; ++b) {
+    const int64_t bhi = lbound(a, m, b + 1);
+    const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
+    const double2 c = means[b];
+    double best = -1.0;
+    long long bi = INT64_MAX;
+    for (int64_t j = blo + threadIdx.x; j < bhi; j += NT) {
+      const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+      if (ar > best) { best = ar; bi = j; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double oa = __shfl_xor_sync(FULL, best, o);
+      const long long oi = __shfl_xor_sync(FULL, bi, o);
+      if (oa > best || (oa == best && oi < bi)) { best = oa; bi = oi; }
+    }
+    if (lane == 0) { s_area[wid] = best; s_idx[wid] = bi; }
+    __syncthreads();
+    if (wid == 0) {
+      best = lane < NT / 32 ? s_area[lane] : -1.0;
+      bi = lane < NT / 32 ? s_idx[lane] : INT64_MAX;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double oa = __shfl_xor_sync(FULL, best, o);
+        const long long oi = __shfl_xor_sync(FULL, bi, o);
+        if (oa > best || (oa == best && oi < bi)) { best = oa; bi = oi; }
+      }
+      if (lane == 0) {
+        const int64_t sel = bi == INT64_MAX ? blo : bi;  // all-NaN bucket keeps bounds[b] (:110)
+        out[b + 1] = map ? map[sel] : sel;
+        s_prev = sel;
+      }
+    }
+    __syncthreads();
+    prev = s_prev;
+    blo = bhi;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = map ? map[0] : 0;
+    out[k3 + 1] = map ? map[m - 1] : m - 1;
+  }
+}
+
+// ----------------------------------------------------------- misc -------
+__global__ void k_fill(int64_t* p, int64_t n, int64_t v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void k_every_nth(int64_t n, int64_t n_out, int64_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_out) out[i] = (i * n) / n_out;  // downsamplers.py:44-47
+}
+
+template <typename XT, typename YT>
+__global__ void k_validate(const XT* x, const YT* y, int64_t n, int* flags) {
+  int f = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double xv = to_f64(x, i), yv = to_f64(y, i);
+    if (!isfinite(xv) || !isfinite(yv)) f |= 1;  // core.py:89-90
+    if (i + 1 < n && to_f64(x, i + 1) < xv) f |= 2;  // core.py:91-92
+  }
+  f = __reduce_or_sync(FULL, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+__global__ void k_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts,
+                               int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy, int64_t* om) {
+  const int64_t g = blockIdx.x;
+  int64_t off = 0;
+  for (int64_t h = 0; h < g; ++h) off += counts[h];
+  const int64_t n = counts[g];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    oi[off + i] = idx[g * cap + i];
+    ox[off + i] = xs[g * cap + i];
+    oy[off + i] = ys[g * cap + i];
+  }
+  if (g == G - 1 && threadIdx.x == 0) om[0] = off + n;
+}
+
+}  // namespace mm
