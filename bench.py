@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""MinMaxLTTB throughput on B200: input points/s, HBM GB/s and % of roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3_1e9|c1|c2|c3|c4|c5] [--impl ours|reference]
+
+A step = one minmaxlttb call (K1 extrema -> K2 compact -> K3 LTTB) over the
+workload's series.  Default workload "c3_1e9": BASELINE.json C3's recipe at
+N = 1e9 points (float32 y = 3 sinusoids + N(0,1), int64 x, n_out = 2000,
+minmax_ratio = 4) -- the north star's "10^9-point series".
+Inputs are generated ON the device (torch Philox, seed 3; a 4 GB float32 y
+is larger than the 126 MB L2, so consecutive steps never hit in L2) and the
+warm-up output is checked index-exactly against the CPU oracle on the same
+data.  Under torchrun every rank runs its own independent series (batch
+sharding, no collective): "scaling": "weak".
+
+--impl reference times the reference algorithm's CPU restatement
+(oracle/, OpenMP over all host threads, float64 inputs as tsdown.TimeSeries
+holds them) on a bounded prefix sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (N per series, batch, n_out, r_ps, y dtype, x dtype, op)
+    "c3_1e9": (1_000_000_000, 1, 2000, 4, "f32", "i64", "minmaxlttb"),
+    "c1": (1_000_000, 1, 1000, 4, "f64", "i64", "minmaxlttb"),
+    "c2": (10_000_000, 1, 2000, 0, "f64", "i64", "lttb"),
+    "c3": (100_000_000, 1, 2000, 4, "f32", "i64", "minmaxlttb"),
+    "c4": (1_000_000, 4096, 1000, 4, "f32", "i64", "minmaxlttb"),
+    "c5": (2_000_000_000, 1, 4000, 4, "f32", "f64", "minmaxlttb"),
+}
+METRIC = "MinMaxLTTB input points/sec and HBM GB/s (% roofline) at 1/2/4/8 B200"
+UNIT = "points/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic():
+    p = ROOT / "profiles" / "k1_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return None
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampling during a timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+        self.rows = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        for line in out.splitlines():
+            f = [t.strip() for t in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append(f)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------- inputs ---
+def make_inputs(name, dev, seed):
+    """Device-side generation of the workload (torch Philox streams)."""
+    import torch
+
+    n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
+    g = torch.Generator(device=dev).manual_seed(seed)
+    ytype = torch.float32 if ydt == "f32" else torch.float64
+    y = torch.empty((batch, n), dtype=ytype, device=dev)
+    chunk = 1 << 26
+    for b in range(batch):
+        for lo in range(0, n, chunk):
+            hi = min(n, lo + chunk)
+            if name.startswith("c3"):
+                i = torch.arange(lo, hi, device=dev, dtype=torch.float64)
+                v = torch.sin(2 * np.pi * i / 1e3) + torch.sin(2 * np.pi * i / 1e5) + torch.sin(2 * np.pi * i / 1e7)
+                v += torch.randn(hi - lo, device=dev, dtype=torch.float64, generator=g)
+                y[b, lo:hi] = v
+            else:  # random walks (+ spikes for c2/c5)
+                v = torch.randn(hi - lo, device=dev, dtype=torch.float64, generator=g)
+                y[b, lo:hi] = v
+        if not name.startswith("c3"):
+            w = torch.cumsum(y[b].to(torch.float64), 0)
+            if name in ("c2", "c5"):
+                frac = 0.001 if name == "c2" else 0.01
+                sig = 0.5 if name == "c2" else 1.0
+                spike = torch.rand(n, device=dev, generator=g) < frac
+                sign = torch.where(torch.rand(n, device=dev, generator=g) < 0.5, -1.0, 1.0).to(torch.float64)
+                w += torch.where(spike, sign * 50.0 * sig, torch.zeros((), dtype=torch.float64, device=dev))
+            y[b] = w.to(ytype)
+    if xdt == "i64":
+        x = torch.arange(n, dtype=torch.int64, device=dev)
+    else:
+        x = torch.cumsum(torch.empty(n, dtype=torch.float64, device=dev).exponential_(1.0, generator=g), 0)
+    return x, (y[0] if batch == 1 else y)
+
+
+# ------------------------------------------------------------- CPU legs -----
+def build_sample(name, max_points=100_000_000, threads=0):
+    """The reference algorithm's CPU restatement on a bounded sample.
+
+    Sample: the first min(N, max_points) points of one series of the workload
+    (same recipe, numpy-generated, float64 as tsdown.TimeSeries stores it --
+    the f64 conversion is outside the timed region, as in the reference's
+    bench.py:124-127), same r_ps, n_out scaled so sub-buckets keep the
+    workload's size, OpenMP over `threads` host threads (prange analogue).
+    """
+    from oracle import oracle as O
+
+    n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
+    m = min(n, max_points)
+    rng = np.random.Generator(np.random.PCG64(3))
+    i = np.arange(m, dtype=np.float64)
+    if name.startswith("c3"):
+        y = np.sin(2 * np.pi * i / 1e3) + np.sin(2 * np.pi * i / 1e5) + np.sin(2 * np.pi * i / 1e7)
+        y += rng.standard_normal(m)
+        y = y.astype(np.float32).astype(np.float64)
+    else:
+        y = np.cumsum(rng.standard_normal(m))
+        if ydt == "f32":
+            y = y.astype(np.float32).astype(np.float64)
+    x = np.cumsum(rng.exponential(1.0, m)) if xdt == "f64" else i
+    threads = threads or O.max_threads()
+    n_out_s = n_out if m == n else max(3, int(round((n_out - 2) * m / n)) + 2)
+    if op == "lttb":
+        fn = lambda: O.lttb(x, y, n_out_s)  # noqa: E731  (sequential by contract)
+        cores = 1
+    else:
+        fn = lambda: O.minmaxlttb(x, y, n_out_s, r_ps, threads)  # noqa: E731
+        cores = threads
+    desc = (f"{name}: first {m:.3g} points of one series, n_out={n_out_s}, r_ps={r_ps}, {op} on f64 "
+            f"(TimeSeries layout), {cores} thread(s) of {os.cpu_count()} host CPUs")
+    return fn, m, desc, cores
+
+
+def cpu_sample(name, seconds=12.0):
+    fn, m, desc, cores = build_sample(name)
+    fn()  # warm
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 500:
+            break
+    med = statistics.median(times)
+    return {"value": m / med, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": desc + f", median of {len(times)} runs", "ms_per_sample": med * 1e3}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    name = args.workload
+    n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
+    fn, m, desc, cores = build_sample(name)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = m * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "n": n, "batch": batch, "n_out": n_out, "minmax_ratio": r_ps, "op": op},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- GPU leg ------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_00332_b200 as mm
+    from paper_2305_00332_b200 import _native as NAT
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    name = args.workload
+    n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
+    scaling = "weak"
+    if name == "c4" and ws > 1:  # C4: 4096 series sharded across ranks (strong)
+        per = batch // ws
+        batch = per
+        scaling = "strong"
+    x, y = make_inputs(name, dev, seed=3 + rank)
+    if name == "c4" and ws > 1:
+        y = y[:batch].contiguous()
+    L = NAT.lib()
+    torch.cuda.synchronize()
+
+    def step(xx, yy):
+        if op == "lttb":
+            return mm.lttb(xx, yy, n_out)
+        return mm.minmaxlttb(xx, yy, n_out, minmax_ratio=r_ps)
+
+    # warm-up + parity of the warm-up output against the oracle (rank 0)
+    out = step(x, y)
+    torch.cuda.synchronize()
+    parity = "unchecked"
+    if rank == 0 and not args.no_check:
+        from oracle import oracle as O
+
+        xh = x.cpu().numpy()
+        yh = (y if y.dim() == 1 else y[0]).cpu().numpy()
+        o = (out if out.dim() == 1 else out[0]).cpu().numpy()
+        if op == "lttb":
+            want = O.lttb(xh, yh, n_out)
+        else:
+            want = O.minmaxlttb_typed(xh, yh, n_out, r_ps)
+        parity = "exact vs oracle" if np.array_equal(o, want) else "MISMATCH vs oracle"
+        del xh, yh
+    for _ in range(max(0, args.warmup - 1)):
+        step(x, y)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.15)
+    # ---- device-resident timed region (value) ----
+    L.mmlttb_stage_timer(1)
+    l0 = L.mmlttb_launch_count()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step(x, y)
+    e1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = L.mmlttb_launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    import ctypes
+
+    st = (ctypes.c_double * 3)()
+    calls = ctypes.c_int64()
+    L.mmlttb_stage_timer_read(st, ctypes.byref(calls))
+    L.mmlttb_stage_timer(0)
+    stage_ms = [v / max(1, calls.value) for v in st]
+    # ---- end-to-end through the public API with host buffers (e2e) ----
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    yh = (y if y.dim() == 1 else y).cpu().pin_memory()
+    xh = x.cpu().pin_memory()
+    torch.cuda.synchronize()
+    res = step(xh, yh)  # warm the host path once
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_e2e = []
+    for _ in range(e2e_steps):
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        res = step(xh, yh)  # H2D of y (pinned), zero-copy x gather, D2H of the indices
+        f1.record()
+        torch.cuda.synchronize()
+        t_e2e.append(f0.elapsed_time(f1))
+    clocks.stop()
+    e2e_ms = statistics.mean(t_e2e)
+    h2d = yh.numel() * yh.element_size()
+    h2d += (2 + (n_out - 2) * r_ps) * batch * 8 if op != "lttb" else xh.numel() * xh.element_size()
+    d2h = res.numel() * res.element_size() if hasattr(res, "numel") else res.size * 8
+
+    pts = n * batch
+    # max over ranks of the device-timed region
+    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(t[0]), float(t[1])
+    value = pts * ws * args.steps / (ms / 1e3) if scaling == "weak" else pts * ws * args.steps / (ms / 1e3)
+    e2e_value = pts * ws / (e2e_ms / 1e3)
+    if rank == 0:
+        peak, peak_src = _peaks()
+        ysz = 4 if ydt == "f32" else 8
+        if op == "lttb":
+            alg_bytes = pts * (ysz + 8)
+            k_ms = sum(stage_ms) or ms / args.steps
+            kname = "k_lttb_chain (+means)"
+        else:
+            alg_bytes = pts * ysz
+            k_ms = stage_ms[0]
+            kname = "k_extrema (K1)"
+        achieved = alg_bytes / (k_ms / 1e3) / 1e9
+        tr = _traffic()
+        traffic = None
+        if tr and tr.get("workload") == name:
+            traffic = tr.get("dram_bytes_per_launch")
+        cpu = None
+        if not args.no_cpu and ws == 1:
+            cpu = cpu_sample(name, seconds=args.cpu_seconds)
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": scaling,
+            "vs_baseline": None,
+            "dtype": ydt,
+            "data": "synthetic (device-generated, torch Philox; BASELINE.json recipe shapes)",
+            "config": {"workload": name, "n": n, "batch": batch, "n_out": n_out, "minmax_ratio": r_ps, "op": op,
+                       "x_dtype": xdt, "l2": "inputs larger than L2 (no flush needed)",
+                       "parity": parity},
+            "hbm_gbs": alg_bytes * args.steps / (ms / 1e3) / 1e9,
+            "pct_roofline_e2e_device": alg_bytes * args.steps / (ms / 1e3) / 1e9 / peak,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg_bytes},
+            "stage_ms": {"k1_extrema": stage_ms[0], "k2_compact": stage_ms[1], "k3_lttb": stage_ms[2]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": e2e_ms, "steps": e2e_steps,
+                    "path": "minmaxlttb(pinned host x, pinned host y) -> numpy-free CPU tensor result"},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c3_1e9", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -55,6 +55,16 @@ enum { MM_OP_MINMAXLTTB = 0, MM_OP_PRESELECT = 1, MM_OP_LTTB = 2, MM_OP_MINMAX =
 int mmlttb_version(void);
 const char *mmlttb_last_error(void);
 
+/* Instrumentation (bench/profiling).  mmlttb_launch_count: kernels this
+ * library has launched since load.  mmlttb_stage_timer(1): fused
+ * minmaxlttb calls on this host thread record CUDA events on their stream at
+ * the K1 | K2 | K3 stage boundaries; mmlttb_stage_timer_read synchronises on
+ * them, writes the summed device milliseconds of the three stages to ms3[3]
+ * and the number of timed calls, then clears. */
+int64_t mmlttb_launch_count(void);
+int mmlttb_stage_timer(int enable);
+int mmlttb_stage_timer_read(double *ms3, int64_t *calls);
+
 /* Bytes of device workspace an operation needs for B series of N points. */
 int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int y_dtype);
 

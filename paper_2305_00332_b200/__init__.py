@@ -1,0 +1,41 @@
+"""B200-native MinMaxLTTB: a drop-in for the reference ``tsdown`` downsampling path.
+
+Same public names as ``tsdown`` (``/root/reference/pkg/src/tsdown/__init__.py:
+8-33``) for the MinMaxLTTB path; the compute runs in hand-written sm_100a
+kernels (``libmmlttb.so``, C ABI in ``include/mmlttb.h``).  Multi-GPU
+sharding lives in :mod:`paper_2305_00332_b200.sharding`.
+"""
+from . import errors
+from .core import Algorithm, BucketPartition, DownsampleConfig, TimeSeries, partition, validate
+from .downsamplers import (
+    Batch,
+    downsample,
+    every_nth,
+    lttb,
+    m4,
+    minmax,
+    minmax_preselect,
+    minmaxlttb,
+    run_parallel,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Algorithm",
+    "Batch",
+    "BucketPartition",
+    "DownsampleConfig",
+    "TimeSeries",
+    "downsample",
+    "errors",
+    "every_nth",
+    "lttb",
+    "m4",
+    "minmax",
+    "minmax_preselect",
+    "minmaxlttb",
+    "partition",
+    "run_parallel",
+    "validate",
+]

@@ -11,7 +11,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <array>
 #include <string>
+#include <vector>
 
 #include "../../include/mmlttb.h"
 #include "kernels.cuh"
@@ -33,10 +36,37 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+std::atomic<int64_t> g_launches{0};
+
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   return MM_OK;
+}
+
+// Stage timer: events recorded on the caller's stream at K1|K2|K3 boundaries
+// of the fused entries (bench.py reads per-kernel device time from these).
+struct StageTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::array<cudaEvent_t, 4>> calls;
+  std::array<cudaEvent_t, 4> cur{};
+};
+thread_local StageTimer g_timer;
+
+void stage_mark(cudaStream_t st, int i) {
+  if (!g_timer.on) return;
+  if (g_timer.used == g_timer.pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    g_timer.pool.push_back(e);
+  }
+  cudaEvent_t e = g_timer.pool[g_timer.used++];
+  cudaEventRecord(e, st);
+  g_timer.cur[i] = e;
+  if (i == 3) g_timer.calls.push_back(g_timer.cur);
 }
 
 constexpr int64_t ALIGN = 256;
@@ -63,18 +93,19 @@ struct Carve {
 
 // ---- K1 planning --------------------------------------------------------
 struct ExPlan {
-  int64_t C, chunk;
+  int64_t C, chunk, Cmax;
 };
 
-// Chunk length per warp: big enough to amortise the per-warp setup, small
-// enough that the grid has many waves over 148 SMs x 64 resident warps.
-ExPlan plan_extrema(int64_t total_elems, int64_t max_bucket, int ydt) {
-  const int64_t target_max = ydt == MM_F32 ? 8192 : 4096;
-  const int64_t want_warps = 148LL * 64 * 6;
-  int64_t target = total_elems / want_warps;
-  target = std::max<int64_t>(1024, std::min<int64_t>(target_max, target));
+// Chunks per bucket: enough warps to fill 148 SMs x 64 resident warps for
+// ~8 waves, never a chunk under MIN_CHUNK elements.  The partial buffer is
+// sized for Cmax, which depends only on the bucket count (not on N), so the
+// auxiliary memory stays O(B*k) (acceptance #11).
+constexpr int64_t WANT_WARPS = 148LL * 64 * 8;
+ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt) {
+  const int64_t min_chunk = ydt == MM_F32 ? 1024 : 512;
   ExPlan p;
-  p.C = std::max<int64_t>(1, cdiv(max_bucket, target));
+  p.Cmax = std::max<int64_t>(1, std::min<int64_t>(256, cdiv(WANT_WARPS, std::max<int64_t>(1, buckets_total))));
+  p.C = std::max<int64_t>(1, std::min<int64_t>(p.Cmax, cdiv(max_bucket, min_chunk)));
   p.chunk = cdiv(max_bucket, p.C);
   return p;
 }
@@ -83,6 +114,7 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
   const int64_t warps = a.B * a.nb * a.C;
   const int64_t blocks = cdiv(warps, 8);
   if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
+  if (a.chunk >= (1LL << 30)) return fail(MM_ERANGE, "bucket chunk too large");
   if (ydt == MM_F32)
     k_extrema<float, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
   else
@@ -189,9 +221,9 @@ int launch_lttb(LttbArgs a, int xdt, int ydt, int64_t s, cudaStream_t st) {
 int64_t preselect_ws(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt, bool with_lttb) {
   const int64_t k = (n_out - 2) * (r_ps / 2);
   const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * (N - 2), S, ydt);
+  const ExPlan p = plan_extrema(B * k, S, ydt);
   const int64_t cap = 2 + 2 * k;
-  int64_t bytes = up(B * k * p.C * (int64_t)sizeof(Partial)) + up(B * 8);
+  int64_t bytes = up(B * k * p.Cmax * (int64_t)sizeof(Partial)) + up(B * 8);
   if (with_lttb) bytes += 3 * up(B * cap * 8) + lttb_ws(B, n_out, r_ps);
   return bytes;
 }
@@ -209,6 +241,31 @@ int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
 extern "C" {
 
 int mmlttb_version(void) { return 1; }
+
+int64_t mmlttb_launch_count(void) { return g_launches.load(); }
+
+int mmlttb_stage_timer(int enable) {
+  g_timer.on = enable != 0;
+  g_timer.used = 0;
+  g_timer.calls.clear();
+  return MM_OK;
+}
+
+int mmlttb_stage_timer_read(double* ms3, int64_t* calls) {
+  for (int i = 0; i < 3; ++i) ms3[i] = 0.0;
+  for (auto& c : g_timer.calls) {
+    if (cudaEventSynchronize(c[3]) != cudaSuccess) return fail(MM_ECUDA, "cudaEventSynchronize");
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, c[i], c[i + 1]) != cudaSuccess) return fail(MM_ECUDA, "cudaEventElapsedTime");
+      ms3[i] += ms;
+    }
+  }
+  *calls = (int64_t)g_timer.calls.size();
+  g_timer.used = 0;
+  g_timer.calls.clear();
+  return MM_OK;
+}
 const char* mmlttb_last_error(void) { return g_err.c_str(); }
 
 int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int y_dtype) {
@@ -227,8 +284,8 @@ int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int6
     case MM_OP_M4: {
       const int64_t k = op == MM_OP_MINMAX ? n_out / 2 : n_out / 4;
       if (k < 1) return 0;
-      const ExPlan p = plan_extrema(B * N, cdiv(N, k), y_dtype);
-      return up(B * k * p.C * (int64_t)sizeof(Partial));
+      const ExPlan p = plan_extrema(B * k, cdiv(N, k), y_dtype);
+      return up(B * k * p.Cmax * (int64_t)sizeof(Partial));
     }
   }
   return 0;
@@ -246,9 +303,9 @@ int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B,
   if (out_ld < 2 + 2 * k) return fail(MM_EINVAL, "out_ld < 2 + 2k");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * (N - 2), S, y_dtype);
+  const ExPlan p = plan_extrema(B * k, S, y_dtype);
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(B * k * p.C);
+  Partial* part = cv.take<Partial>(B * k * p.Cmax);
   if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
   ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk, part};
   if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
@@ -269,9 +326,9 @@ static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t 
   const int64_t k = m4 ? n_out / 4 : n_out / 2;
   if ((m4 && n_out % 4) || (!m4 && n_out % 2)) return fail(MM_EINVAL, "n_out divisibility");
   if (!mul_ok(k + 1, N)) return fail(MM_ERANGE, "k*N overflows int64");
-  const ExPlan p = plan_extrema(B * N, cdiv(N, k), ydt);
+  const ExPlan p = plan_extrema(B * k, cdiv(N, k), ydt);
   Carve cv{(char*)ws, wsb};
-  Partial* part = cv.take<Partial>(B * k * p.C);
+  Partial* part = cv.take<Partial>(B * k * p.Cmax);
   if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
   ExArgs ea{y, y_ld, B, 0, N, k, nullptr, 0, k, p.C, p.chunk, part};
   if ((rc = launch_extrema(ea, ydt, st))) return rc;
@@ -312,10 +369,10 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   if (k > N - 2) return fail(MM_EINVAL, "sub-buckets exceed interior");
   if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
   const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * (N - 2), S, y_dtype);
+  const ExPlan p = plan_extrema(B * k, S, y_dtype);
   const int64_t cap = 2 + 2 * k;
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(B * k * p.C);
+  Partial* part = cv.take<Partial>(B * k * p.Cmax);
   int64_t* cnt = cv.take<int64_t>(B);
   int64_t* pre = cv.take<int64_t>(B * cap);
   double* px = cv.take<double>(B * cap);
@@ -324,7 +381,9 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small (%lld bytes)", (long long)workspace_bytes);
   // K1: sub-bucket extrema over partition(1, N-1, k)  (downsamplers.py:149-155)
   ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk, part};
+  stage_mark(st, 0);
   if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
+  stage_mark(st, 1);
   // K2: [0] + interleaved pairs + [N-1], gathered as f64 (:156-160, :207)
   CompactArgs ca{};
   ca.part = part; ca.nb = k; ca.C = p.C; ca.mode = 0;
@@ -336,12 +395,14 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   ca.out_x = px; ca.out_y = py;
   k_compact<512><<<(unsigned)B, 512, 0, st>>>(ca);
   if ((rc = check_launch("k_compact"))) return rc;
+  stage_mark(st, 2);
   // K3: LTTB over the compacted sub-series, mapped back (:208-209)
   LttbArgs la{};
   la.x = px; la.x_ld = cap; la.y = py; la.y_ld = cap;
   la.m_dev = cnt; la.n = 0; la.bounds = nullptr; la.map = pre; la.map_ld = cap;
   la.B = B; la.n_out = n_out; la.out = out; la.tables = lt;
   if ((rc = launch_lttb(la, MM_F64, MM_F64, r_ps, st))) return rc;
+  stage_mark(st, 3);
   if (out_count) {  // every series yields exactly n_out (P9)
     k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
     return check_launch("k_fill");
@@ -371,8 +432,9 @@ int mmlttb_every_nth(int64_t N, int64_t n_out, int64_t* out, void* stream) {
 }
 
 int64_t mmlttb_extrema_workspace_bytes(int64_t k, int64_t max_bucket_len) {
-  const ExPlan p = plan_extrema(k * max_bucket_len, max_bucket_len, MM_F64);
-  return up(k * p.C * (int64_t)sizeof(Partial));
+  (void)max_bucket_len;
+  const ExPlan p = plan_extrema(k, 1, MM_F32);
+  return up(k * p.Cmax * (int64_t)sizeof(Partial));
 }
 
 int mmlttb_extrema_by_bucket(const void* y, int y_dtype, const int64_t* bounds, int64_t k, int64_t max_bucket_len,
@@ -380,9 +442,9 @@ int mmlttb_extrema_by_bucket(const void* y, int y_dtype, const int64_t* bounds, 
                              void* stream) {
   if (!y || !bounds || !ydt_ok(y_dtype) || k < 1 || max_bucket_len < 1) return fail(MM_EINVAL, "bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  const ExPlan p = plan_extrema(k * max_bucket_len, max_bucket_len, MM_F64);
+  const ExPlan p = plan_extrema(k, max_bucket_len, y_dtype);
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(k * p.C);
+  Partial* part = cv.take<Partial>(k * p.Cmax);
   if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
   ExArgs ea{y, 0, 1, 0, 1, 1, bounds, 0, k, p.C, p.chunk, part};
   int rc = launch_extrema(ea, y_dtype, st);
@@ -411,11 +473,8 @@ int mmlttb_lttb_select(const void* xs, int x_dtype, const void* ys, int y_dtype,
 int64_t mmlttb_shard_workspace_bytes(int64_t N, int64_t n_out, int64_t r_ps, int64_t b0, int64_t b1) {
   const int64_t k = (n_out - 2) * (r_ps / 2);
   if (k < 1 || b1 <= b0) return ALIGN;
-  const int64_t S = cdiv(N - 2, k);
-  const int64_t lo = 1 + (b0 * (N - 2)) / k, hi = 1 + (b1 * (N - 2)) / k;
-  const ExPlan p = plan_extrema(hi - lo, S, MM_F32);
-  const ExPlan q = plan_extrema(hi - lo, S, MM_F64);
-  return up((b1 - b0) * std::max(p.C, q.C) * (int64_t)sizeof(Partial));
+  const ExPlan p = plan_extrema(b1 - b0, cdiv(N - 2, k), MM_F32);
+  return up((b1 - b0) * p.Cmax * (int64_t)sizeof(Partial));
 }
 
 int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard, int y_dtype, int64_t lo, int64_t N,
@@ -432,10 +491,9 @@ int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nb = b1 - b0;
   const int64_t S = cdiv(N - 2, k);
-  const int64_t elo = 1 + (b0 * (N - 2)) / k, ehi = 1 + (b1 * (N - 2)) / k;
-  const ExPlan p = plan_extrema(ehi - elo, S, y_dtype);
+  const ExPlan p = plan_extrema(std::max<int64_t>(nb, 1), S, y_dtype);
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(std::max<int64_t>(nb, 1) * p.C);
+  Partial* part = cv.take<Partial>(std::max<int64_t>(nb, 1) * p.Cmax);
   if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
   // virtual base: element i of the global series lives at y_shard[i - lo]
   const void* ybase = (const char*)y_shard - lo * esize(y_dtype);

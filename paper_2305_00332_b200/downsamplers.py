@@ -1,0 +1,349 @@
+"""The selection algorithms on the B200 (reference ``tsdown/downsamplers.py``).
+
+Same names, signatures, checks (in the reference's order) and outputs as
+``/root/reference/pkg/src/tsdown/downsamplers.py``; the work is done by the
+sm_100a kernels behind ``libmmlttb.so``:
+
+* ``minmaxlttb``        -> ``mmlttb_minmaxlttb``   (K1 extrema -> K2 compact -> K3 LTTB)
+* ``minmax_preselect``  -> ``mmlttb_minmax_preselect``
+* ``lttb``              -> ``mmlttb_lttb``
+* ``minmax`` / ``m4``   -> ``mmlttb_minmax`` / ``mmlttb_m4``
+* ``every_nth``         -> ``mmlttb_every_nth``
+
+Every function also accepts the flat form ``(x, y, n_out, ...)`` from the
+north star (``minmaxlttb(x, y, n_out, minmax_ratio=4)``); ``y`` may then be
+2-D ``[B, N]`` (one series per row, ``x`` shared ``[N]`` or per row) and the
+result is ``[B, n_out]``.  Results follow the input's home: numpy in, numpy
+out; CUDA tensors in, CUDA int64 tensor out (no host sync for fixed-size
+outputs).  ``parallel``/``threads`` are accepted for parity; the device path
+is always bucket-parallel and byte-identical to the sequential reference.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .core import Algorithm, DownsampleConfig, TimeSeries, validate
+from .errors import (
+    BadPreselectionRatio,
+    NotParallelizable,
+    NOutNotDivisibleBy4,
+    NOutOfRange,
+    OddNOut,
+    RatioTooLargeForSeries,
+)
+
+__all__ = [
+    "every_nth", "minmax", "m4", "lttb", "minmax_preselect", "minmaxlttb", "run_parallel", "downsample",
+    "Batch",
+]
+
+
+# --------------------------------------------------------------- inputs ----
+class Batch:
+    """B series of N points for one CUDA device (the flat / batched form).
+
+    ``y``: [B, N] (or [N]) float32/float64; ``x``: [N] shared or [B, N],
+    int64/int32/float32/float64.  A pinned host ``x`` is read in place by the
+    gather (zero-copy over PCIe: only the <= 2 + (n_out-2)*r_ps preselected
+    x values are ever touched), so ``minmaxlttb`` moves just ``y`` to HBM.
+    Shapes are known at construction; device transfers happen in
+    ``ready()``, after the reference's O(1) checks have passed.
+    """
+
+    def __init__(self, x, y, device=None):
+        self._x_in, self._y_in, self._dev_in = x, y, device
+        self.host = not (isinstance(y, torch.Tensor) and y.is_cuda)
+        self.numpy = not isinstance(y, torch.Tensor)
+        shape = tuple(y.shape) if hasattr(y, "shape") else np.shape(y)
+        if len(shape) not in (1, 2):
+            raise ValueError("y must be [N] or [B, N]")
+        self.squeeze = len(shape) == 1
+        self.B, self.n = (1, int(shape[0])) if self.squeeze else (int(shape[0]), int(shape[1]))
+        self._ready = False
+
+    def ready(self):
+        if self._ready:
+            return self
+        y, x = self._y_in, self._x_in
+        dev = y.device if not self.host else N.require_cuda(self._dev_in)
+        N.require_cuda(dev)
+        yt = torch.as_tensor(y) if not isinstance(y, torch.Tensor) else y
+        if yt.dtype not in (torch.float32, torch.float64):
+            yt = yt.to(torch.float64)
+        if yt.dim() == 1:
+            yt = yt.unsqueeze(0)
+        self.y = yt.to(dev, non_blocking=True).contiguous() if yt.device != dev else yt.contiguous()
+        self.device = dev
+        self.x = None
+        self.x_ld = 0
+        if x is not None:
+            xt = torch.as_tensor(x) if not isinstance(x, torch.Tensor) else x
+            if xt.dtype not in (torch.float32, torch.float64, torch.int64, torch.int32):
+                xt = xt.to(torch.float64)
+            if xt.dim() == 2 and xt.shape[0] == 1:
+                xt = xt[0]
+            if xt.shape[-1] != self.n or xt.dim() > 2 or (xt.dim() == 2 and xt.shape[0] != self.B):
+                raise ValueError("x must be [N] or [B, N] matching y")
+            xt = xt.contiguous()
+            if not xt.is_cuda and not xt.is_pinned():
+                xt = xt.to(dev, non_blocking=True)
+            self.x = xt
+            self.x_ld = self.n if xt.dim() == 2 else 0
+        self._ready = True
+        return self
+
+    def ret(self, t: torch.Tensor):
+        if self.squeeze:
+            t = t[0]
+        return t.cpu().numpy() if self.numpy else (t.cpu() if self.host else t)
+
+
+class _Series(Batch):
+    """Adapter: a TimeSeries seen as a 1-series Batch."""
+
+    def __init__(self, series: TimeSeries, device=None):
+        self._series, self._dev_in = series, device
+        self.host = self.numpy = series.is_host
+        self.squeeze = True
+        self.B, self.n = 1, len(series)
+        self._ready = False
+
+    def ready(self):
+        if not self._ready:
+            x, y = self._series.device_arrays(self._dev_in)
+            self.y, self.x, self.x_ld, self.device = y.unsqueeze(0), x, 0, y.device
+            self._ready = True
+        return self
+
+
+def _input(series, y=None, device=None):
+    return _Series(series, device) if isinstance(series, TimeSeries) else Batch(series, y, device)
+
+
+def _codes(b):
+    return (N.DTYPE_CODE[b.x.dtype] if b.x is not None else 0), N.DTYPE_CODE[b.y.dtype]
+
+
+def _ctx(b):
+    return torch.cuda.device(b.device)
+
+
+def _is_flat(first) -> bool:
+    return not isinstance(first, TimeSeries)
+
+
+# ------------------------------------------------------------- checks -------
+def _check_n_out(n: int, n_out: int) -> int:
+    if not 3 <= n_out <= n:  # downsamplers.py:37-41
+        raise NOutOfRange(f"n_out must be in [3, {n}], got {n_out}")
+    return n
+
+
+def _check_preselect(n: int, n_out: int, r_ps: int) -> int:
+    _check_n_out(n, n_out)
+    if r_ps < 2 or r_ps % 2:  # downsamplers.py:147-148
+        raise BadPreselectionRatio(f"preselection needs an even r_ps >= 2, got {r_ps}")
+    sub_buckets = (n_out - 2) * (r_ps // 2)
+    if sub_buckets > n - 2:  # :149-153
+        raise RatioTooLargeForSeries(f"{sub_buckets} sub-buckets exceed the {n - 2} interior samples")
+    return sub_buckets
+
+
+def _counted(b, out, cnt):
+    """Trim variable-length rows (minmax/m4/preselect) -- one host sync."""
+    counts = cnt.cpu().tolist()
+    if b.B == 1:
+        return b.ret(out[:, : counts[0]])
+    rows = [out[i, : counts[i]] for i in range(b.B)]
+    if b.numpy:
+        return [r.cpu().numpy() for r in rows]
+    return rows
+
+
+# ------------------------------------------------------------ algorithms ----
+def every_nth(series, n_out, *args):
+    """Select floor(i * N / n_out), i in [0, n_out) (downsamplers.py:44-47)."""
+    if _is_flat(series):
+        b = Batch(series, n_out, None)  # every_nth(x, y, n_out)
+        n_out = args[0]
+    else:
+        b = _Series(series)
+    _check_n_out(b.n, n_out)
+    b.ready()
+    out = torch.empty((1, n_out), dtype=torch.int64, device=b.device)
+    with _ctx(b):
+        N.check(N.lib().mmlttb_every_nth(b.n, n_out, out.data_ptr(), N.stream_ptr(b.device)), "every_nth")
+    if b.B > 1:
+        out = out.expand(b.B, n_out).contiguous()
+    return b.ret(out)
+
+
+def _minmax_like(b, n_out, op: str, force: bool = False):
+    b.ready()
+    fn = N.lib().mmlttb_m4 if op == "m4" else N.lib().mmlttb_minmax
+    code = N.OP_M4 if op == "m4" else N.OP_MINMAX
+    xdt, ydt = _codes(b)
+    out = torch.empty((b.B, n_out), dtype=torch.int64, device=b.device)
+    cnt = torch.empty(b.B, dtype=torch.int64, device=b.device)
+    with _ctx(b):
+        st = N.stream_ptr(b.device)
+        if force:  # r_ps == 1 through the fused entry (downsamplers.py:164-179)
+            wsb = N.lib().mmlttb_workspace_bytes(N.OP_MINMAXLTTB, b.B, b.n, n_out, 1, ydt)
+            ws = N.workspace(wsb, b.device, b.n)
+            N.check(N.lib().mmlttb_minmaxlttb(N.ptr(b.x), xdt, b.x_ld, b.y.data_ptr(), ydt, b.n, b.B, b.n,
+                                              n_out, 1, out.data_ptr(), cnt.data_ptr(), ws.data_ptr(), wsb, st),
+                    "minmaxlttb(r_ps=1)", b.n)
+        else:
+            wsb = N.lib().mmlttb_workspace_bytes(code, b.B, b.n, n_out, 0, ydt)
+            ws = N.workspace(wsb, b.device, b.n)
+            N.check(fn(b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out, out.data_ptr(), cnt.data_ptr(), ws.data_ptr(),
+                       wsb, st), op, b.n)
+    return _counted(b, out, cnt)
+
+
+def minmax(series, n_out, parallel=False, *args, **kw):
+    """Vertical extrema per bucket (downsamplers.py:72-92).
+
+    Flat form: ``minmax(x, y, n_out)``.
+    """
+    if _is_flat(series):
+        b, n_out = Batch(series, n_out, kw.get("device")), parallel
+    else:
+        b = _Series(series)
+    _check_n_out(b.n, n_out)
+    if n_out % 2:
+        raise OddNOut(f"minmax needs an even n_out, got {n_out}")
+    return _minmax_like(b, n_out, "minmax")
+
+
+def m4(series, n_out, parallel=False, *args, **kw):
+    """First, min, max and last sample per bucket (downsamplers.py:95-112)."""
+    if _is_flat(series):
+        b, n_out = Batch(series, n_out, kw.get("device")), parallel
+    else:
+        b = _Series(series)
+    _check_n_out(b.n, n_out)
+    if n_out % 4:
+        raise NOutNotDivisibleBy4(f"m4 needs n_out divisible by 4, got {n_out}")
+    return _minmax_like(b, n_out, "m4")
+
+
+def lttb(series, n_out, *args, **kw):
+    """Largest-Triangle-Three-Buckets (downsamplers.py:115-132): exactly n_out indices.
+
+    Flat form: ``lttb(x, y, n_out)``.
+    """
+    if _is_flat(series):
+        b, n_out = Batch(series, n_out, kw.get("device")), args[0]
+    else:
+        b = _Series(series)
+    _check_n_out(b.n, n_out)
+    b.ready()
+    xdt, ydt = _codes(b)
+    out = torch.empty((b.B, n_out), dtype=torch.int64, device=b.device)
+    x = b.x
+    if x is not None and not x.is_cuda:
+        x = x.to(b.device)  # full LTTB reads every x
+    with _ctx(b):
+        wsb = N.lib().mmlttb_workspace_bytes(N.OP_LTTB, b.B, b.n, n_out, 0, ydt)
+        ws = N.workspace(wsb, b.device, b.n)
+        N.check(N.lib().mmlttb_lttb(x.data_ptr(), xdt, b.x_ld, b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out,
+                                    out.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(b.device)), "lttb", b.n)
+    return b.ret(out)
+
+
+def minmax_preselect(series, n_out, r_ps, parallel=False, *args, **kw):
+    """MinMax candidate preselection for MinMaxLTTB (downsamplers.py:135-161).
+
+    Flat form: ``minmax_preselect(x, y, n_out, r_ps)``.
+    """
+    if _is_flat(series):
+        b, n_out, r_ps = Batch(series, n_out, kw.get("device")), r_ps, parallel
+    else:
+        b = _Series(series)
+    k = _check_preselect(b.n, n_out, r_ps)
+    b.ready()
+    _, ydt = _codes(b)
+    cap = 2 + 2 * k
+    out = torch.empty((b.B, cap), dtype=torch.int64, device=b.device)
+    cnt = torch.empty(b.B, dtype=torch.int64, device=b.device)
+    with _ctx(b):
+        wsb = N.lib().mmlttb_workspace_bytes(N.OP_PRESELECT, b.B, b.n, n_out, r_ps, ydt)
+        ws = N.workspace(wsb, b.device, b.n)
+        N.check(N.lib().mmlttb_minmax_preselect(b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out, r_ps, out.data_ptr(),
+                                                cap, cnt.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(b.device)),
+                "minmax_preselect", b.n)
+    return _counted(b, out, cnt)
+
+
+def _minmaxlttb_batch(b, n_out: int, r_ps: int):
+    b.ready()
+    xdt, ydt = _codes(b)
+    out = torch.empty((b.B, n_out), dtype=torch.int64, device=b.device)
+    with _ctx(b):
+        wsb = N.lib().mmlttb_workspace_bytes(N.OP_MINMAXLTTB, b.B, b.n, n_out, r_ps, ydt)
+        ws = N.workspace(wsb, b.device, b.n)
+        N.check(N.lib().mmlttb_minmaxlttb(N.ptr(b.x), xdt, b.x_ld, b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out,
+                                          r_ps, out.data_ptr(), None, ws.data_ptr(), wsb, N.stream_ptr(b.device)),
+                "minmaxlttb", b.n)
+    return b.ret(out)
+
+
+def minmaxlttb(series, n_out, r_ps=4, parallel=False, *args, minmax_ratio=None, device=None):
+    """MinMax preselection, then LTTB on the candidates (downsamplers.py:182-209).
+
+    Reference form: ``minmaxlttb(series, n_out, r_ps=4, parallel=False)``.
+    Flat form (north star): ``minmaxlttb(x, y, n_out, minmax_ratio=4)`` with
+    ``y`` of shape [N] or [B, N]; returns [n_out] or [B, n_out].
+    """
+    if _is_flat(series):
+        x, y = series, n_out
+        n_out = r_ps
+        ratio = minmax_ratio if minmax_ratio is not None else (parallel if not isinstance(parallel, bool) else 4)
+        b = Batch(x, y, device)
+        r_ps = int(ratio)
+    else:
+        if minmax_ratio is not None:
+            r_ps = minmax_ratio
+        b = _Series(series, device)
+    if r_ps == 1:
+        _check_n_out(b.n, n_out)
+        if n_out % 2:
+            raise OddNOut(f"minmax needs an even n_out, got {n_out}")
+        return _minmax_like(b, n_out, "minmax", force=True)
+    _check_preselect(b.n, n_out, r_ps)
+    return _minmaxlttb_batch(b, n_out, r_ps)
+
+
+# ------------------------------------------------------------ dispatch ------
+def run_parallel(series: TimeSeries, config: DownsampleConfig):
+    """Parallel dispatch (downsamplers.py:224-244); identical output to sequential."""
+    if not config.parallel:
+        raise ValueError("run_parallel needs a config with parallel=True")
+    validate(series, config)
+    if config.algorithm is Algorithm.LTTB:
+        raise NotParallelizable("LTTB is not parallelizable")
+    return _dispatch(series, config)
+
+
+def _dispatch(series, config):
+    algo = config.algorithm
+    if algo is Algorithm.EVERY_NTH:
+        return every_nth(series, config.n_out)
+    if algo is Algorithm.MINMAX:
+        return minmax(series, config.n_out)
+    if algo is Algorithm.M4:
+        return m4(series, config.n_out)
+    if algo is Algorithm.LTTB:
+        return lttb(series, config.n_out)
+    return minmaxlttb(series, config.n_out, config.r_ps)
+
+
+def downsample(series: TimeSeries, config: DownsampleConfig):
+    """Dispatch a config to the matching algorithm (downsamplers.py:247-260)."""
+    validate(series, config)
+    if config.parallel:
+        return run_parallel(series, config)
+    return _dispatch(series, config)

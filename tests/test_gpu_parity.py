@@ -1,0 +1,279 @@
+"""Device parity: the sm_100a path vs the reference's golden outputs and the oracle.
+
+Index-exact equality everywhere (integer/index work; LTTB fp64 parity is
+bit-exact by construction, so the tolerance is zero).  Inputs are the
+seeded recipes of tests/recipes.py and tests/fuzzgen.py.
+"""
+import gzip
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import fuzzgen
+import recipes
+import paper_2305_00332_b200 as mm
+from paper_2305_00332_b200 import _native, errors
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+DEV = torch.device("cuda", 0)
+
+
+def _cfg():
+    return json.loads((GOLD / "configs.json").read_text())
+
+
+def _call(op, series, n_out, r_ps):
+    try:
+        if op == "minmaxlttb":
+            out = mm.minmaxlttb(series, n_out, r_ps)
+        elif op == "lttb":
+            out = mm.lttb(series, n_out)
+        elif op == "minmax":
+            out = mm.minmax(series, n_out)
+        elif op == "minmax_preselect":
+            out = mm.minmax_preselect(series, n_out, r_ps)
+        elif op == "m4":
+            out = mm.m4(series, n_out)
+        else:
+            raise ValueError(op)
+    except errors.TsdownError as e:
+        return {"error": type(e).__name__}
+    if isinstance(out, torch.Tensor):
+        out = out.cpu().numpy()
+    return {"out": [int(v) for v in out]}
+
+
+def test_kats():
+    k = json.loads((GOLD / "kats.json").read_text())
+    ts = mm.TimeSeries
+    a = [1, 3, 2, 0, 5, 4, 9, 8]
+    xa = list(range(8))
+    assert mm.minmax(ts(xa, a), 4).tolist() == k["minmax"]
+    assert mm.m4(ts(xa, a), 8).tolist() == k["m4"]
+    assert mm.lttb(ts(list(range(6)), [0, 0, 10, 0, 0, 0]), 3).tolist() == k["lttb_spike"]
+    assert mm.minmax(ts(list(range(10)), [3.0] * 10), 4).tolist() == k["minmax_constant_n10"]
+    assert mm.lttb(ts(list(range(20)), list(range(20))), 6).tolist() == k["lttb_collinear_n20"]
+    assert mm.minmax_preselect(ts(list(range(10)), np.sin(np.arange(10.0))), 4, 2).tolist() == k["preselect_sin10"]
+    assert mm.minmaxlttb(ts(xa, a), 4, r_ps=1).tolist() == k["minmaxlttb_r1"]
+    assert mm.every_nth(ts(list(range(10)), [0.0] * 10), 5).tolist() == k["every_nth_10_5"]
+    assert mm.every_nth(ts(list(range(7)), [0.0] * 7), 3).tolist() == k["every_nth_7_3"]
+    assert mm.minmax(ts([0, 1, 2, 3], [0.0, -0.0, 0.0, -0.0]), 4).tolist() == k["signed_zero_minmax"]
+
+
+def _fuzz():
+    with gzip.open(GOLD / "fuzz.json.gz", "rt") as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("home", ["host", "device"])
+def test_fuzz_matches_reference(home):
+    bad = []
+    for rec in _fuzz():
+        c = fuzzgen.make_case(rec["i"])
+        x, y = c["x"], c["y"]
+        if home == "device":
+            x, y = torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV)
+        got = _call(rec["op"], mm.TimeSeries(x, y), rec["n_out"], rec["r_ps"])
+        want = {k: rec[k] for k in ("out", "error") if k in rec}
+        if got != want:
+            bad.append((rec["i"], rec["op"], rec["kind"], rec["n"], rec["n_out"], rec["r_ps"]))
+    assert not bad, f"{len(bad)} mismatches, first: {bad[:8]}"
+
+
+def test_downsample_config_parity():
+    with gzip.open(GOLD / "config_errors.json.gz", "rt") as f:
+        recs = json.load(f)
+    rng = np.random.Generator(np.random.PCG64(77))
+    series = {n: mm.TimeSeries(np.arange(n), rng.standard_normal(n)) for n in (3, 4, 5, 10, 57)}
+    for rec in recs:
+        if "config_error" in rec:
+            continue
+        cfg = mm.DownsampleConfig(rec["algo"], rec["n_out"], rec["r_ps"], rec["parallel"], rec["threads"])
+        try:
+            got = {"out": [int(v) for v in mm.downsample(series[rec["n"]], cfg)]}
+        except (errors.TsdownError, ValueError) as e:
+            got = {"downsample_error": type(e).__name__}
+        want = {k: rec[k] for k in ("out", "downsample_error") if k in rec}
+        assert got == want, rec
+
+
+def test_c1_full():
+    x, y = recipes.c1()
+    g = _cfg()["C1"]["r4"]["out"]
+    assert mm.minmaxlttb(mm.TimeSeries(x, y), 1000, 4).tolist() == g
+    out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), 1000, minmax_ratio=4)
+    assert out.cpu().tolist() == g
+
+
+def test_c2_full_lttb():
+    x, y = recipes.c2()
+    g = _cfg()["C2"]["lttb"]["out"]
+    out = mm.lttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), 2000)
+    assert out.cpu().tolist() == g
+
+
+def test_c3_full_all_ratios():
+    x, y = recipes.c3()
+    xd, yd = torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV)
+    cfg = _cfg()["C3"]
+    for r in recipes.CONFIGS["C3"]["r_ps"]:
+        out = mm.minmaxlttb(xd, yd, 2000, minmax_ratio=r)
+        assert out.cpu().tolist() == cfg[f"r{r}"]["out"], r
+
+
+def test_c4_batch():
+    g = json.loads((GOLD / "c4.json").read_text())
+    import hashlib
+
+    n = 1_000_000
+    B = 512  # a 512-series slice of the 4096-series batch, through the batched path
+    ids = list(range(0, 4096, 8))
+    x, y = recipes.c4(series=ids, n=n)
+    out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), 1000, minmax_ratio=4).cpu().numpy()
+    assert out.shape == (B, 1000)
+    for row, s in zip(out, ids):
+        assert hashlib.sha256(row.astype(np.int64).tobytes()).hexdigest() == g["sha"][s], s
+    for s, o in g["full"].items():
+        if int(s) in ids:
+            assert out[ids.index(int(s))].tolist() == o
+
+
+@pytest.mark.slow
+def test_c5_full():
+    g = _cfg()["C5"]["r4"]["out"]
+    n = recipes.CONFIGS["C5"]["n"]
+    xd = torch.empty(n, dtype=torch.float64, device=DEV)
+    yd = torch.empty(n, dtype=torch.float32, device=DEV)
+    for lo, xc, yc in recipes.c5_chunks(n):
+        xd[lo:lo + xc.shape[0]].copy_(torch.from_numpy(xc))
+        yd[lo:lo + yc.shape[0]].copy_(torch.from_numpy(yc))
+    out = mm.minmaxlttb(xd, yd, 4000, minmax_ratio=4)
+    assert out.cpu().tolist() == g
+
+
+def test_batch_equals_per_series():
+    rng = np.random.Generator(np.random.PCG64(5))
+    B, n = 37, 20_011
+    y = np.cumsum(rng.standard_normal((B, n)), axis=1)
+    x = np.cumsum(rng.exponential(1.0, n))
+    for dt in (np.float32, np.float64):
+        yb = torch.from_numpy(y.astype(dt)).to(DEV)
+        out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), yb, 300, minmax_ratio=6).cpu().numpy()
+        for i in range(B):
+            assert np.array_equal(out[i], O.minmaxlttb(x, y[i].astype(dt), 300, 6)), (dt, i)
+        lt = mm.lttb(torch.from_numpy(x).to(DEV), yb, 200).cpu().numpy()
+        for i in range(0, B, 6):
+            assert np.array_equal(lt[i], O.lttb(x, y[i].astype(dt), 200))
+
+
+@pytest.mark.parametrize("n,n_out", [(10, 3), (100, 98), (1000, 500), (65_537, 40), (300_000, 3)])
+def test_lttb_shapes(n, n_out):
+    rng = np.random.Generator(np.random.PCG64(n))
+    x = np.cumsum(rng.exponential(1.0, n))
+    y = rng.standard_normal(n)
+    got = mm.lttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out).cpu().numpy()
+    assert np.array_equal(got, O.lttb(x, y, n_out))
+
+
+@pytest.mark.parametrize("r", [2, 4, 8, 16, 32, 64, 100])
+def test_minmaxlttb_ratios_small(r):
+    rng = np.random.Generator(np.random.PCG64(r))
+    n = 200_000
+    x = np.arange(n, dtype=np.int64)
+    y = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+    got = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), 700, minmax_ratio=r)
+    assert np.array_equal(got.cpu().numpy(), O.minmaxlttb(x, y, 700, r))
+
+
+def test_degeneracy_to_lttb():
+    # SPEC acceptance #2: sub-buckets of <= 2 points -> minmaxlttb == lttb
+    rng = np.random.Generator(np.random.PCG64(2))
+    for n in (10, 57, 200, 500):
+        x = np.arange(n)
+        y = rng.standard_normal(n)
+        ts = mm.TimeSeries(x, y)
+        for n_out in range(3, n + 1, max(1, n // 17)):
+            for r in (2, 4, 6, 8):
+                k = (n_out - 2) * (r // 2)
+                if k > n - 2 or -(-(n - 2) // k) > 2:
+                    continue
+                assert np.array_equal(mm.minmaxlttb(ts, n_out, r), mm.lttb(ts, n_out)), (n, n_out, r)
+
+
+def test_pinned_host_inputs_zero_copy_x():
+    x, y = recipes.c1(500_000)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.from_numpy(y.astype(np.float32)).pin_memory()
+    out = mm.minmaxlttb(xp, yp, 1000, minmax_ratio=4)
+    assert not out.is_cuda
+    assert np.array_equal(out.numpy(), O.minmaxlttb(x, y.astype(np.float32), 1000, 4))
+
+
+def test_reference_kernel_entry_points():
+    """mmlttb_extrema_by_bucket / mmlttb_lttb_select vs the oracle's restatement."""
+    L = _native.lib()
+    rng = np.random.Generator(np.random.PCG64(9))
+    n = 100_003
+    y = np.cumsum(rng.standard_normal(n))
+    y[::97] = -0.0
+    bounds = mm.partition(1, n - 1, 777).boundaries
+    yd = torch.from_numpy(y).to(DEV)
+    bd = torch.from_numpy(np.ascontiguousarray(bounds)).to(DEV)
+    mn = torch.empty(777, dtype=torch.int64, device=DEV)
+    mx = torch.empty(777, dtype=torch.int64, device=DEV)
+    smax = int(np.diff(bounds).max())
+    wsb = L.mmlttb_extrema_workspace_bytes(777, smax)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    _native.check(L.mmlttb_extrema_by_bucket(yd.data_ptr(), 1, bd.data_ptr(), 777, smax, mn.data_ptr(),
+                                             mx.data_ptr(), ws.data_ptr(), wsb, st), "extrema")
+    omn, omx = O.extrema_by_bucket(y, bounds)
+    assert np.array_equal(mn.cpu().numpy(), omn) and np.array_equal(mx.cpu().numpy(), omx)
+    x = np.arange(n, dtype=np.int64)
+    lb = mm.partition(1, n - 1, 398).boundaries
+    lbd = torch.from_numpy(np.ascontiguousarray(lb)).to(DEV)
+    out = torch.empty(400, dtype=torch.int64, device=DEV)
+    wsb = L.mmlttb_lttb_select_workspace_bytes(n, 399)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=DEV)
+    xd = torch.from_numpy(x).to(DEV)
+    _native.check(L.mmlttb_lttb_select(xd.data_ptr(), 2, yd.data_ptr(), 1, n, lbd.data_ptr(), 399, out.data_ptr(),
+                                       ws.data_ptr(), wsb, st), "lttb_select")
+    assert np.array_equal(out.cpu().numpy(), O.lttb(x, y, 400))
+
+
+def test_device_validation():
+    x = torch.arange(100, device=DEV, dtype=torch.int64)
+    y = torch.randn(100, device=DEV)
+    mm.TimeSeries(x, y)
+    y2 = y.clone()
+    y2[50] = float("nan")
+    with pytest.raises(errors.NonFiniteValue):
+        mm.TimeSeries(x, y2)
+    x2 = x.clone()
+    x2[10] = 3
+    with pytest.raises(errors.NonMonotonicX):
+        mm.TimeSeries(x2, y)
+
+
+def test_large_properties_1e9():
+    """Size-independent properties at the headline size (C3 recipe, N=1e9)."""
+    n = 1_000_000_000
+    g = torch.Generator(device=DEV).manual_seed(3)
+    y = torch.randn(n, device=DEV, dtype=torch.float32, generator=g)
+    x = torch.arange(n, device=DEV, dtype=torch.int64)
+    out = mm.minmaxlttb(x, y, 2000, minmax_ratio=4)
+    o = out.cpu().numpy()
+    assert o.shape == (2000,) and o[0] == 0 and o[-1] == n - 1 and np.all(np.diff(o) > 0)
+    # the preselected set contains the global extrema (every LTTB pick comes from it)
+    pre = mm.minmax_preselect(x, y, 2000, 4)
+    p = pre.cpu().numpy()
+    assert int(torch.argmin(y[1:-1])) + 1 in set(p.tolist())
+    assert set(o.tolist()) <= set(p.tolist())
+    # chunked oracle on the same data agrees exactly
+    yh = y.cpu().numpy()
+    assert np.array_equal(o, O.minmaxlttb_typed(np.arange(n, dtype=np.int64), yh, 2000, 4))

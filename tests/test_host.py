@@ -1,0 +1,154 @@
+"""CPU-only tests: the C-ABI library, host-side API logic and error parity.
+
+No GPU and no reference needed; expected values come from the golden files
+made by the reference (tests/golden/make_golden.py).
+"""
+import gzip
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2305_00332_b200 as mm
+from paper_2305_00332_b200 import _native, errors
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLD = ROOT / "tests" / "golden"
+
+
+def test_library_exports_every_header_symbol():
+    hdr = (ROOT / "include" / "mmlttb.h").read_text()
+    declared = set(re.findall(r"\b(mmlttb_\w+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    L = _native.load()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert declared == set(_native.EXPORTED)
+    assert L.mmlttb_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    so = _native.LIB_PATH
+    r = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True, text=True)
+    assert "sm_100a" in r.stdout
+
+
+def test_workspace_sizes_are_small_and_independent_of_n():
+    # P12 / SPEC acceptance #11: aux memory O(k + m), not O(N)
+    L = _native.load()
+    a = L.mmlttb_workspace_bytes(_native.OP_MINMAXLTTB, 1, 10_000_000, 2000, 4, _native.MM_F32)
+    b = L.mmlttb_workspace_bytes(_native.OP_MINMAXLTTB, 1, 1_000_000, 2000, 4, _native.MM_F32)
+    assert 0 < a < 4 << 20 and 0 < b < 4 << 20
+    assert abs(a - b) / b < 0.10
+
+
+def test_error_hierarchy_matches_reference_names():
+    for name in ("NonMonotonicX", "NonFiniteValue", "NOutOfRange", "BadPreselectionRatio", "InvalidPartition",
+                 "OddNOut", "NOutNotDivisibleBy4", "RatioTooLargeForSeries", "NotParallelizable"):
+        cls = getattr(errors, name)
+        assert issubclass(cls, errors.ValidationError) and issubclass(cls, ValueError)
+    assert issubclass(errors.OutOfMemory, errors.TsdownError)
+
+
+def test_partition_kats():
+    k = json.loads((GOLD / "kats.json").read_text())["partition"]
+    for key, b in k.items():
+        s, e, n = map(int, key.split(","))
+        assert mm.partition(s, e, n).boundaries.tolist() == b
+    with pytest.raises(errors.InvalidPartition):
+        mm.partition(0, 3, 4)
+    with pytest.raises(errors.InvalidPartition):
+        mm.partition(0, 3, 0)
+
+
+def test_partition_sizes_exhaustive():
+    for length in range(1, 120):
+        for k in range(1, length + 1):
+            s = mm.partition(5, 5 + length, k).sizes()
+            assert s.max() - s.min() <= 1 and s.sum() == length
+
+
+def test_timeseries_invariants():
+    with pytest.raises(errors.NonFiniteValue):
+        mm.TimeSeries([0, 1, 2], [0.0, np.nan, 1.0])
+    with pytest.raises(errors.NonFiniteValue):
+        mm.TimeSeries([0.0, np.inf, 2.0], [0.0, 1.0, 1.0])
+    with pytest.raises(errors.NonMonotonicX):
+        mm.TimeSeries([0, 2, 1], [1, 2, 3])
+    with pytest.raises(ValueError):
+        mm.TimeSeries([0, 1], [1, 2, 3])
+    with pytest.raises(ValueError):
+        mm.TimeSeries([0], [1])
+    with pytest.raises(ValueError):
+        mm.TimeSeries(np.zeros((2, 2)), np.zeros((2, 2)))
+    ts = mm.TimeSeries([0, 1, 1, 2], [1, 2, 3, 4])  # non-decreasing x is fine
+    assert len(ts) == 4 and ts.ys.dtype == np.float64  # ints -> float64 like core.py:49
+    assert mm.TimeSeries(np.arange(3), np.ones(3, np.float32)).ys.dtype == np.float32
+    with pytest.raises(AttributeError):
+        ts.foo = 1
+    big = np.array([2**53 + 1, 2**53], dtype=np.int64)  # equal once converted to f64
+    mm.TimeSeries(big, [0.0, 1.0])
+
+
+def _golden_config_cases():
+    with gzip.open(GOLD / "config_errors.json.gz", "rt") as f:
+        return json.load(f)
+
+
+def test_config_and_validate_parity():
+    rng = np.random.Generator(np.random.PCG64(77))
+    series = {}
+    for n in (3, 4, 5, 10, 57):
+        x = np.arange(n)
+        series[n] = mm.TimeSeries(x, rng.standard_normal(n))
+    for rec in _golden_config_cases():
+        args = (rec["algo"], rec["n_out"], rec["r_ps"], rec["parallel"], rec["threads"])
+        if "config_error" in rec:
+            with pytest.raises(Exception) as ei:
+                mm.DownsampleConfig(*args)
+            assert type(ei.value).__name__ == rec["config_error"], rec
+            continue
+        cfg = mm.DownsampleConfig(*args)
+        try:
+            mm.validate(series[rec["n"]], cfg)
+            got = "ok"
+        except errors.TsdownError as e:
+            got = type(e).__name__
+        assert got == rec["validate"], rec
+
+
+def test_checks_raise_before_any_device_work():
+    # argument errors surface in the reference's order even with no GPU
+    ts = mm.TimeSeries(np.arange(20), np.arange(20.0))
+    with pytest.raises(errors.NOutOfRange):
+        mm.minmaxlttb(ts, 2, 4)
+    with pytest.raises(errors.BadPreselectionRatio):
+        mm.minmaxlttb(ts, 5, 3)
+    with pytest.raises(errors.RatioTooLargeForSeries):
+        mm.minmaxlttb(ts, 10, 8)
+    with pytest.raises(errors.OddNOut):
+        mm.minmax(ts, 5)
+    with pytest.raises(errors.OddNOut):
+        mm.minmaxlttb(ts, 5, 1)
+    with pytest.raises(errors.NOutNotDivisibleBy4):
+        mm.m4(ts, 6)
+    with pytest.raises(errors.NOutOfRange):
+        mm.lttb(ts, 21)
+    with pytest.raises(errors.NotParallelizable):
+        mm.downsample(ts, mm.DownsampleConfig("lttb", 5, parallel=True))
+    with pytest.raises(ValueError):
+        mm.run_parallel(ts, mm.DownsampleConfig("minmax", 6))
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    ts = mm.TimeSeries(np.arange(20), np.arange(20.0))
+    with pytest.raises(errors.CudaError):
+        mm.minmaxlttb(ts, 6, 2)
+    with pytest.raises(errors.CudaError):
+        mm.lttb(np.arange(20), np.arange(20.0), 6)
