@@ -8,6 +8,7 @@
 #include <stdint.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -110,15 +111,66 @@ ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt) {
   return p;
 }
 
+// K1 buffers for nbt = B*nb buckets
+int64_t ex_ws(int64_t nbt, const ExPlan& p) {
+  int64_t b = up(nbt * (int64_t)sizeof(Ext)) + up(nbt);
+  if (p.Cmax > 1) b += up(nbt * p.Cmax * (int64_t)sizeof(Partial)) + up(nbt * 4);
+  return b;
+}
+
+bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
+  a.ext = cv.take<Ext>(nbt);
+  a.cnt8 = cv.take<unsigned char>(nbt);
+  a.part = nullptr;
+  a.arrivals = nullptr;
+  if (p.Cmax > 1) {
+    a.part = cv.take<Partial>(nbt * p.Cmax);
+    a.arrivals = cv.take<unsigned>(nbt);
+  }
+  return cv.ok;
+}
+
 int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
   const int64_t warps = a.B * a.nb * a.C;
+  if (a.C > 1 && cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
+    return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
   const int64_t blocks = cdiv(warps, 8);
   if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
   if (a.chunk >= (1LL << 30)) return fail(MM_ERANGE, "bucket chunk too large");
-  if (ydt == MM_F32)
-    k_extrema<float, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
-  else
-    k_extrema<double, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
+  static const int variant = [] {
+    const char* e = getenv("MMLTTB_K1_VARIANT");  // tuning knob, default = tuned choice
+    return e ? atoi(e) : 0;
+  }();
+  const unsigned g = (unsigned)blocks;
+#define MM_K1(T, U, L) k_extrema<T, U, L><<<g, 256, 0, st>>>(a)
+#define MM_K1B(T, U, L, MB) k_extrema<T, U, L, MB><<<g, 256, 0, st>>>(a)
+  if (ydt == MM_F32) {
+    switch (variant) {
+      case 1: MM_K1(float, 4, 1); break;
+      case 2: MM_K1(float, 4, 2); break;
+      case 3: MM_K1(float, 4, 3); break;
+      case 4: MM_K1(float, 8, 0); break;
+      case 5: MM_K1(float, 8, 1); break;
+      case 6: MM_K1(float, 8, 3); break;
+      case 7: MM_K1(float, 2, 1); break;
+      case 8: MM_K1B(float, 4, 2, 6); break;
+      case 9: MM_K1B(float, 4, 3, 6); break;
+      case 10: MM_K1B(float, 2, 2, 8); break;
+      case 11: MM_K1B(float, 8, 2, 4); break;
+      case 12: MM_K1(float, 4, 0); break;
+      default: MM_K1(float, 8, 3); break;  // tuned: U=8 vectors in flight, evict-first
+    }
+  } else {
+    switch (variant) {
+      case 1: MM_K1(double, 4, 1); break;
+      case 4: MM_K1(double, 8, 0); break;
+      case 5: MM_K1(double, 8, 1); break;
+      case 12: MM_K1(double, 4, 0); break;
+      default: MM_K1(double, 8, 3); break;
+    }
+  }
+#undef MM_K1
+#undef MM_K1B
   return check_launch("k_extrema");
 }
 
@@ -170,9 +222,14 @@ int launch_tables_jump(LttbArgs a, cudaStream_t st) {
   k_lttb_tables<XT, YT, SMAX, NBB><<<g, NT, 0, st>>>(a);
   int rc = check_launch("k_lttb_tables");
   if (rc) return rc;
-  if ((rc = jump_attr<SMAX>())) return rc;
-  k_lttb_jump<SMAX><<<(unsigned)a.B, 1024, (size_t)jump_smem(k3, SMAX), st>>>(a);
-  return check_launch("k_lttb_jump");
+  if constexpr (SMAX <= 8) {
+    k_lttb_scan<SMAX, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
+    return check_launch("k_lttb_scan");
+  } else {
+    if ((rc = jump_attr<SMAX>())) return rc;
+    k_lttb_jump<SMAX><<<(unsigned)a.B, 1024, (size_t)jump_smem(k3, SMAX), st>>>(a);
+    return check_launch("k_lttb_jump");
+  }
 }
 
 template <typename XT, typename YT>
@@ -223,9 +280,32 @@ int64_t preselect_ws(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt,
   const int64_t S = cdiv(N - 2, k);
   const ExPlan p = plan_extrema(B * k, S, ydt);
   const int64_t cap = 2 + 2 * k;
-  int64_t bytes = up(B * k * p.Cmax * (int64_t)sizeof(Partial)) + up(B * 8);
+  int64_t bytes = ex_ws(B * k, p) + up(B * 8);
   if (with_lttb) bytes += 3 * up(B * cap * 8) + lttb_ws(B, n_out, r_ps);
   return bytes;
+}
+
+constexpr int PAIR_NT = 128, PAIR_ITEMS = 2;
+
+template <typename XT, typename YT>
+void pairs_t(const PairArgs& pa, dim3 g, cudaStream_t st) {
+  k_compact_pairs<XT, YT, PAIR_NT, PAIR_ITEMS><<<g, PAIR_NT, 0, st>>>(pa);
+}
+
+// K2 launch; pa.out_x == null means no gather (x/y dtypes then irrelevant)
+int launch_pairs(PairArgs pa, int64_t B, cudaStream_t st) {
+  const int64_t tiles = std::max<int64_t>(1, cdiv(pa.nb, PAIR_NT * PAIR_ITEMS));
+  if (B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
+  const dim3 g((unsigned)tiles, (unsigned)B);
+  if (!pa.out_x) { pa.x = pa.y = nullptr; pairs_t<double, double>(pa, g, st); return check_launch("k_compact_pairs"); }
+  const bool y32 = pa.ydt == MM_F32;
+  switch (pa.xdt) {
+    case MM_F32: y32 ? pairs_t<float, float>(pa, g, st) : pairs_t<float, double>(pa, g, st); break;
+    case MM_F64: y32 ? pairs_t<double, float>(pa, g, st) : pairs_t<double, double>(pa, g, st); break;
+    case MM_I64: y32 ? pairs_t<long long, float>(pa, g, st) : pairs_t<long long, double>(pa, g, st); break;
+    default: y32 ? pairs_t<int, float>(pa, g, st) : pairs_t<int, double>(pa, g, st); break;
+  }
+  return check_launch("k_compact_pairs");
 }
 
 int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
@@ -284,8 +364,7 @@ int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int6
     case MM_OP_M4: {
       const int64_t k = op == MM_OP_MINMAX ? n_out / 2 : n_out / 4;
       if (k < 1) return 0;
-      const ExPlan p = plan_extrema(B * k, cdiv(N, k), y_dtype);
-      return up(B * k * p.Cmax * (int64_t)sizeof(Partial));
+      return ex_ws(B * k, plan_extrema(B * k, cdiv(N, k), y_dtype));
     }
   }
   return 0;
@@ -305,17 +384,14 @@ int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B,
   const int64_t S = cdiv(N - 2, k);
   const ExPlan p = plan_extrema(B * k, S, y_dtype);
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(B * k * p.Cmax);
-  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
-  ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk, part};
+  ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
+  if (!carve_ex(cv, B * k, p, ea)) return fail(MM_EWORKSPACE, "workspace too small");
   if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
-  CompactArgs ca{};
-  ca.part = part; ca.nb = k; ca.C = p.C; ca.mode = 0;
-  ca.emit_first = 0; ca.emit_last = N - 1; ca.force_n_out = 0; ca.last_index = N - 1;
-  ca.start = 1; ca.len = N - 2; ca.k = k; ca.b0 = 0;
-  ca.out_idx = out; ca.out_ld = out_ld; ca.out_count = out_count;
-  k_compact<512><<<(unsigned)B, 512, 0, st>>>(ca);
-  return check_launch("k_compact");
+  PairArgs pa{};
+  pa.ext = ea.ext; pa.cnt8 = ea.cnt8; pa.nb = k;
+  pa.emit_first = 0; pa.emit_last = N - 1;
+  pa.out_idx = out; pa.out_ld = out_ld; pa.out_count = out_count;
+  return launch_pairs(pa, B, st);
 }
 
 static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int m4,
@@ -328,12 +404,18 @@ static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t 
   if (!mul_ok(k + 1, N)) return fail(MM_ERANGE, "k*N overflows int64");
   const ExPlan p = plan_extrema(B * k, cdiv(N, k), ydt);
   Carve cv{(char*)ws, wsb};
-  Partial* part = cv.take<Partial>(B * k * p.Cmax);
-  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
-  ExArgs ea{y, y_ld, B, 0, N, k, nullptr, 0, k, p.C, p.chunk, part};
+  ExArgs ea{y, y_ld, B, 0, N, k, nullptr, 0, k, p.C, p.chunk};
+  if (!carve_ex(cv, B * k, p, ea)) return fail(MM_EWORKSPACE, "workspace too small");
   if ((rc = launch_extrema(ea, ydt, st))) return rc;
+  if (!m4 && force_n_out == 0) {
+    PairArgs pa{};
+    pa.ext = ea.ext; pa.cnt8 = ea.cnt8; pa.nb = k;
+    pa.emit_first = -1; pa.emit_last = -1;
+    pa.out_idx = out; pa.out_ld = n_out; pa.out_count = out_count;
+    return launch_pairs(pa, B, st);
+  }
   CompactArgs ca{};
-  ca.part = part; ca.nb = k; ca.C = p.C; ca.mode = m4 ? 1 : 0;
+  ca.ext = ea.ext; ca.nb = k; ca.mode = m4 ? 1 : 0;
   ca.emit_first = -1; ca.emit_last = -1; ca.force_n_out = force_n_out; ca.last_index = N - 1;
   ca.start = 0; ca.len = N; ca.k = k; ca.b0 = 0;
   ca.out_idx = out; ca.out_ld = n_out; ca.out_count = out_count;
@@ -372,7 +454,8 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   const ExPlan p = plan_extrema(B * k, S, y_dtype);
   const int64_t cap = 2 + 2 * k;
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(B * k * p.Cmax);
+  ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
+  carve_ex(cv, B * k, p, ea);
   int64_t* cnt = cv.take<int64_t>(B);
   int64_t* pre = cv.take<int64_t>(B * cap);
   double* px = cv.take<double>(B * cap);
@@ -380,21 +463,18 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   unsigned char* lt = cv.take<unsigned char>(lttb_ws(B, n_out, r_ps));
   if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small (%lld bytes)", (long long)workspace_bytes);
   // K1: sub-bucket extrema over partition(1, N-1, k)  (downsamplers.py:149-155)
-  ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk, part};
   stage_mark(st, 0);
   if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
   stage_mark(st, 1);
   // K2: [0] + interleaved pairs + [N-1], gathered as f64 (:156-160, :207)
-  CompactArgs ca{};
-  ca.part = part; ca.nb = k; ca.C = p.C; ca.mode = 0;
-  ca.emit_first = 0; ca.emit_last = N - 1; ca.force_n_out = 0; ca.last_index = N - 1;
-  ca.start = 1; ca.len = N - 2; ca.k = k; ca.b0 = 0;
-  ca.out_idx = pre; ca.out_ld = cap; ca.out_count = cnt;
-  ca.x = x; ca.xdt = x_dtype; ca.x_ld = x_ld; ca.x_off = 0;
-  ca.y = y; ca.ydt = y_dtype; ca.y_ld = y_ld; ca.y_off = 0;
-  ca.out_x = px; ca.out_y = py;
-  k_compact<512><<<(unsigned)B, 512, 0, st>>>(ca);
-  if ((rc = check_launch("k_compact"))) return rc;
+  PairArgs pa{};
+  pa.ext = ea.ext; pa.cnt8 = ea.cnt8; pa.nb = k;
+  pa.emit_first = 0; pa.emit_last = N - 1;
+  pa.out_idx = pre; pa.out_ld = cap; pa.out_count = cnt;
+  pa.x = x; pa.xdt = x_dtype; pa.x_ld = x_ld;
+  pa.y = y; pa.ydt = y_dtype; pa.y_ld = y_ld;
+  pa.out_x = px; pa.out_y = py;
+  if ((rc = launch_pairs(pa, B, st))) return rc;
   stage_mark(st, 2);
   // K3: LTTB over the compacted sub-series, mapped back (:208-209)
   LttbArgs la{};
@@ -433,8 +513,7 @@ int mmlttb_every_nth(int64_t N, int64_t n_out, int64_t* out, void* stream) {
 
 int64_t mmlttb_extrema_workspace_bytes(int64_t k, int64_t max_bucket_len) {
   (void)max_bucket_len;
-  const ExPlan p = plan_extrema(k, 1, MM_F32);
-  return up(k * p.Cmax * (int64_t)sizeof(Partial));
+  return ex_ws(k, plan_extrema(k, 1, MM_F32));
 }
 
 int mmlttb_extrema_by_bucket(const void* y, int y_dtype, const int64_t* bounds, int64_t k, int64_t max_bucket_len,
@@ -444,12 +523,11 @@ int mmlttb_extrema_by_bucket(const void* y, int y_dtype, const int64_t* bounds, 
   cudaStream_t st = (cudaStream_t)stream;
   const ExPlan p = plan_extrema(k, max_bucket_len, y_dtype);
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(k * p.Cmax);
-  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
-  ExArgs ea{y, 0, 1, 0, 1, 1, bounds, 0, k, p.C, p.chunk, part};
+  ExArgs ea{y, 0, 1, 0, 1, 1, bounds, 0, k, p.C, p.chunk};
+  if (!carve_ex(cv, k, p, ea)) return fail(MM_EWORKSPACE, "workspace too small");
   int rc = launch_extrema(ea, y_dtype, st);
   if (rc) return rc;
-  k_finalize_extrema<<<(unsigned)cdiv(k, 256), 256, 0, st>>>(part, k, p.C, out_min, out_max);
+  k_finalize_extrema<<<(unsigned)cdiv(k, 256), 256, 0, st>>>(ea.ext, k, out_min, out_max);
   return check_launch("k_finalize_extrema");
 }
 
@@ -473,8 +551,7 @@ int mmlttb_lttb_select(const void* xs, int x_dtype, const void* ys, int y_dtype,
 int64_t mmlttb_shard_workspace_bytes(int64_t N, int64_t n_out, int64_t r_ps, int64_t b0, int64_t b1) {
   const int64_t k = (n_out - 2) * (r_ps / 2);
   if (k < 1 || b1 <= b0) return ALIGN;
-  const ExPlan p = plan_extrema(b1 - b0, cdiv(N - 2, k), MM_F32);
-  return up((b1 - b0) * p.Cmax * (int64_t)sizeof(Partial));
+  return ex_ws(b1 - b0, plan_extrema(b1 - b0, cdiv(N - 2, k), MM_F32));
 }
 
 int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard, int y_dtype, int64_t lo, int64_t N,
@@ -490,28 +567,22 @@ int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard
   if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nb = b1 - b0;
-  const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(std::max<int64_t>(nb, 1), S, y_dtype);
+  const ExPlan p = plan_extrema(std::max<int64_t>(nb, 1), cdiv(N - 2, k), y_dtype);
   Carve cv{(char*)workspace, workspace_bytes};
-  Partial* part = cv.take<Partial>(std::max<int64_t>(nb, 1) * p.Cmax);
-  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
   // virtual base: element i of the global series lives at y_shard[i - lo]
   const void* ybase = (const char*)y_shard - lo * esize(y_dtype);
-  if (nb > 0) {
-    ExArgs ea{ybase, 0, 1, 1, N - 2, k, nullptr, b0, nb, p.C, p.chunk, part};
-    if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
-  }
-  CompactArgs ca{};
-  ca.part = part; ca.nb = nb; ca.C = p.C; ca.mode = 0;
-  ca.emit_first = emit_first ? 0 : -1; ca.emit_last = emit_last ? N - 1 : -1;
-  ca.force_n_out = 0; ca.last_index = N - 1;
-  ca.start = 1; ca.len = N - 2; ca.k = k; ca.b0 = b0;
-  ca.out_idx = out_idx; ca.out_ld = 0; ca.out_count = out_count;
-  ca.x = x_shard; ca.xdt = x_dtype; ca.x_ld = 0; ca.x_off = lo;
-  ca.y = y_shard; ca.ydt = y_dtype; ca.y_ld = 0; ca.y_off = lo;
-  ca.out_x = out_x; ca.out_y = out_y;
-  k_compact<512><<<1, 512, 0, st>>>(ca);
-  return check_launch("k_compact(shard)");
+  const void* xbase = (const char*)x_shard - lo * esize(x_dtype);
+  ExArgs ea{ybase, 0, 1, 1, N - 2, k, nullptr, b0, nb, p.C, p.chunk};
+  if (!carve_ex(cv, std::max<int64_t>(nb, 1), p, ea)) return fail(MM_EWORKSPACE, "workspace too small");
+  if (nb > 0 && (rc = launch_extrema(ea, y_dtype, st))) return rc;
+  PairArgs pa{};
+  pa.ext = ea.ext; pa.cnt8 = ea.cnt8; pa.nb = nb;
+  pa.emit_first = emit_first ? 0 : -1; pa.emit_last = emit_last ? N - 1 : -1;
+  pa.out_idx = out_idx; pa.out_ld = 0; pa.out_count = out_count;
+  pa.x = xbase; pa.xdt = x_dtype; pa.x_ld = 0;
+  pa.y = ybase; pa.ydt = y_dtype; pa.y_ld = 0;
+  pa.out_x = out_x; pa.out_y = out_y;
+  return launch_pairs(pa, 1, st);
 }
 
 int mmlttb_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts, int64_t G,

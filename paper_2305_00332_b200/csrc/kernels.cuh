@@ -22,6 +22,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <limits.h>
 
 namespace mm {
 
@@ -39,11 +40,23 @@ __device__ __forceinline__ long long key64(unsigned long long u) {
   return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
 }
 
+// 16-byte streaming loads; LDV picks the cache policy (tuned on B200, see
+// 0 = nc + no L1 allocate + 256B L2 prefetch, 1 = nc + no L1
+// allocate, 2 = plain nc (__ldg), 3 = evict-first streaming (__ldcs)).
+template <int LDV>
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  if constexpr (LDV == 0) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  } else if constexpr (LDV == 1) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  } else if constexpr (LDV == 2) {
+    r = __ldg(p);
+  } else {
+    r = __ldcs(p);
+  }
   return r;
 }
 
@@ -87,6 +100,7 @@ struct Partial {
   long long imin, imax;  // element index (INT64_MAX = none)
 };
 
+struct Ext;
 struct ExArgs {
   const void* y;
   int64_t y_ld;
@@ -95,7 +109,14 @@ struct ExArgs {
   const int64_t* bounds;   // or explicit bounds (k+1 entries), shared by all series
   int64_t b0, nb;          // buckets [b0, b0+nb) of every series
   int64_t C, chunk;        // chunks per bucket, chunk length (elements)
-  Partial* part;           // [B][nb][C]
+  Partial* part;           // [B][nb][C]   chunk partials (C > 1 only)
+  unsigned* arrivals;      // [B][nb]      zeroed per call (C > 1 only)
+  struct Ext* ext;         // [B][nb]      final (imin, imax) per bucket
+  unsigned char* cnt8;     // [B][nb]      1 + (imin != imax): K2's scan input
+};
+
+struct Ext {
+  long long imin, imax;
 };
 
 __device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k, int64_t b) {
@@ -109,8 +130,8 @@ __device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k,
 // from that vector at the end, then reduce (key, index) lexicographically
 // across the warp -- the same first-occurrence argmin/argmax as
 // _argminmax_range (_kernels.py:28-60) independent of evaluation order.
-template <typename T, int U>
-__global__ void __launch_bounds__(256) k_extrema(ExArgs a) {
+template <typename T, int U, int LDV, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
   typedef YTr<T> Tr;
   typedef typename Tr::K K;
   const int lane = threadIdx.x & 31;
@@ -133,27 +154,32 @@ __global__ void __launch_bounds__(256) k_extrema(ExArgs a) {
   const int64_t hi = min(bhi, lo + a.chunk);
   const T* y = (const T*)a.y + s * a.y_ld;
 
+  // Offsets are int32 relative to the chunk start (host keeps chunk < 2^30).
+  // When a vector improves the running extreme its raw 16 bytes are kept in
+  // registers, so the exact element is recovered without re-reading memory
+  // (a re-read would miss L2 on a 4 GB stream and cost extra DRAM traffic).
   K mn = Tr::kmax(), mx = Tr::kmin();
-  int64_t pmn = INT64_MAX, pmx = INT64_MAX;
+  int omn = INT_MAX, omx = INT_MAX;
   bool vmn = false, vmx = false;
+  uint4 rmn = make_uint4(0, 0, 0, 0), rmx = make_uint4(0, 0, 0, 0);
   if (lo < hi) {
     const int n = (int)(hi - lo);
-    const uintptr_t addr = (uintptr_t)(y + lo);
+    const T* base = y + lo;
+    const uintptr_t addr = (uintptr_t)base;
     int head = (int)(((16u - (unsigned)(addr & 15u)) & 15u) / sizeof(T));
     if (head > n) head = n;
     if (lane < head) {
-      const K kk = Tr::key(y + lo + lane);
-      mn = kk; mx = kk; pmn = pmx = lo + lane;
+      const K kk = Tr::key(base + lane);
+      mn = kk; mx = kk; omn = omx = lane;
     }
-    const int64_t vstart = lo + head;
     const int nvec = (n - head) / Tr::VEC;
-    const uint4* vp = reinterpret_cast<const uint4*>(y + vstart);
+    const uint4* vp = reinterpret_cast<const uint4*>(base + head);
     for (int v0 = 0; v0 < nvec; v0 += 32 * U) {
       uint4 r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32 + lane;
-        if (v < nvec) r[u] = ld_stream(vp + v);
+        if (v < nvec) r[u] = ld_stream<LDV>(vp + v);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -164,61 +190,93 @@ __global__ void __launch_bounds__(256) k_extrema(ExArgs a) {
           K vl = kk[0], vh = kk[0];
 #pragma unroll
           for (int e = 1; e < Tr::VEC; ++e) { vl = min(vl, kk[e]); vh = max(vh, kk[e]); }
-          if (vl < mn) { mn = vl; pmn = vstart + (int64_t)v * Tr::VEC; vmn = true; }
-          if (vh > mx) { mx = vh; pmx = vstart + (int64_t)v * Tr::VEC; vmx = true; }
+          if (vl < mn) { mn = vl; omn = head + v * Tr::VEC; vmn = true; rmn = r[u]; }
+          if (vh > mx) { mx = vh; omx = head + v * Tr::VEC; vmx = true; rmx = r[u]; }
         }
       }
     }
-    const int64_t tp = vstart + (int64_t)nvec * Tr::VEC + lane;
-    if (tp < hi) {
-      const K kk = Tr::key(y + tp);
-      if (kk < mn) { mn = kk; pmn = tp; vmn = false; }
-      if (kk > mx) { mx = kk; pmx = tp; vmx = false; }
+    const int tp = head + nvec * Tr::VEC + lane;
+    if (tp < n) {
+      const K kk = Tr::key(base + tp);
+      if (kk < mn) { mn = kk; omn = tp; vmn = false; }
+      if (kk > mx) { mx = kk; omx = tp; vmx = false; }
     }
     // exact element inside the winning vector: first component with the key
     if (vmn) {
       K kk[Tr::VEC];
-      Tr::keys(__ldg(reinterpret_cast<const uint4*>(y + pmn)), kk);
+      Tr::keys(rmn, kk);
       int e = Tr::VEC - 1;
 #pragma unroll
       for (int q = Tr::VEC - 1; q >= 0; --q) if (kk[q] == mn) e = q;
-      pmn += e;
+      omn += e;
     }
     if (vmx) {
       K kk[Tr::VEC];
-      Tr::keys(__ldg(reinterpret_cast<const uint4*>(y + pmx)), kk);
+      Tr::keys(rmx, kk);
       int e = Tr::VEC - 1;
 #pragma unroll
       for (int q = Tr::VEC - 1; q >= 0; --q) if (kk[q] == mx) e = q;
-      pmx += e;
+      omx += e;
     }
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
-    const K omn = __shfl_xor_sync(FULL, mn, off);
-    const int64_t opmn = __shfl_xor_sync(FULL, pmn, off);
-    if (omn < mn || (omn == mn && opmn < pmn)) { mn = omn; pmn = opmn; }
-    const K omx = __shfl_xor_sync(FULL, mx, off);
-    const int64_t opmx = __shfl_xor_sync(FULL, pmx, off);
-    if (omx > mx || (omx == mx && opmx < pmx)) { mx = omx; pmx = opmx; }
+    const K omn2 = __shfl_xor_sync(FULL, mn, off);
+    const int oo = __shfl_xor_sync(FULL, omn, off);
+    if (omn2 < mn || (omn2 == mn && oo < omn)) { mn = omn2; omn = oo; }
+    const K omx2 = __shfl_xor_sync(FULL, mx, off);
+    const int oq = __shfl_xor_sync(FULL, omx, off);
+    if (omx2 > mx || (omx2 == mx && oq < omx)) { mx = omx2; omx = oq; }
   }
+  const int64_t pmn = omn == INT_MAX ? INT64_MAX : lo + omn;
+  const int64_t pmx = omx == INT_MAX ? INT64_MAX : lo + omx;
+  // publish: one chunk per bucket -> final; otherwise the last-arriving warp
+  // of the bucket combines all C partials (threadfence-reduction pattern), so
+  // no separate combine pass and no single-CTA bottleneck downstream.
+  const int64_t bkt = t;  // s * nb + (b - b0)
+  if (a.C == 1) {
+    if (lane == 0) {
+      a.ext[bkt].imin = pmn;
+      a.ext[bkt].imax = pmx;
+      a.cnt8[bkt] = (unsigned char)(pmn != pmx ? 2 : 1);
+    }
+    return;
+  }
+  unsigned last = 0;
   if (lane == 0) {
     Partial p;
     p.kmin = (long long)mn; p.kmax = (long long)mx; p.imin = pmn; p.imax = pmx;
     a.part[w] = p;
+    __threadfence();
+    last = atomicAdd(&a.arrivals[bkt], 1u) == (unsigned)(a.C - 1);
   }
-}
-
-// combine the C chunk partials of one bucket (lexicographic, order-free)
-__device__ __forceinline__ void combine(const Partial* p, int64_t C, int64_t& imin, int64_t& imax) {
-  Partial r = p[0];
-  for (int64_t c = 1; c < C; ++c) {
-    const Partial q = p[c];
-    if (q.kmin < r.kmin || (q.kmin == r.kmin && q.imin < r.imin)) { r.kmin = q.kmin; r.imin = q.imin; }
-    if (q.kmax > r.kmax || (q.kmax == r.kmax && q.imax < r.imax)) { r.kmax = q.kmax; r.imax = q.imax; }
+  last = __shfl_sync(FULL, last, 0);
+  if (!last) return;
+  __threadfence();
+  long long cmn = LLONG_MAX, cmx = LLONG_MIN;
+  int64_t cimn = INT64_MAX, cimx = INT64_MAX;
+  const Partial* pp = a.part + bkt * a.C;
+  for (int64_t c2 = lane; c2 < a.C; c2 += 32) {
+    const long long kmn = __ldcg(&pp[c2].kmin), kmx = __ldcg(&pp[c2].kmax);
+    const long long qmn = __ldcg(&pp[c2].imin), qmx = __ldcg(&pp[c2].imax);
+    if (kmn < cmn || (kmn == cmn && qmn < cimn)) { cmn = kmn; cimn = qmn; }
+    if (kmx > cmx || (kmx == cmx && qmx < cimx)) { cmx = kmx; cimx = qmx; }
   }
-  imin = r.imin;
-  imax = r.imax;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const long long omn = __shfl_xor_sync(FULL, cmn, off);
+    const int64_t oimn = __shfl_xor_sync(FULL, cimn, off);
+    if (omn < cmn || (omn == cmn && oimn < cimn)) { cmn = omn; cimn = oimn; }
+    const long long omx = __shfl_xor_sync(FULL, cmx, off);
+    const int64_t oimx = __shfl_xor_sync(FULL, cimx, off);
+    if (omx > cmx || (omx == cmx && oimx < cimx)) { cmx = omx; cimx = oimx; }
+  }
+  if (lane == 0) {
+    a.ext[bkt].imin = cimn;
+    a.ext[bkt].imax = cimx;
+    a.cnt8[bkt] = (unsigned char)(cimn != cimx ? 2 : 1);
+    a.arrivals[bkt] = 0;  // leave the counter reusable
+  }
 }
 
 // ---------------------------------------------------- block scan helper --
@@ -251,8 +309,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int& total, int* sh /* >= 
 
 // ---------------------------------------------------------- K2 compact ---
 struct CompactArgs {
-  const Partial* part;
-  int64_t nb, C;            // per series: nb buckets x C chunks
+  const Ext* ext;
+  int64_t nb;               // per series: nb buckets
   int mode;                 // 0: minmax pairs, 1: m4 quads
   int64_t emit_first;       // index emitted before everything (-1: none)
   int64_t emit_last;        // index emitted after everything (-1: none)
@@ -282,7 +340,7 @@ __global__ void __launch_bounds__(NT) k_compact(CompactArgs a) {
   __shared__ int sh[NT / 32 + 1];
   __shared__ long long s_first, s_last, s_m;
   const int64_t s = blockIdx.x;
-  const Partial* part = a.part + s * a.nb * a.C;
+  const Ext* ext = a.ext + s * a.nb;
   int64_t* out = a.out_idx + s * a.out_ld;
   double* ox = a.out_x ? a.out_x + s * a.out_ld : nullptr;
   double* oy = a.out_y ? a.out_y + s * a.out_ld : nullptr;
@@ -295,8 +353,7 @@ __global__ void __launch_bounds__(NT) k_compact(CompactArgs a) {
     if (oy) oy[pos] = load_any(ys, a.ydt, idx - a.y_off);
   };
   auto items_of = [&](int64_t bl, int64_t* it) -> int {
-    int64_t imin, imax;
-    combine(part + bl * a.C, a.C, imin, imax);
+    const int64_t imin = ext[bl].imin, imax = ext[bl].imax;
     const int64_t lo = min(imin, imax), hi = max(imin, imax);
     if (a.mode == 0) {  // downsamplers.py:60-69
       it[0] = lo; it[1] = hi;
@@ -365,13 +422,108 @@ __global__ void __launch_bounds__(NT) k_compact(CompactArgs a) {
 }
 
 // extrema-only finalize for the _extrema_by_bucket entry point
-__global__ void k_finalize_extrema(const Partial* part, int64_t k, int64_t C, int64_t* out_min, int64_t* out_max) {
+__global__ void k_finalize_extrema(const Ext* ext, int64_t k, int64_t* out_min, int64_t* out_max) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= k) return;
-  int64_t a, c;
-  combine(part + b * C, C, a, c);
-  out_min[b] = a;
-  out_max[b] = c;
+  out_min[b] = ext[b].imin;
+  out_max[b] = ext[b].imax;
+}
+
+// K2 (hot path): multi-CTA compaction of (lo, hi) pairs.  CTA (tile, s)
+// owns TB = NT*ITEMS consecutive buckets of series s; its output offset is
+// the sum of the previous buckets' 1-byte counts (cnt8, written by K1), so
+// there is no inter-CTA handshake.  Each thread gathers its <= 2*ITEMS
+// preselected (x, y) values with all loads in flight together.
+struct PairArgs {
+  const Ext* ext;
+  const unsigned char* cnt8;
+  int64_t nb;
+  int64_t emit_first, emit_last;   // -1: none
+  int64_t* out_idx; int64_t out_ld; int64_t* out_count;
+  const void* x; int xdt; int64_t x_ld;
+  const void* y; int ydt; int64_t y_ld;
+  double* out_x; double* out_y;    // may be null (no gather)
+};
+
+template <typename XT, typename YT, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
+  __shared__ int sh[NT / 32 + 1];
+  __shared__ long long s_red[NT / 32];
+  constexpr int TB = NT * ITEMS;
+  const int64_t s = blockIdx.y;
+  const int64_t b_lo = (int64_t)blockIdx.x * TB;
+  const unsigned char* cnt = a.cnt8 + s * a.nb;
+  const Ext* ext = a.ext + s * a.nb;
+  // 1. offset of this tile = items of buckets [0, b_lo)
+  long long pre = 0;
+  for (int64_t i = threadIdx.x; i < b_lo; i += NT) pre += cnt[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(FULL, pre, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pre;
+  __syncthreads();
+  long long off = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) off += s_red[w];
+  // 2. this thread's buckets: slot 2i = lo, 2i+1 = hi (kept if != lo); all
+  //    indexing static so everything stays in registers
+  int64_t v[2 * ITEMS];
+  bool keep[2 * ITEMS];
+  int n = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t bl = b_lo + (int64_t)threadIdx.x * ITEMS + i;
+    const bool ok = bl < a.nb;
+    Ext e;
+    e.imin = e.imax = 0;
+    if (ok) e = ext[bl];
+    v[2 * i] = min(e.imin, e.imax);  // downsamplers.py:60-69
+    v[2 * i + 1] = max(e.imin, e.imax);
+    keep[2 * i] = ok;
+    keep[2 * i + 1] = ok && v[2 * i + 1] != v[2 * i];
+    n += (int)keep[2 * i] + (int)keep[2 * i + 1];
+  }
+  int tot;
+  const int ex = block_excl_scan<NT>(n, tot, sh);
+  const int64_t base = (a.emit_first >= 0 ? 1 : 0) + off + ex;
+  int64_t* out = a.out_idx + s * a.out_ld;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  if (a.out_x) {
+    // all 4*ITEMS gathers in flight at once (templated types: no per-load switch)
+    double gx[2 * ITEMS], gy[2 * ITEMS];
+#pragma unroll
+    for (int j = 0; j < 2 * ITEMS; ++j) {
+      const int64_t q = keep[j] ? v[j] : v[0] * 0;
+      gx[j] = keep[j] ? to_f64(xs, q) : 0.0;
+      gy[j] = keep[j] ? to_f64(ys, q) : 0.0;
+    }
+    int64_t pos = base;
+#pragma unroll
+    for (int j = 0; j < 2 * ITEMS; ++j)
+      if (keep[j]) { a.out_x[s * a.out_ld + pos] = gx[j]; a.out_y[s * a.out_ld + pos] = gy[j]; ++pos; }
+  }
+  {
+    int64_t pos = base;
+#pragma unroll
+    for (int j = 0; j < 2 * ITEMS; ++j)
+      if (keep[j]) out[pos++] = v[j];
+  }
+  // 3. endpoints (downsamplers.py:157-160) and the count
+  if (threadIdx.x == 0) {
+    auto emit = [&](int64_t pos, int64_t v) {
+      out[pos] = v;
+      if (a.out_x) {
+        a.out_x[s * a.out_ld + pos] = to_f64(xs, v);
+        a.out_y[s * a.out_ld + pos] = to_f64(ys, v);
+      }
+    };
+    if (blockIdx.x == 0 && a.emit_first >= 0) emit(0, a.emit_first);
+    if (blockIdx.x == gridDim.x - 1) {
+      int64_t end = (a.emit_first >= 0 ? 1 : 0) + off + tot;
+      if (a.emit_last >= 0) emit(end++, a.emit_last);
+      if (a.out_count) a.out_count[s] = end;
+    }
+  }
 }
 
 // -------------------------------------------------------------- LTTB -----
@@ -501,6 +653,107 @@ __global__ void __launch_bounds__(1024) k_lttb_jump(LttbArgs a) {
   for (int64_t b = threadIdx.x; b < k3; b += blockDim.x) {
     const int64_t pos = lbound(a, m, b) + A[b * SMAX];
     out[b + 1] = map ? map[pos] : pos;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = map ? map[0] : 0;
+    out[k3 + 1] = map ? map[m - 1] : m - 1;
+  }
+}
+
+// K3a, part 2 for buckets of <= 8 points: each transition table T_b is a
+// packed byte map (4 or 8 bytes) and composition is one or two PRMTs, so the
+// chain is resolved by a block-wide inclusive scan with the composition
+// operator (warp shuffles + one smem level) instead of log2(k3) smem rounds.
+// P_b = T_b o ... o T_0; P_b[0] is bucket b's pick (_kernels.py:108-119).
+template <int W> struct PMap;
+template <> struct PMap<4> {
+  uint32_t v;
+  static __device__ __forceinline__ PMap ident() { return {0x03020100u}; }
+  static __device__ __forceinline__ uint32_t sel(uint32_t f) {
+    return (f & 0xFu) | ((f >> 4) & 0xF0u) | ((f >> 8) & 0xF00u) | ((f >> 12) & 0xF000u);
+  }
+  // (g o f)[p] = g[f[p]]
+  static __device__ __forceinline__ PMap comp(PMap g, PMap f) { return {__byte_perm(g.v, 0u, sel(f.v))}; }
+  __device__ __forceinline__ int at0() const { return (int)(v & 0xFFu); }
+  __device__ __forceinline__ PMap shfl_up(int o) const { return {__shfl_up_sync(FULL, v, o)}; }
+  static __device__ __forceinline__ PMap load(const unsigned char* t) { return {*reinterpret_cast<const uint32_t*>(t)}; }
+};
+template <> struct PMap<8> {
+  uint32_t lo, hi;
+  static __device__ __forceinline__ PMap ident() { return {0x03020100u, 0x07060504u}; }
+  static __device__ __forceinline__ PMap comp(PMap g, PMap f) {
+    return {__byte_perm(g.lo, g.hi, PMap<4>::sel(f.lo)), __byte_perm(g.lo, g.hi, PMap<4>::sel(f.hi))};
+  }
+  __device__ __forceinline__ int at0() const { return (int)(lo & 0xFFu); }
+  __device__ __forceinline__ PMap shfl_up(int o) const {
+    return {__shfl_up_sync(FULL, lo, o), __shfl_up_sync(FULL, hi, o)};
+  }
+  static __device__ __forceinline__ PMap load(const unsigned char* t) {
+    const uint2 u = *reinterpret_cast<const uint2*>(t);
+    return {u.x, u.y};
+  }
+};
+
+template <int W, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
+  typedef PMap<W> M;
+  __shared__ M s_warp[NT / 32];
+  __shared__ M s_carry;
+  const int64_t s = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const unsigned char* tab = a.tables + s * a.tab_ld;
+  int64_t* out = a.out + s * a.n_out;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  M carry = M::ident();
+  for (int64_t c0 = 0; c0 < k3; c0 += (int64_t)NT * ITEMS) {
+    const int64_t b0 = c0 + (int64_t)threadIdx.x * ITEMS;
+    M t[ITEMS];
+    M agg = M::ident();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      t[i] = (b0 + i < k3) ? M::load(tab + (b0 + i) * W) : M::ident();
+      agg = M::comp(t[i], agg);
+    }
+    // warp inclusive scan of the per-thread aggregates (earlier lanes apply first)
+    M inc = agg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const M other = inc.shfl_up(o);
+      if (lane >= o) inc = M::comp(inc, other);
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      M w = lane < NT / 32 ? s_warp[lane] : M::ident();
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const M other = w.shfl_up(o);
+        if (lane >= o) w = M::comp(w, other);
+      }
+      if (lane < NT / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    // exclusive prefix of this thread = carry, then earlier warps, then earlier lanes
+    M pre = carry;
+    if (wid > 0) pre = M::comp(s_warp[wid - 1], pre);
+    const M lane_prev = inc.shfl_up(1);
+    if (lane > 0) pre = M::comp(lane_prev, pre);
+    M cur = pre;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t b = b0 + i;
+      cur = M::comp(t[i], cur);
+      if (b < k3) {
+        const int64_t pos = lbound(a, m, b) + cur.at0();
+        out[b + 1] = map ? map[pos] : pos;
+      }
+    }
+    if (threadIdx.x == NT - 1) s_carry = cur;
+    __syncthreads();
+    carry = s_carry;
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
     out[0] = map ? map[0] : 0;

@@ -277,3 +277,14 @@ def test_large_properties_1e9():
     # chunked oracle on the same data agrees exactly
     yh = y.cpu().numpy()
     assert np.array_equal(o, O.minmaxlttb_typed(np.arange(n, dtype=np.int64), yh, 2000, 4))
+
+
+@pytest.mark.parametrize("n_out,r", [(5000, 2), (5000, 4), (3001, 6), (3001, 8), (4500, 16), (2100, 32)])
+def test_lttb_scan_multi_chunk(n_out, r):
+    """k3 > 2048 buckets: several scan chunks with a carried prefix map."""
+    rng = np.random.Generator(np.random.PCG64(n_out + r))
+    n = 3_000_000
+    x = np.cumsum(rng.exponential(1.0, n))
+    y = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+    got = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out, minmax_ratio=r)
+    assert np.array_equal(got.cpu().numpy(), O.minmaxlttb(x, y, n_out, r))
