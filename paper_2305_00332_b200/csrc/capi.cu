@@ -97,16 +97,27 @@ struct ExPlan {
   int64_t C, chunk, Cmax;
 };
 
-// Chunks per bucket: enough warps to fill 148 SMs x 64 resident warps for
-// ~8 waves, never a chunk under MIN_CHUNK elements.  The partial buffer is
+// Chunks per bucket: enough warps for ~4 waves over 148 SMs x 32 resident
+// warps, never a chunk under MIN_CHUNK elements; buckets of <= 4096 points
+// are one item each (8-lane groups).  The partial buffer is
 // sized for Cmax, which depends only on the bucket count (not on N), so the
 // auxiliary memory stays O(B*k) (acceptance #11).
-constexpr int64_t WANT_WARPS = 148LL * 64 * 8;
+constexpr int64_t SMALL_BUCKET = 4096;  // elements: <= this -> one 8-lane group per bucket
+
+int64_t env_i64(const char* name, int64_t dflt) {
+  const char* e = getenv(name);  // tuning knobs for tools/k1_sweep.sh only
+  return e ? atoll(e) : dflt;
+}
+
 ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt) {
-  const int64_t min_chunk = ydt == MM_F32 ? 1024 : 512;
+  // tuned on B200 (tools/plan_sweep.sh): ~4 waves of 148 SMs x 32 resident
+  // warps, chunks of >= 4096 float32 elements
+  static const int64_t want = env_i64("MMLTTB_K1_WANT_WARPS", 148LL * 128);
+  static const int64_t minc32 = env_i64("MMLTTB_K1_MIN_CHUNK", 4096);
+  const int64_t min_chunk = ydt == MM_F32 ? minc32 : minc32 / 2;
   ExPlan p;
-  p.Cmax = std::max<int64_t>(1, std::min<int64_t>(256, cdiv(WANT_WARPS, std::max<int64_t>(1, buckets_total))));
-  p.C = std::max<int64_t>(1, std::min<int64_t>(p.Cmax, cdiv(max_bucket, min_chunk)));
+  p.Cmax = std::max<int64_t>(1, std::min<int64_t>(256, cdiv(want, std::max<int64_t>(1, buckets_total))));
+  p.C = max_bucket <= SMALL_BUCKET ? 1 : std::max<int64_t>(1, std::min<int64_t>(p.Cmax, cdiv(max_bucket, min_chunk)));
   p.chunk = cdiv(max_bucket, p.C);
   return p;
 }
@@ -131,6 +142,16 @@ bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
 }
 
 int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
+  const bool small = a.C == 1 && a.chunk <= SMALL_BUCKET;
+  if (small) {
+    const int64_t blocks = cdiv(a.B * a.nb, 8 * 4);
+    if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
+    if (ydt == MM_F32)
+      k_extrema<float, 8, 3, 1, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else
+      k_extrema<double, 8, 3, 1, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
+    return check_launch("k_extrema(small)");
+  }
   const int64_t warps = a.B * a.nb * a.C;
   if (a.C > 1 && cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
     return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");

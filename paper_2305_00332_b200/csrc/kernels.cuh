@@ -130,16 +130,21 @@ __device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k,
 // from that vector at the end, then reduce (key, index) lexicographically
 // across the warp -- the same first-occurrence argmin/argmax as
 // _argminmax_range (_kernels.py:28-60) independent of evaluation order.
-template <typename T, int U, int LDV, int MINB = 1>
+//
+// G < 32: a G-lane group per item (small buckets, C == 1): 32/G buckets per
+// warp, each group still reading G*16 contiguous bytes per load, so a warp's
+// fixed costs (bounds, reduction, stores) are shared by several buckets.
+template <typename T, int U, int LDV, int MINB = 1, int G = 32>
 __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
   typedef YTr<T> Tr;
   typedef typename Tr::K K;
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & (G - 1);  // lane within the item's group
+  const int64_t w = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G) + (threadIdx.x & 31) / G;
   const int64_t total = a.B * a.nb * a.C;
-  if (w >= total) return;  // warp-uniform
-  const int64_t c = w % a.C;
-  const int64_t t = w / a.C;
+  const bool live = w < total;
+  if (G == 32 && !live) return;  // warp-uniform
+  const int64_t c = live ? w % a.C : 0;
+  const int64_t t = live ? w / a.C : 0;
   const int64_t b = a.b0 + t % a.nb;
   const int64_t s = t / a.nb;
   int64_t blo, bhi;
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
     bhi = pbound(a.start, a.len, a.k, b + 1);
   }
   const int64_t lo = blo + c * a.chunk;
-  const int64_t hi = min(bhi, lo + a.chunk);
+  const int64_t hi = live ? min(bhi, lo + a.chunk) : lo;
   const T* y = (const T*)a.y + s * a.y_ld;
 
   // Offsets are int32 relative to the chunk start (host keeps chunk < 2^30).
@@ -174,16 +179,16 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
     }
     const int nvec = (n - head) / Tr::VEC;
     const uint4* vp = reinterpret_cast<const uint4*>(base + head);
-    for (int v0 = 0; v0 < nvec; v0 += 32 * U) {
+    for (int v0 = 0; v0 < nvec; v0 += G * U) {
       uint4 r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int v = v0 + u * 32 + lane;
+        const int v = v0 + u * G + lane;
         if (v < nvec) r[u] = ld_stream<LDV>(vp + v);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int v = v0 + u * 32 + lane;
+        const int v = v0 + u * G + lane;
         if (v < nvec) {
           K kk[Tr::VEC];
           Tr::keys(r[u], kk);
@@ -220,7 +225,7 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
     }
   }
 #pragma unroll
-  for (int off = 16; off; off >>= 1) {
+  for (int off = G / 2; off; off >>= 1) {
     const K omn2 = __shfl_xor_sync(FULL, mn, off);
     const int oo = __shfl_xor_sync(FULL, omn, off);
     if (omn2 < mn || (omn2 == mn && oo < omn)) { mn = omn2; omn = oo; }
@@ -234,8 +239,8 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
   // of the bucket combines all C partials (threadfence-reduction pattern), so
   // no separate combine pass and no single-CTA bottleneck downstream.
   const int64_t bkt = t;  // s * nb + (b - b0)
-  if (a.C == 1) {
-    if (lane == 0) {
+  if (G < 32 || a.C == 1) {  // (G < 32 is only launched with C == 1)
+    if (lane == 0 && live) {
       a.ext[bkt].imin = pmn;
       a.ext[bkt].imax = pmx;
       a.cnt8[bkt] = (unsigned char)(pmn != pmx ? 2 : 1);
