@@ -116,8 +116,19 @@ struct ExArgs {
 };
 
 struct Ext {
-  long long imin, imax;
+  long long imin, imax;  // first-occurrence argmin / argmax
+  long long kmin, kmax;  // their total-order keys: the key map is an involution,
+                         // so K2 recovers y[imin], y[imax] without a gather
 };
+
+// value of a total-order key (inverse of key32/key64: the same xor)
+template <typename T> __device__ __forceinline__ double key_value(long long k);
+template <> __device__ __forceinline__ double key_value<float>(long long k) {
+  return (double)__int_as_float(key32((uint32_t)(int32_t)k));
+}
+template <> __device__ __forceinline__ double key_value<double>(long long k) {
+  return __longlong_as_double(key64((unsigned long long)k));
+}
 
 __device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k, int64_t b) {
   return start + (b * len) / k;  // core.py:173 (host guarantees k*len < 2^63)
@@ -243,6 +254,8 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
     if (lane == 0 && live) {
       a.ext[bkt].imin = pmn;
       a.ext[bkt].imax = pmx;
+      a.ext[bkt].kmin = (long long)mn;
+      a.ext[bkt].kmax = (long long)mx;
       a.cnt8[bkt] = (unsigned char)(pmn != pmx ? 2 : 1);
     }
     return;
@@ -279,6 +292,8 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
   if (lane == 0) {
     a.ext[bkt].imin = cimn;
     a.ext[bkt].imax = cimx;
+    a.ext[bkt].kmin = cmn;
+    a.ext[bkt].kmax = cmx;
     a.cnt8[bkt] = (unsigned char)(cimn != cimx ? 2 : 1);
     a.arrivals[bkt] = 0;  // leave the counter reusable
   }
@@ -472,6 +487,7 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
   // 2. this thread's buckets: slot 2i = lo, 2i+1 = hi (kept if != lo); all
   //    indexing static so everything stays in registers
   int64_t v[2 * ITEMS];
+  long long kv[2 * ITEMS];
   bool keep[2 * ITEMS];
   int n = 0;
 #pragma unroll
@@ -479,10 +495,13 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
     const int64_t bl = b_lo + (int64_t)threadIdx.x * ITEMS + i;
     const bool ok = bl < a.nb;
     Ext e;
-    e.imin = e.imax = 0;
+    e.imin = e.imax = e.kmin = e.kmax = 0;
     if (ok) e = ext[bl];
-    v[2 * i] = min(e.imin, e.imax);  // downsamplers.py:60-69
-    v[2 * i + 1] = max(e.imin, e.imax);
+    const bool mfirst = e.imin <= e.imax;
+    v[2 * i] = mfirst ? e.imin : e.imax;  // downsamplers.py:60-69
+    v[2 * i + 1] = mfirst ? e.imax : e.imin;
+    kv[2 * i] = mfirst ? e.kmin : e.kmax;
+    kv[2 * i + 1] = mfirst ? e.kmax : e.kmin;
     keep[2 * i] = ok;
     keep[2 * i + 1] = ok && v[2 * i + 1] != v[2 * i];
     n += (int)keep[2 * i] + (int)keep[2 * i + 1];
@@ -498,9 +517,8 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
     double gx[2 * ITEMS], gy[2 * ITEMS];
 #pragma unroll
     for (int j = 0; j < 2 * ITEMS; ++j) {
-      const int64_t q = keep[j] ? v[j] : v[0] * 0;
-      gx[j] = keep[j] ? to_f64(xs, q) : 0.0;
-      gy[j] = keep[j] ? to_f64(ys, q) : 0.0;
+      gx[j] = keep[j] ? to_f64(xs, v[j]) : 0.0;
+      gy[j] = key_value<YT>(kv[j]);  // exact y[v[j]] from its key: no gather
     }
     int64_t pos = base;
 #pragma unroll

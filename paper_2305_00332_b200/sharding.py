@@ -1,0 +1,199 @@
+"""Multi-GPU MinMaxLTTB: one process per GPU over ``torch.distributed``.
+
+Two decompositions; the reference has no multi-device code,
+its only parallelism is numba ``prange`` over disjoint buckets
+(``_kernels.py:71-78``), and both paths below keep its output byte-identical.
+
+* **Batch sharding** (BASELINE.json C4): independent series, rank r owns rows
+  ``batch_range(B, r, G)``; no collective on the data path (an optional
+  ``all_gather`` assembles the [B, n_out] result).
+* **Bucket-range sharding of one series** (C5): rank r owns MinMax
+  sub-buckets ``[b0, b1)`` of ``partition(1, N-1, k)`` and exactly the y/x
+  elements they cover (rank 0 also element 0, rank G-1 also element N-1), so
+  no sub-bucket straddles ranks.  Each rank runs K1 + K2 on its shard
+  (``mmlttb_shard_preselect``), the small preselected sets (global index, x,
+  y as f64; <= 2*(b1-b0)+2 entries) are packed into one int64 buffer and
+  exchanged with ONE ``all_gather`` (NCCL over NVLink), every rank merges
+  them in rank order on the device (``mmlttb_merge_shards``) and runs the
+  LTTB stage on the merged set (``mmlttb_lttb_preselected``).  The exchanged
+  bytes are O(k), independent of N.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .downsamplers import Batch, _check_n_out, _check_preselect, _minmaxlttb_batch
+
+
+# ------------------------------------------------------------ batch path ----
+def batch_range(B: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [lo, hi) of a B-series batch owned by `rank` (balanced, contiguous)."""
+    return (B * rank) // world, (B * (rank + 1)) // world
+
+
+def minmaxlttb_batch_sharded(x, y_local, n_out: int, r_ps: int = 4, *, B: int | None = None,
+                             gather: bool = False, group=None):
+    """MinMaxLTTB over this rank's rows of a batch (no collective on the data path).
+
+    ``y_local``: this rank's [b, N] rows (see :func:`batch_range`).  With
+    ``gather=True`` the [B, n_out] result is all-gathered to every rank.
+    """
+    out = _minmaxlttb_batch(_prepared(x, y_local), n_out, r_ps)
+    if not gather:
+        return out
+    world = dist.get_world_size(group)
+    B = B if B is not None else out.shape[0] * world
+    per = -(-B // world)
+    buf = torch.full((per, n_out), -1, dtype=torch.int64, device=out.device)
+    buf[: out.shape[0]] = out
+    allb = torch.empty((world * per, n_out), dtype=torch.int64, device=out.device)
+    dist.all_gather_into_tensor(allb, buf, group=group)
+    rows = [allb[r * per: r * per + (batch_range(B, r, world)[1] - batch_range(B, r, world)[0])] for r in range(world)]
+    return torch.cat(rows, 0)
+
+
+def _prepared(x, y):
+    b = Batch(x, y)
+    b.squeeze = False
+    return b
+
+
+# ----------------------------------------------------- single-series path ---
+@dataclass(frozen=True)
+class Shard:
+    """What rank `rank` of `world` owns of one N-point series."""
+
+    rank: int
+    world: int
+    b0: int   # first MinMax sub-bucket (of k)
+    b1: int   # one past the last
+    lo: int   # first element index held by the rank
+    hi: int   # one past the last element index
+    k: int
+    cap: int  # fixed per-rank capacity of the exchanged preselected set
+
+    @property
+    def emit_first(self) -> bool:
+        return self.rank == 0
+
+    @property
+    def emit_last(self) -> bool:
+        return self.rank == self.world - 1
+
+
+def bucket_ranges(n: int, n_out: int, r_ps: int, world: int) -> list[Shard]:
+    """Bucket-range sharding plan of partition(1, N-1, k) over `world` ranks.
+
+    Rank r owns sub-buckets [floor(r*k/G), floor((r+1)*k/G)) and the elements
+    they cover -- index arithmetic only (core.py:173 closed form), x is never
+    consulted, so every rank's sub-buckets are exactly the reference's.
+    """
+    k = _check_preselect(n, n_out, r_ps)
+    L = n - 2
+
+    def bound(b):
+        return 1 + (b * L) // k
+
+    per = max((k * (r + 1)) // world - (k * r) // world for r in range(world))
+    cap = 2 * per + 2
+    out = []
+    for r in range(world):
+        b0, b1 = (k * r) // world, (k * (r + 1)) // world
+        lo = 0 if r == 0 else bound(b0)
+        hi = n if r == world - 1 else bound(b1)
+        out.append(Shard(r, world, b0, b1, lo, hi, k, cap))
+    return out
+
+
+def pack(idx: torch.Tensor, xs: torch.Tensor, ys: torch.Tensor, count: torch.Tensor, cap: int) -> torch.Tensor:
+    """One int64 message: [idx(cap) | x bits(cap) | y bits(cap) | count]."""
+    buf = torch.empty(3 * cap + 1, dtype=torch.int64, device=idx.device)
+    buf[:cap] = idx[:cap]
+    buf[cap:2 * cap] = xs[:cap].view(torch.int64)
+    buf[2 * cap:3 * cap] = ys[:cap].view(torch.int64)
+    buf[3 * cap:] = count.reshape(1)
+    return buf
+
+
+def unpack(allbuf: torch.Tensor, world: int, cap: int):
+    """Inverse of :func:`pack` over the all-gathered [world*(3cap+1)] buffer."""
+    m = allbuf.view(world, 3 * cap + 1)
+    idx = m[:, :cap].contiguous()
+    xs = m[:, cap:2 * cap].contiguous().view(torch.float64)
+    ys = m[:, 2 * cap:3 * cap].contiguous().view(torch.float64)
+    counts = m[:, 3 * cap].contiguous()
+    return idx, xs, ys, counts
+
+
+def exchange(buf: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """The one collective of the path: all_gather of the packed shard sets."""
+    allbuf = torch.empty(world * buf.numel(), dtype=buf.dtype, device=buf.device)
+    dist.all_gather_into_tensor(allbuf, buf, group=group)
+    return allbuf
+
+
+def shard_preselect(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out: int, r_ps: int, shard: Shard):
+    """K1 + K2 on this rank's elements -> (idx, x f64, y f64, count) on device."""
+    dev = y_shard.device
+    cap = shard.cap
+    idx = torch.empty(cap, dtype=torch.int64, device=dev)
+    xs = torch.empty(cap, dtype=torch.float64, device=dev)
+    ys = torch.empty(cap, dtype=torch.float64, device=dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    L = N.lib()
+    with torch.cuda.device(dev):
+        wsb = L.mmlttb_shard_workspace_bytes(n, n_out, r_ps, shard.b0, shard.b1)
+        ws = N.workspace(wsb, dev, n)
+        N.check(L.mmlttb_shard_preselect(x_shard.data_ptr(), N.DTYPE_CODE[x_shard.dtype], y_shard.data_ptr(),
+                                         N.DTYPE_CODE[y_shard.dtype], shard.lo, n, n_out, r_ps, shard.b0, shard.b1,
+                                         int(shard.emit_first), int(shard.emit_last), idx.data_ptr(), xs.data_ptr(),
+                                         ys.data_ptr(), cnt.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(dev)),
+                "shard_preselect", n)
+    return idx, xs, ys, cnt
+
+
+def merge_and_lttb(idx, xs, ys, counts, n_out: int, r_ps: int) -> torch.Tensor:
+    """Device merge of the G shard sets in rank order, then the LTTB stage."""
+    dev = idx.device
+    G, cap = idx.shape
+    tot = G * cap
+    oi = torch.empty(tot, dtype=torch.int64, device=dev)
+    ox = torch.empty(tot, dtype=torch.float64, device=dev)
+    oy = torch.empty(tot, dtype=torch.float64, device=dev)
+    om = torch.empty(1, dtype=torch.int64, device=dev)
+    out = torch.empty(n_out, dtype=torch.int64, device=dev)
+    L = N.lib()
+    with torch.cuda.device(dev):
+        st = N.stream_ptr(dev)
+        N.check(L.mmlttb_merge_shards(idx.data_ptr(), xs.data_ptr(), ys.data_ptr(), counts.data_ptr(), G, cap,
+                                      oi.data_ptr(), ox.data_ptr(), oy.data_ptr(), om.data_ptr(), st), "merge_shards")
+        wsb = L.mmlttb_lttb_preselected_workspace_bytes(1, n_out, r_ps)
+        ws = N.workspace(wsb, dev)
+        N.check(L.mmlttb_lttb_preselected(oi.data_ptr(), ox.data_ptr(), oy.data_ptr(), om.data_ptr(), 1, tot, n_out,
+                                          r_ps, out.data_ptr(), ws.data_ptr(), wsb, st), "lttb_preselected")
+    return out
+
+
+def minmaxlttb_series_sharded(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out: int, r_ps: int = 4,
+                              group=None) -> torch.Tensor:
+    """minmaxlttb of ONE series split by bucket ranges across the ranks.
+
+    ``x_shard``/``y_shard`` hold elements ``[shard.lo, shard.hi)`` of the
+    series for this rank (see :func:`bucket_ranges`).  Returns the n_out
+    indices (identical to the single-device result) on every rank.
+    """
+    _check_n_out(n, n_out)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    shard = bucket_ranges(n, n_out, r_ps, world)[rank]
+    if y_shard.shape[0] != shard.hi - shard.lo or x_shard.shape[0] != y_shard.shape[0]:
+        raise ValueError(f"rank {rank} must hold elements [{shard.lo}, {shard.hi}) of the series")
+    idx, xs, ys, cnt = shard_preselect(x_shard, y_shard, n, n_out, r_ps, shard)
+    buf = pack(idx, xs, ys, cnt, shard.cap)
+    allbuf = exchange(buf, world, group) if world > 1 else buf
+    gi, gx, gy, gc = unpack(allbuf, world, shard.cap)
+    return merge_and_lttb(gi, gx, gy, gc, n_out, r_ps)
