@@ -198,7 +198,10 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
 bool mul_ok(int64_t a, int64_t b) { return a == 0 || b <= INT64_MAX / a; }
 
 // ---- K3 planning --------------------------------------------------------
-constexpr int NBB = 32;  // buckets per k_lttb_tables block
+// Buckets of <= 64 points: exact transition tables over all points (K3a).
+// Larger buckets: hull-candidate tables + full verification + repair (K3c).
+constexpr int NBB = 32;   // buckets per k_lttb_tables block
+constexpr int HMAX = 32;  // K3c candidates per bucket
 
 int smax_for(int64_t s) {
   if (s <= 4) return 4;
@@ -209,19 +212,27 @@ int smax_for(int64_t s) {
   return 0;
 }
 
-int64_t jump_smem(int64_t k3, int smax) { return 2 * ((k3 * smax + 15) / 16 * 16); }
 constexpr int64_t JUMP_SMEM_MAX = 200 * 1024;
-
-// Which LTTB kernel pair runs for bucket-size bound `s` and k3 buckets.
-bool use_tables(int64_t s, int64_t k3) {
-  const int sm = smax_for(s);
-  return sm > 0 && jump_smem(k3, sm) <= JUMP_SMEM_MAX;
+// buckets per k_lttb_jump shared-memory segment (two byte tables of seg*SMAX)
+int64_t jump_seg(int64_t k3, int smax) {
+  const int64_t cap = (JUMP_SMEM_MAX / (2 * smax)) / 16 * 16;
+  return std::min<int64_t>(cap, (k3 + 15) / 16 * 16);
 }
+
+bool use_tables(int64_t s) { return smax_for(s) > 0; }
+bool use_chain() {
+  static const bool c = env_i64("MMLTTB_LTTB_CHAIN", 0) != 0;  // A/B knob: old sequential chain
+  return c;
+}
+
+int64_t tab_ld(int64_t k3, int smax) { return (k3 * smax + 15) / 16 * 16; }
 
 int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s) {
   const int64_t k3 = n_out - 2;
-  if (use_tables(s, k3)) return up(B * ((k3 * smax_for(s) + 15) / 16 * 16));
-  return up(B * k3 * (int64_t)sizeof(double2));
+  if (use_tables(s)) return up(B * tab_ld(k3, smax_for(s)));
+  if (use_chain()) return up(B * k3 * (int64_t)sizeof(double2));
+  return up(B * k3 * (int64_t)sizeof(double2)) + up(B * k3 * HMAX * 8) + up(B * k3 * 4) + up(B * tab_ld(k3, HMAX)) +
+         up(B * (k3 + 2) * 8) + up(B * k3 * 8) + up(B * k3 * 4);
 }
 
 template <int SMAX> int jump_attr() {
@@ -234,10 +245,20 @@ template <int SMAX> int jump_attr() {
   return MM_OK;
 }
 
+template <int SMAX>
+int launch_jump(LttbArgs a, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  int rc = jump_attr<SMAX>();
+  if (rc) return rc;
+  a.jump_seg = jump_seg(k3, SMAX);
+  k_lttb_jump<SMAX><<<(unsigned)a.B, 1024, (size_t)(2 * a.jump_seg * SMAX), st>>>(a);
+  return check_launch("k_lttb_jump");
+}
+
 template <typename XT, typename YT, int SMAX>
 int launch_tables_jump(LttbArgs a, cudaStream_t st) {
   const int64_t k3 = a.n_out - 2;
-  a.tab_ld = (k3 * SMAX + 15) / 16 * 16;
+  a.tab_ld = tab_ld(k3, SMAX);
   dim3 g((unsigned)cdiv(k3, NBB), (unsigned)a.B);
   constexpr int NT = NBB * SMAX < 1024 ? NBB * SMAX : 1024;
   k_lttb_tables<XT, YT, SMAX, NBB><<<g, NT, 0, st>>>(a);
@@ -247,17 +268,48 @@ int launch_tables_jump(LttbArgs a, cudaStream_t st) {
     k_lttb_scan<SMAX, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
     return check_launch("k_lttb_scan");
   } else {
-    if ((rc = jump_attr<SMAX>())) return rc;
-    k_lttb_jump<SMAX><<<(unsigned)a.B, 1024, (size_t)jump_smem(k3, SMAX), st>>>(a);
-    return check_launch("k_lttb_jump");
+    return launch_jump<SMAX>(a, st);
   }
+}
+
+// K3c: large buckets (see kernels.cuh): means, hull candidates, candidate
+// tables, jump (positions), verification, repair + output
+template <typename XT, typename YT>
+int launch_lttb_large(LttbArgs a, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  Carve cv{(char*)a.tables, INT64_MAX / 4};
+  a.means = cv.take<double2>(a.B * k3);
+  a.means_ld = k3;
+  a.cand = cv.take<int64_t>(a.B * k3 * HMAX);
+  a.cand_ld = k3 * HMAX;
+  a.cand_cnt = cv.take<int>(a.B * k3);
+  a.tab_ld = tab_ld(k3, HMAX);
+  unsigned char* tabs = cv.take<unsigned char>(a.B * a.tab_ld);
+  a.pos = cv.take<int64_t>(a.B * (k3 + 2));
+  a.pos_ld = k3 + 2;
+  a.best = cv.take<int64_t>(a.B * k3);
+  a.flag = cv.take<int>(a.B * k3);
+  a.tables = tabs;
+  a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", HMAX);  // test knob: a poor heuristic must still be exact
+  k_lttb_means_staged<XT, YT, 128><<<(unsigned)cdiv(a.B * k3, 8), 256, 0, st>>>(a);
+  int rc = check_launch("k_lttb_means_staged");
+  if (rc) return rc;
+  k_lttb_hull<XT, YT, HMAX><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);
+  if ((rc = check_launch("k_lttb_hull"))) return rc;
+  k_lttb_ctables<XT, YT, HMAX><<<dim3((unsigned)cdiv(k3, 1024 / HMAX), (unsigned)a.B), 1024, 0, st>>>(a);
+  if ((rc = check_launch("k_lttb_ctables"))) return rc;
+  if ((rc = launch_jump<HMAX>(a, st))) return rc;
+  k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
+  if ((rc = check_launch("k_lttb_verify"))) return rc;
+  k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
+  return check_launch("k_lttb_repair");
 }
 
 template <typename XT, typename YT>
 int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
   const int64_t k3 = a.n_out - 2;
-  if (a.B > 65535 && use_tables(s, k3)) return fail(MM_ERANGE, "batch > 65535 series");
-  if (use_tables(s, k3)) {
+  if (a.B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
+  if (use_tables(s)) {
     switch (smax_for(s)) {
       case 4: return launch_tables_jump<XT, YT, 4>(a, st);
       case 8: return launch_tables_jump<XT, YT, 8>(a, st);
@@ -266,6 +318,7 @@ int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
       default: return launch_tables_jump<XT, YT, 64>(a, st);
     }
   }
+  if (!use_chain()) return launch_lttb_large<XT, YT>(a, st);
   a.means = reinterpret_cast<double2*>(a.tables);
   a.means_ld = k3;
   const int64_t n = a.B * k3;
@@ -554,7 +607,7 @@ int mmlttb_extrema_by_bucket(const void* y, int y_dtype, const int64_t* bounds, 
 
 int64_t mmlttb_lttb_select_workspace_bytes(int64_t n, int64_t nb) {
   (void)n;
-  return up((nb - 1) * (int64_t)sizeof(double2));
+  return lttb_ws(1, nb + 1, INT64_MAX / 4);
 }
 
 int mmlttb_lttb_select(const void* xs, int x_dtype, const void* ys, int y_dtype, int64_t n, const int64_t* bounds,
@@ -565,7 +618,7 @@ int mmlttb_lttb_select(const void* xs, int x_dtype, const void* ys, int y_dtype,
   LttbArgs la{};
   la.x = xs; la.y = ys; la.n = n; la.bounds = bounds; la.B = 1; la.n_out = nb + 1; la.out = out;
   la.tables = (unsigned char*)workspace;
-  // explicit bounds: always the chain pair (bucket sizes are the caller's)
+  // explicit bounds: bucket sizes are the caller's -> the general (K3c) path
   return launch_lttb(la, x_dtype, y_dtype, INT64_MAX / 4, (cudaStream_t)stream);
 }
 

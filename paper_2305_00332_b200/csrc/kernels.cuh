@@ -562,6 +562,14 @@ struct LttbArgs {
   int64_t* out;                      // [B][n_out]
   unsigned char* tables; int64_t tab_ld;  // K3a: [B][k3*SMAX]
   double2* means; int64_t means_ld;       // K3b: [B][k3]
+  int64_t jump_seg;                       // buckets per shared-memory segment (k_lttb_jump)
+  // K3c (large buckets): hull candidates, verification, repair
+  int64_t* cand; int64_t cand_ld;         // [B][k3][HMAX] candidate positions (ascending)
+  int* cand_cnt;                          // [B][k3]
+  int64_t* pos; int64_t pos_ld;           // [B][k3+2] chosen positions (pre-map)
+  int64_t* best;                          // [B][k3] exact argmax given pos[b] (verify)
+  int* flag;                              // [B][k3] best != pos[b+1]
+  int cand_cap;                           // <= HMAX (tests lower it to force repairs)
 };
 
 __device__ __forceinline__ double lttb_area(double ax, double ay, double cx, double cy, double xj, double yj) {
@@ -640,46 +648,72 @@ __global__ void __launch_bounds__(NBB * SMAX < 1024 ? NBB * SMAX : 1024) k_lttb_
   }
 }
 
-// K3a, part 2: one CTA per series loads its tables into shared memory and
-// composes them by pointer jumping: after level w, G_b maps bucket
-// (b-w)'s points to bucket b; ceil(log2 k3) levels leave G_b[0] = the LTTB
-// pick of bucket b (the chain out[b+1] = T_b[out[b]] of :108-119).
+// K3a/K3c, part 2: one CTA per series composes the transition tables by
+// pointer jumping in shared memory, a segment of `jump_seg` buckets at a
+// time: after level w, G_b maps the candidates of bucket (b-w) to bucket b;
+// ceil(log2 seg) levels leave G_b mapping the segment's entry domain (the
+// previous segment's last pick, carried) to bucket b's pick -- the chain
+// out[b+1] = T_b[out[b]] of _kernels.py:108-119 without the sequential walk.
+// Output: positions into a.pos (K3c, verified later) or mapped indices into
+// a.out.  Candidate mode: local pick -> a.cand[b][pick], else lbound + pick.
 template <int SMAX>
 __global__ void __launch_bounds__(1024) k_lttb_jump(LttbArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int s_carry;
   const int64_t s = blockIdx.x;
   const int64_t k3 = a.n_out - 2;
   const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const int64_t nent = k3 * SMAX;
-  unsigned char* A = sm;
-  unsigned char* Bf = sm + ((nent + 15) & ~(int64_t)15);
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(a.tables + s * a.tab_ld);
-    uint4* dst = reinterpret_cast<uint4*>(A);
-    const int64_t nv = (nent + 15) / 16;
-    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
-  for (int64_t w = 1; w < k3; w <<= 1) {
-    for (int64_t it = threadIdx.x; it < nent; it += blockDim.x) {
-      const int64_t b = it / SMAX;
-      const int p = (int)(it % SMAX);
-      unsigned char v = A[it];
-      if (b >= w) v = A[b * SMAX + A[(b - w) * SMAX + p]];
-      Bf[it] = v;
+  const int64_t seg = a.jump_seg;
+  unsigned char* const A0 = sm;
+  unsigned char* const B0 = sm + seg * SMAX;
+  const unsigned char* tab = a.tables + s * a.tab_ld;
+  int64_t* out = a.out + s * a.n_out;
+  int64_t* pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  const int64_t* cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
+  int carry = 0;
+  for (int64_t s0 = 0; s0 < k3; s0 += seg) {
+    const int64_t len = min(seg, k3 - s0);
+    const int64_t nent = len * SMAX;
+    unsigned char* A = A0;
+    unsigned char* Bf = B0;
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(tab + s0 * SMAX);
+      uint4* dst = reinterpret_cast<uint4*>(A);
+      for (int64_t i = threadIdx.x; i < (nent + 15) / 16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    unsigned char* t = A; A = Bf; Bf = t;
-  }
-  int64_t* out = a.out + s * a.n_out;
-  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
-  for (int64_t b = threadIdx.x; b < k3; b += blockDim.x) {
-    const int64_t pos = lbound(a, m, b) + A[b * SMAX];
-    out[b + 1] = map ? map[pos] : pos;
+    for (int64_t w = 1; w < len; w <<= 1) {
+      for (int64_t it = threadIdx.x; it < nent; it += blockDim.x) {
+        const int64_t b = it / SMAX;
+        const int p = (int)(it % SMAX);
+        unsigned char v = A[it];
+        if (b >= w) v = A[b * SMAX + A[(b - w) * SMAX + p]];
+        Bf[it] = v;
+      }
+      __syncthreads();
+      unsigned char* t = A; A = Bf; Bf = t;
+    }
+    for (int64_t bl = threadIdx.x; bl < len; bl += blockDim.x) {
+      const int64_t b = s0 + bl;
+      const int sel = A[bl * SMAX + carry];
+      const int64_t p = cand ? cand[b * SMAX + sel] : lbound(a, m, b) + sel;
+      if (pos) pos[b + 1] = p;
+      else out[b + 1] = map ? map[p] : p;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = A[(len - 1) * SMAX + carry];
+    __syncthreads();
+    carry = s_carry;
   }
   if (threadIdx.x == 0) {
-    out[0] = map ? map[0] : 0;
-    out[k3 + 1] = map ? map[m - 1] : m - 1;
+    if (pos) {
+      pos[0] = 0;
+      pos[k3 + 1] = m - 1;
+    } else {
+      out[0] = map ? map[0] : 0;
+      out[k3 + 1] = map ? map[m - 1] : m - 1;
+    }
   }
 }
 
@@ -796,6 +830,69 @@ __global__ void k_lttb_means(LttbArgs a) {
       lttb_next_mean(a, (const XT*)a.x + s * a.x_ld, (const YT*)a.y + s * a.y_ld, m, b);
 }
 
+// Large-bucket means: one warp per (series, bucket).  The in-order fp64 sum
+// is one dependent chain per bucket (it cannot be re-associated), so the
+// warp's lanes stream the bucket through a double-buffered shared-memory tile
+// with coalesced loads while lane 0 runs the chain (_kernels.py:98-104).
+template <typename XT, typename YT, int TILE>
+__global__ void __launch_bounds__(256) k_lttb_means_staged(LttbArgs a) {
+  __shared__ double2 s_t[8][2][TILE];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t g = (int64_t)blockIdx.x * 8 + wid;
+  if (g >= a.B * k3) return;
+  const int64_t s = g / k3, b = g % k3;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  double2 c;
+  if (b + 1 < k3) {
+    const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
+    constexpr int PER = TILE / 32;
+    double rx[PER], ry[PER];
+    auto fetch = [&](int64_t t0) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int64_t j = t0 + q * 32 + lane;
+        rx[q] = j < nhi ? to_f64(xs, j) : 0.0;
+        ry[q] = j < nhi ? to_f64(ys, j) : 0.0;
+      }
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) s_t[wid][buf][q * 32 + lane] = make_double2(rx[q], ry[q]);
+    };
+    double sx = 0.0, sy = 0.0;
+    fetch(nlo);
+    stash(0);
+    __syncwarp();
+    int buf = 0;
+    for (int64_t t0 = nlo; t0 < nhi; t0 += TILE) {
+      const bool more = t0 + TILE < nhi;
+      if (more) fetch(t0 + TILE);  // in flight while lane 0 sums this tile
+      if (lane == 0) {
+        const int n = (int)(nhi - t0 < TILE ? nhi - t0 : (int64_t)TILE);
+        for (int i = 0; i < n; ++i) {
+          const double2 v = s_t[wid][buf][i];
+          sx = __dadd_rn(sx, v.x);
+          sy = __dadd_rn(sy, v.y);
+        }
+      }
+      __syncwarp();
+      if (more) stash(buf ^ 1);
+      __syncwarp();
+      buf ^= 1;
+    }
+    const double cnt = (double)(nhi - nlo);
+    c.x = __ddiv_rn(sx, cnt);
+    c.y = __ddiv_rn(sy, cnt);
+  } else {
+    c.x = to_f64(xs, m - 1);
+    c.y = to_f64(ys, m - 1);
+  }
+  if (lane == 0) a.means[s * a.means_ld + b] = c;
+}
+
 // K3b, part 2: one CTA per series carries the bucket-to-bucket dependency.
 template <typename XT, typename YT, int NT>
 __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
@@ -853,6 +950,250 @@ __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
   if (threadIdx.x == 0) {
     out[0] = map ? map[0] : 0;
     out[k3 + 1] = map ? map[m - 1] : m - 1;
+  }
+}
+
+// ---------------------------------------------------------------- K3c ----
+// LTTB over LARGE buckets (e.g. C2: 1998 buckets of 5005 points), bit-exact.
+// area_j = |alpha*(y_j - ay) - (ax - x_j)*beta| is affine in (x_j, y_j), so
+// in exact arithmetic each bucket's pick is a vertex of the bucket's convex
+// hull whatever the previous pick.  The hull vertices are the candidates:
+//   k_lttb_hull     one warp per bucket: per-lane monotone-chain hulls of
+//                   32 contiguous segments, merged by lane 0 (a heuristic --
+//                   rounding, ties and the HMAX cap can make it miss)
+//   k_lttb_ctables  exact reference areas between candidate sets ->
+//                   transition tables; k_lttb_jump resolves the chain
+//   k_lttb_verify   every bucket re-scanned in full with the exact formula
+//                   and tie rule given the previous pick -> flag mismatches
+//   k_lttb_repair   one CTA walks from the first mismatch with exact full-
+//                   bucket scans until the chain re-joins the candidate
+//                   chain (whose later buckets were verified), then writes
+//                   the output.  So the result never depends on the heuristic.
+__device__ __forceinline__ double hcross(double ox, double oy, double ax, double ay, double bx, double by) {
+  return (ax - ox) * (by - oy) - (ay - oy) * (bx - ox);
+}
+
+template <typename XT, typename YT, int HMAX>
+__global__ void __launch_bounds__(64) k_lttb_hull(LttbArgs a) {
+  constexpr int LC = 12;  // per-lane, per-side hull capacity (heuristic cap)
+  struct HP { double x, y; long long j; };
+  __shared__ HP s_h[2][2][32 * LC];  // per warp, per side: lane stacks, then the merged hull in place
+  __shared__ int s_n[2][2][32];
+  const int64_t s = blockIdx.y;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t b = (int64_t)blockIdx.x * 2 + wid;
+  if (b >= k3) return;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t blo = lbound(a, m, b), bhi = lbound(a, m, b + 1);
+  const int64_t seg = (bhi - blo + 31) / 32;
+  const int64_t j0 = blo + lane * seg, j1 = min(bhi, j0 + seg);
+  HP* U = &s_h[wid][0][lane * LC];
+  HP* Lw = &s_h[wid][1][lane * LC];
+  int nu = 0, nl = 0;
+  // per-lane monotone chain over a contiguous segment (x non-decreasing),
+  // points prefetched 8 at a time
+  for (int64_t t = j0; t < j1; t += 8) {
+    double px[8], py[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t j = t + q < j1 ? t + q : j1 - 1;
+      px[q] = to_f64(xs, j);
+      py[q] = to_f64(ys, j);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (t + q >= j1) break;
+      const HP p = {px[q], py[q], (long long)(t + q)};
+      while (nu >= 2 && hcross(U[nu - 2].x, U[nu - 2].y, U[nu - 1].x, U[nu - 1].y, p.x, p.y) >= 0.0) --nu;
+      if (nu == LC) --nu;  // cap: keep the newest point
+      U[nu++] = p;
+      while (nl >= 2 && hcross(Lw[nl - 2].x, Lw[nl - 2].y, Lw[nl - 1].x, Lw[nl - 1].y, p.x, p.y) <= 0.0) --nl;
+      if (nl == LC) --nl;
+      Lw[nl++] = p;
+    }
+  }
+  s_n[wid][0][lane] = nu;
+  s_n[wid][1][lane] = nl;
+  __syncwarp();
+  // lanes 0 and 1: hull of the lane hulls (upper / lower), built in place
+  // (the write cursor never passes the read cursor)
+  if (lane < 2) {
+    const int side = lane;
+    HP* H = s_h[wid][side];
+    int n = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int cnt = s_n[wid][side][l];
+      for (int q = 0; q < cnt; ++q) {
+        const HP p = H[l * LC + q];
+        if (side == 0) {
+          while (n >= 2 && hcross(H[n - 2].x, H[n - 2].y, H[n - 1].x, H[n - 1].y, p.x, p.y) >= 0.0) --n;
+        } else {
+          while (n >= 2 && hcross(H[n - 2].x, H[n - 2].y, H[n - 1].x, H[n - 1].y, p.x, p.y) <= 0.0) --n;
+        }
+        H[n++] = p;
+      }
+    }
+    s_n[wid][side][0] = n;
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  // sorted union of the two hulls, dedup, capped (keep ascending prefix)
+  const HP* Hu = s_h[wid][0];
+  const HP* Hl = s_h[wid][1];
+  const int fu = s_n[wid][0][0], fl = s_n[wid][1][0];
+  int64_t* cand = a.cand + s * a.cand_ld + b * HMAX;
+  const int cap = a.cand_cap > 0 && a.cand_cap < HMAX ? a.cand_cap : HMAX;
+  int iu = 0, il = 0, c = 0;
+  long long last = -1;
+  while ((iu < fu || il < fl) && c < cap) {
+    long long v;
+    if (il >= fl || (iu < fu && Hu[iu].j <= Hl[il].j)) v = Hu[iu++].j;
+    else v = Hl[il++].j;
+    if (v != last) { cand[c++] = v; last = v; }
+  }
+  a.cand_cnt[s * k3 + b] = c;
+}
+
+// T_b[p] over candidates: exact reference area (lttb_area), strict '>' in
+// ascending index order = lowest index on ties, NaN never wins.
+template <typename XT, typename YT, int HMAX>
+__global__ void __launch_bounds__(1024) k_lttb_ctables(LttbArgs a) {
+  constexpr int NBK = 1024 / HMAX;
+  const int64_t s = blockIdx.y;
+  const int64_t k3 = a.n_out - 2;
+  const int bi = threadIdx.x / HMAX, p = threadIdx.x % HMAX;
+  const int64_t b = (int64_t)blockIdx.x * NBK + bi;
+  if (b >= k3) return;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t* cand = a.cand + s * a.cand_ld;
+  const int* cnt = a.cand_cnt + s * k3;
+  bool valid;
+  int64_t ap;
+  if (b == 0) { valid = p == 0; ap = 0; }
+  else { valid = p < cnt[b - 1]; ap = valid ? cand[(b - 1) * HMAX + p] : 0; }
+  unsigned char r = 0;
+  if (valid) {
+    const double ax = to_f64(xs, ap), ay = to_f64(ys, ap);
+    const double2 c = a.means[s * a.means_ld + b];
+    const int nc = cnt[b];
+    double bestv = -1.0;
+    for (int q = 0; q < nc; ++q) {
+      const int64_t j = cand[b * HMAX + q];
+      const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+      if (ar > bestv) { bestv = ar; r = (unsigned char)q; }
+    }
+  }
+  a.tables[s * a.tab_ld + b * HMAX + p] = r;
+}
+
+// block argmax of the exact area over [lo, hi) given anchor (ax, ay) and mean c
+template <typename XT, typename YT, int NT>
+__device__ __forceinline__ int64_t block_bucket_argmax(const XT* xs, const YT* ys, int64_t lo, int64_t hi, double ax,
+                                                       double ay, double2 c, double* s_a, long long* s_i) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double bestv = -1.0;
+  long long bi = LLONG_MAX;
+  for (int64_t j = lo + threadIdx.x; j < hi; j += NT) {
+    const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+    if (ar > bestv) { bestv = ar; bi = j; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double oa = __shfl_xor_sync(FULL, bestv, o);
+    const long long oi = __shfl_xor_sync(FULL, bi, o);
+    if (oa > bestv || (oa == bestv && oi < bi)) { bestv = oa; bi = oi; }
+  }
+  if (lane == 0) { s_a[wid] = bestv; s_i[wid] = bi; }
+  __syncthreads();
+  if (wid == 0) {
+    bestv = lane < NT / 32 ? s_a[lane] : -1.0;
+    bi = lane < NT / 32 ? s_i[lane] : LLONG_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double oa = __shfl_xor_sync(FULL, bestv, o);
+      const long long oi = __shfl_xor_sync(FULL, bi, o);
+      if (oa > bestv || (oa == bestv && oi < bi)) { bestv = oa; bi = oi; }
+    }
+    if (lane == 0) s_i[0] = bi == LLONG_MAX ? lo : bi;  // all-NaN bucket keeps bounds[b] (:110)
+  }
+  __syncthreads();
+  const int64_t r = s_i[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_verify(LttbArgs a) {
+  __shared__ double s_a[NT / 32];
+  __shared__ long long s_i[NT / 32];
+  const int64_t s = blockIdx.y;
+  const int64_t b = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t* pos = a.pos + s * a.pos_ld;
+  const int64_t prev = pos[b];
+  const double2 c = a.means[s * a.means_ld + b];
+  const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
+                                                    to_f64(ys, prev), c, s_a, s_i);
+  if (threadIdx.x == 0) {
+    a.best[s * k3 + b] = r;
+    a.flag[s * k3 + b] = r != pos[b + 1];
+  }
+}
+
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
+  __shared__ double s_a[NT / 32];
+  __shared__ long long s_i[NT / 32];
+  __shared__ long long s_next;
+  const int64_t s = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  int64_t* pos = a.pos + s * a.pos_ld;
+  const int* flag = a.flag + s * k3;
+  const int64_t* best = a.best + s * k3;
+  int64_t b = 0;
+  bool synced = true;
+  while (b < k3) {
+    if (synced) {  // next verified mismatch at or after b
+      if (threadIdx.x == 0) s_next = LLONG_MAX;
+      __syncthreads();
+      for (int64_t i = b + threadIdx.x; i < k3; i += NT)
+        if (flag[i]) atomicMin(&s_next, (long long)i);
+      __syncthreads();
+      const long long nb = s_next;
+      __syncthreads();
+      if (nb == LLONG_MAX) break;
+      b = nb;
+      if (threadIdx.x == 0) pos[b + 1] = best[b];  // exact: prev pos[b] is on the true chain
+      synced = false;
+      ++b;
+      __syncthreads();
+      continue;
+    }
+    const int64_t prev = pos[b];
+    const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
+                                                      to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+    const int64_t was = pos[b + 1];
+    __syncthreads();
+    if (threadIdx.x == 0) pos[b + 1] = r;
+    synced = r == was;  // re-joined the candidate chain: later buckets were verified with this prev
+    ++b;
+    __syncthreads();
+  }
+  int64_t* out = a.out + s * a.n_out;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  for (int64_t i = threadIdx.x; i < k3 + 2; i += NT) {
+    const int64_t p = pos[i];
+    out[i] = map ? map[p] : p;
   }
 }
 

@@ -288,3 +288,40 @@ def test_lttb_scan_multi_chunk(n_out, r):
     y = np.cumsum(rng.standard_normal(n)).astype(np.float32)
     got = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out, minmax_ratio=r)
     assert np.array_equal(got.cpu().numpy(), O.minmaxlttb(x, y, n_out, r))
+
+
+def test_lttb_large_bucket_repair_path():
+    """K3c with the candidate sets cut to 1-2 points: verification must flag
+    the wrong picks and the repair walk must still reproduce the reference."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, '.');"
+        "import paper_2305_00332_b200 as mm; from oracle import oracle as O;"
+        "rng = np.random.Generator(np.random.PCG64(8)); n = 300_000;"
+        "x = np.cumsum(rng.exponential(1.0, n)); y = np.cumsum(rng.standard_normal(n));"
+        "g = mm.lttb(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), 700).cpu().numpy();"
+        "assert np.array_equal(g, O.lttb(x, y, 700)), 'mismatch';"
+        "x2 = np.arange(n, dtype=np.int64); y2 = np.repeat(rng.standard_normal(n // 100), 100);"
+        "g = mm.lttb(torch.from_numpy(x2).cuda(), torch.from_numpy(y2).cuda(), 300).cpu().numpy();"
+        "assert np.array_equal(g, O.lttb(x2, y2, 300)), 'mismatch2'; print('ok')"
+    )
+    for cap in ("1", "2"):
+        env = dict(__import__("os").environ, MMLTTB_K3C_CAND_CAP=cap)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           cwd=str(GOLD.parent.parent), timeout=300)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_lttb_large_bucket_degenerate():
+    """Ties everywhere (constant / collinear / duplicated points) through K3c."""
+    n = 100_000
+    x = np.arange(n, dtype=np.int64)
+    for y in (np.zeros(n), 3.0 * x + 1.0, np.repeat(np.arange(n // 1000, dtype=np.float64), 1000)):
+        got = mm.lttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), 90).cpu().numpy()
+        assert np.array_equal(got, O.lttb(x, y, 90))
+    xr = np.repeat(np.arange(n // 4, dtype=np.float64), 4)  # repeated x
+    yr = np.random.Generator(np.random.PCG64(1)).standard_normal(n)
+    got = mm.lttb(torch.from_numpy(xr).to(DEV), torch.from_numpy(yr).to(DEV), 120).cpu().numpy()
+    assert np.array_equal(got, O.lttb(xr, yr, 120))
