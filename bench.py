@@ -318,6 +318,7 @@ def run_ours(args):
     time.sleep(0.15)
     # ---- device-resident timed region (value) ----
     L.mmlttb_stage_timer(1)
+    rep0 = L.mmlttb_repair_scans()
     l0 = L.mmlttb_launch_count()
     if ws > 1:
         dist.barrier()
@@ -332,6 +333,7 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     launches = L.mmlttb_launch_count() - l0
+    repairs = (L.mmlttb_repair_scans() - rep0) / args.steps
     ms = e0.elapsed_time(e1)
     import ctypes
 
@@ -404,6 +406,7 @@ def run_ours(args):
                     "ms_per_step": e2e_ms, "steps": e2e_steps,
                     "path": "minmaxlttb(pinned host x, pinned host y) -> numpy-free CPU tensor result"},
             "gpu_launches": int(launches),
+            "lttb_repair_scans_per_step": repairs,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -62,6 +62,9 @@ const char *mmlttb_last_error(void);
  * them, writes the summed device milliseconds of the three stages to ms3[3]
  * and the number of timed calls, then clears. */
 int64_t mmlttb_launch_count(void);
+/* Exact bucket re-scans the large-bucket LTTB repair walk has performed since
+ * load (synchronises the device; statistics for tests/bench only). */
+int64_t mmlttb_repair_scans(void);
 int mmlttb_stage_timer(int enable);
 int mmlttb_stage_timer_read(double *ms3, int64_t *calls);
 

@@ -35,6 +35,7 @@ _SIGS = {
     "mmlttb_version": (_i32, []),
     "mmlttb_last_error": (ctypes.c_char_p, []),
     "mmlttb_launch_count": (_i64, []),
+    "mmlttb_repair_scans": (_i64, []),
     "mmlttb_stage_timer": (_i32, [_i32]),
     "mmlttb_stage_timer_read": (_i32, [_p, _p]),
     "mmlttb_workspace_bytes": (_i64, [_i32, _i64, _i64, _i64, _i64, _i32]),

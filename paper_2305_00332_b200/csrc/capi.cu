@@ -201,7 +201,7 @@ bool mul_ok(int64_t a, int64_t b) { return a == 0 || b <= INT64_MAX / a; }
 // Buckets of <= 64 points: exact transition tables over all points (K3a).
 // Larger buckets: hull-candidate tables + full verification + repair (K3c).
 constexpr int NBB = 32;   // buckets per k_lttb_tables block
-constexpr int HMAX = 32;  // K3c candidates per bucket
+constexpr int HMAX = 32;  // K3c workspace bound: <= 2 x 16 sampled directions per bucket
 
 int smax_for(int64_t s) {
   if (s <= 4) return 4;
@@ -220,6 +220,10 @@ int64_t jump_seg(int64_t k3, int smax) {
 }
 
 bool use_tables(int64_t s) { return smax_for(s) > 0; }
+bool use_hull() {
+  static const bool h = env_i64("MMLTTB_K3C_HULL", 0) != 0;  // A/B knob: hull candidates
+  return h;
+}
 bool use_chain() {
   static const bool c = env_i64("MMLTTB_LTTB_CHAIN", 0) != 0;  // A/B knob: old sequential chain
   return c;
@@ -232,7 +236,7 @@ int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s) {
   if (use_tables(s)) return up(B * tab_ld(k3, smax_for(s)));
   if (use_chain()) return up(B * k3 * (int64_t)sizeof(double2));
   return up(B * k3 * (int64_t)sizeof(double2)) + up(B * k3 * HMAX * 8) + up(B * k3 * 4) + up(B * tab_ld(k3, HMAX)) +
-         up(B * (k3 + 2) * 8) + up(B * k3 * 8) + up(B * k3 * 4);
+         up(B * (k3 + 2) * 8) + up(B * k3 * 8) + up(B * k3 * 4) + up(B * k3 * (int64_t)sizeof(double2));
 }
 
 template <int SMAX> int jump_attr() {
@@ -264,7 +268,7 @@ int launch_tables_jump(LttbArgs a, cudaStream_t st) {
   k_lttb_tables<XT, YT, SMAX, NBB><<<g, NT, 0, st>>>(a);
   int rc = check_launch("k_lttb_tables");
   if (rc) return rc;
-  if constexpr (SMAX <= 8) {
+  if constexpr (SMAX <= 32) {
     k_lttb_scan<SMAX, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
     return check_launch("k_lttb_scan");
   } else {
@@ -274,31 +278,39 @@ int launch_tables_jump(LttbArgs a, cudaStream_t st) {
 
 // K3c: large buckets (see kernels.cuh): means, hull candidates, candidate
 // tables, jump (positions), verification, repair + output
-template <typename XT, typename YT>
+template <typename XT, typename YT, int H>
 int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   const int64_t k3 = a.n_out - 2;
   Carve cv{(char*)a.tables, INT64_MAX / 4};
   a.means = cv.take<double2>(a.B * k3);
   a.means_ld = k3;
   a.cand = cv.take<int64_t>(a.B * k3 * HMAX);
-  a.cand_ld = k3 * HMAX;
+  a.cand_ld = k3 * H;
   a.cand_cnt = cv.take<int>(a.B * k3);
-  a.tab_ld = tab_ld(k3, HMAX);
-  unsigned char* tabs = cv.take<unsigned char>(a.B * a.tab_ld);
+  a.tab_ld = tab_ld(k3, H);
+  unsigned char* tabs = cv.take<unsigned char>(a.B * tab_ld(k3, HMAX));
   a.pos = cv.take<int64_t>(a.B * (k3 + 2));
   a.pos_ld = k3 + 2;
   a.best = cv.take<int64_t>(a.B * k3);
   a.flag = cv.take<int>(a.B * k3);
+  a.yrange = cv.take<double2>(a.B * k3);
   a.tables = tabs;
-  a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", HMAX);  // test knob: a poor heuristic must still be exact
-  k_lttb_means_staged<XT, YT, 128><<<(unsigned)cdiv(a.B * k3, 8), 256, 0, st>>>(a);
+  a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", H);  // test knob: a poor heuristic must still be exact
+  // one warp per bucket, 8 KB of tiles each: every bucket's chain resident at once
+  k_lttb_means_staged<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
   int rc = check_launch("k_lttb_means_staged");
   if (rc) return rc;
-  k_lttb_hull<XT, YT, HMAX><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);
-  if ((rc = check_launch("k_lttb_hull"))) return rc;
-  k_lttb_ctables<XT, YT, HMAX><<<dim3((unsigned)cdiv(k3, 1024 / HMAX), (unsigned)a.B), 1024, 0, st>>>(a);
+  if (use_hull()) {
+    k_lttb_hull<XT, YT, H><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);
+    if ((rc = check_launch("k_lttb_hull"))) return rc;
+  } else {
+    k_lttb_dircand<XT, YT, H, H / 2><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
+    if ((rc = check_launch("k_lttb_dircand"))) return rc;
+  }
+  k_lttb_ctables<XT, YT, H><<<dim3((unsigned)cdiv(k3, 1024 / H), (unsigned)a.B), 1024, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_ctables"))) return rc;
-  if ((rc = launch_jump<HMAX>(a, st))) return rc;
+  k_lttb_scan<H, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
+  if ((rc = check_launch("k_lttb_scan"))) return rc;
   k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_verify"))) return rc;
   k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
@@ -318,7 +330,10 @@ int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
       default: return launch_tables_jump<XT, YT, 64>(a, st);
     }
   }
-  if (!use_chain()) return launch_lttb_large<XT, YT>(a, st);
+  if (!use_chain()) {
+    static const int64_t h = env_i64("MMLTTB_K3C_HMAX", 16);  // A/B knob: 16 or 32 candidates
+    return h == 32 ? launch_lttb_large<XT, YT, 32>(a, st) : launch_lttb_large<XT, YT, 16>(a, st);
+  }
   a.means = reinterpret_cast<double2*>(a.tables);
   a.means_ld = k3;
   const int64_t n = a.B * k3;
@@ -397,6 +412,12 @@ extern "C" {
 int mmlttb_version(void) { return 1; }
 
 int64_t mmlttb_launch_count(void) { return g_launches.load(); }
+
+int64_t mmlttb_repair_scans(void) {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_repair_scans, sizeof v) != cudaSuccess) return -1;
+  return (int64_t)v;
+}
 
 int mmlttb_stage_timer(int enable) {
   g_timer.on = enable != 0;

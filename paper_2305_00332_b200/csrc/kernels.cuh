@@ -570,6 +570,7 @@ struct LttbArgs {
   int64_t* best;                          // [B][k3] exact argmax given pos[b] (verify)
   int* flag;                              // [B][k3] best != pos[b+1]
   int cand_cap;                           // <= HMAX (tests lower it to force repairs)
+  double2* yrange;                        // [B][k3] per-bucket (ymin, ymax) (K3c candidates)
 };
 
 __device__ __forceinline__ double lttb_area(double ax, double ay, double cx, double cy, double xj, double yj) {
@@ -751,6 +752,78 @@ template <> struct PMap<8> {
   }
 };
 
+// W = 16 / 32: maps of W bytes; output byte p = g[f[p]] selects among W
+// bytes with one PRMT per 8-byte block and a per-byte mux on f's high bits.
+template <int W> struct PMapN {
+  static constexpr int NW = W / 4;
+  uint32_t v[NW];
+  static __device__ __forceinline__ PMapN ident() {
+    PMapN r;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) r.v[i] = 0x03020100u + 0x04040404u * (uint32_t)i;
+    return r;
+  }
+  static __device__ __forceinline__ PMapN comp(const PMapN& g, const PMapN& f) {
+    PMapN r;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const uint32_t fw = f.v[i];
+      const uint32_t sel = PMap<4>::sel(fw & 0x07070707u);
+      uint32_t q[W / 8];
+#pragma unroll
+      for (int k = 0; k < W / 8; ++k) q[k] = __byte_perm(g.v[2 * k], g.v[2 * k + 1], sel);
+      uint32_t acc[W / 8];
+#pragma unroll
+      for (int k = 0; k < W / 8; ++k) acc[k] = q[k];
+      int n = W / 8, bit = 3;
+#pragma unroll
+      while (n > 1) {
+        const uint32_t msk = ((fw >> bit) & 0x01010101u) * 0xFFu;
+#pragma unroll
+        for (int k = 0; k < n / 2; ++k) acc[k] = (acc[2 * k] & ~msk) | (acc[2 * k + 1] & msk);
+        n >>= 1;
+        ++bit;
+      }
+      r.v[i] = acc[0];
+    }
+    return r;
+  }
+  __device__ __forceinline__ int at0() const { return (int)(v[0] & 0xFFu); }
+  __device__ __forceinline__ int at(int p) const { return (int)((v[p >> 2] >> (8 * (p & 3))) & 0xFFu); }
+  __device__ __forceinline__ PMapN shfl_up(int o) const {
+    PMapN r;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) r.v[i] = __shfl_up_sync(FULL, v[i], o);
+    return r;
+  }
+  static __device__ __forceinline__ PMapN load(const unsigned char* t) {
+    PMapN r;
+    const uint4* q = reinterpret_cast<const uint4*>(t);
+#pragma unroll
+    for (int i = 0; i < NW / 4; ++i) {
+      const uint4 u = q[i];
+      r.v[4 * i] = u.x; r.v[4 * i + 1] = u.y; r.v[4 * i + 2] = u.z; r.v[4 * i + 3] = u.w;
+    }
+    return r;
+  }
+};
+template <> struct PMap<16> : PMapN<16> {
+  PMap() = default;
+  __device__ __forceinline__ PMap(const PMapN<16>& o) : PMapN<16>(o) {}
+  static __device__ __forceinline__ PMap ident() { return PMapN<16>::ident(); }
+  static __device__ __forceinline__ PMap comp(const PMap& g, const PMap& f) { return PMapN<16>::comp(g, f); }
+  __device__ __forceinline__ PMap shfl_up(int o) const { return PMapN<16>::shfl_up(o); }
+  static __device__ __forceinline__ PMap load(const unsigned char* t) { return PMapN<16>::load(t); }
+};
+template <> struct PMap<32> : PMapN<32> {
+  PMap() = default;
+  __device__ __forceinline__ PMap(const PMapN<32>& o) : PMapN<32>(o) {}
+  static __device__ __forceinline__ PMap ident() { return PMapN<32>::ident(); }
+  static __device__ __forceinline__ PMap comp(const PMap& g, const PMap& f) { return PMapN<32>::comp(g, f); }
+  __device__ __forceinline__ PMap shfl_up(int o) const { return PMapN<32>::shfl_up(o); }
+  static __device__ __forceinline__ PMap load(const unsigned char* t) { return PMapN<32>::load(t); }
+};
+
 template <int W, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
   typedef PMap<W> M;
@@ -761,7 +834,9 @@ __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
   const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
   const unsigned char* tab = a.tables + s * a.tab_ld;
   int64_t* out = a.out + s * a.n_out;
+  int64_t* pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
   const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  const int64_t* cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   M carry = M::ident();
   for (int64_t c0 = 0; c0 < k3; c0 += (int64_t)NT * ITEMS) {
@@ -803,8 +878,10 @@ __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
       const int64_t b = b0 + i;
       cur = M::comp(t[i], cur);
       if (b < k3) {
-        const int64_t pos = lbound(a, m, b) + cur.at0();
-        out[b + 1] = map ? map[pos] : pos;
+        const int sel = cur.at0();
+        const int64_t p = cand ? cand[b * W + sel] : lbound(a, m, b) + sel;
+        if (pos) pos[b + 1] = p;
+        else out[b + 1] = map ? map[p] : p;
       }
     }
     if (threadIdx.x == NT - 1) s_carry = cur;
@@ -813,8 +890,13 @@ __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    out[0] = map ? map[0] : 0;
-    out[k3 + 1] = map ? map[m - 1] : m - 1;
+    if (pos) {
+      pos[0] = 0;
+      pos[k3 + 1] = m - 1;
+    } else {
+      out[0] = map ? map[0] : 0;
+      out[k3 + 1] = map ? map[m - 1] : m - 1;
+    }
   }
 }
 
@@ -835,62 +917,85 @@ __global__ void k_lttb_means(LttbArgs a) {
 // warp's lanes stream the bucket through a double-buffered shared-memory tile
 // with coalesced loads while lane 0 runs the chain (_kernels.py:98-104).
 template <typename XT, typename YT, int TILE>
-__global__ void __launch_bounds__(256) k_lttb_means_staged(LttbArgs a) {
-  __shared__ double2 s_t[8][2][TILE];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(32) k_lttb_means_staged(LttbArgs a) {
+  __shared__ double s_t[1][2][2][TILE];  // [warp][buffer][x|y][i]
+  const int wid = 0, lane = threadIdx.x & 31;
   const int64_t k3 = a.n_out - 2;
-  const int64_t g = (int64_t)blockIdx.x * 8 + wid;
-  if (g >= a.B * k3) return;
-  const int64_t s = g / k3, b = g % k3;
+  const int64_t g = (int64_t)blockIdx.x;
+  if (g >= a.B * (k3 + 1)) return;
+  // b = -1 .. k3-1: warp b scans bucket b+1 (b = -1 only for bucket 0's y range)
+  const int64_t s = g / (k3 + 1), b = g % (k3 + 1) - 1;
   const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
   const XT* xs = (const XT*)a.x + s * a.x_ld;
   const YT* ys = (const YT*)a.y + s * a.y_ld;
-  double2 c;
   if (b + 1 < k3) {
     const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
     constexpr int PER = TILE / 32;
-    double rx[PER], ry[PER];
+    XT rx[PER];
+    YT ry[PER];
+    double ymn = INFINITY, ymx = -INFINITY;
+    // raw loads only: nothing consumes them until stash(), after the sums,
+    // so the next tile's latency hides behind lanes 0/1's add chains
     auto fetch = [&](int64_t t0) {
 #pragma unroll
       for (int q = 0; q < PER; ++q) {
         const int64_t j = t0 + q * 32 + lane;
-        rx[q] = j < nhi ? to_f64(xs, j) : 0.0;
-        ry[q] = j < nhi ? to_f64(ys, j) : 0.0;
+        rx[q] = j < nhi ? xs[j] : (XT)0;
+        ry[q] = j < nhi ? ys[j] : (YT)0;
       }
     };
-    auto stash = [&](int buf) {
+    auto stash = [&](int buf, int64_t t0) {
 #pragma unroll
-      for (int q = 0; q < PER; ++q) s_t[wid][buf][q * 32 + lane] = make_double2(rx[q], ry[q]);
+      for (int q = 0; q < PER; ++q) {
+        const double vy = (double)ry[q];
+        s_t[wid][buf][0][q * 32 + lane] = (double)rx[q];
+        s_t[wid][buf][1][q * 32 + lane] = vy;
+        if (t0 + q * 32 + lane < nhi) { ymn = fmin(ymn, vy); ymx = fmax(ymx, vy); }
+      }
     };
-    double sx = 0.0, sy = 0.0;
+    // lane 0 carries the x chain, lane 1 the y chain: one DADD instruction
+    // advances both in-order sums (sx = 0.0; sx += x_j, _kernels.py:98-102)
+    double acc = 0.0;
+    const int which = lane & 1;
     fetch(nlo);
-    stash(0);
+    stash(0, nlo);
     __syncwarp();
     int buf = 0;
     for (int64_t t0 = nlo; t0 < nhi; t0 += TILE) {
       const bool more = t0 + TILE < nhi;
-      if (more) fetch(t0 + TILE);  // in flight while lane 0 sums this tile
-      if (lane == 0) {
+      if (more) fetch(t0 + TILE);  // in flight while lanes 0/1 sum this tile
+      if (lane < 2) {
         const int n = (int)(nhi - t0 < TILE ? nhi - t0 : (int64_t)TILE);
-        for (int i = 0; i < n; ++i) {
-          const double2 v = s_t[wid][buf][i];
-          sx = __dadd_rn(sx, v.x);
-          sy = __dadd_rn(sy, v.y);
+        const double* src = s_t[wid][buf][which];
+        int i = 0;
+        for (; i + 8 <= n; i += 8) {  // loads issued ahead of the dependent adds
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = src[i + q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
         }
+        for (; i < n; ++i) acc = __dadd_rn(acc, src[i]);
       }
       __syncwarp();
-      if (more) stash(buf ^ 1);
+      if (more) stash(buf ^ 1, t0 + TILE);
       __syncwarp();
       buf ^= 1;
     }
     const double cnt = (double)(nhi - nlo);
-    c.x = __ddiv_rn(sx, cnt);
-    c.y = __ddiv_rn(sy, cnt);
-  } else {
-    c.x = to_f64(xs, m - 1);
-    c.y = to_f64(ys, m - 1);
+    const double sy = __shfl_sync(FULL, acc, 1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      ymn = fmin(ymn, __shfl_xor_sync(FULL, ymn, o));
+      ymx = fmax(ymx, __shfl_xor_sync(FULL, ymx, o));
+    }
+    if (lane == 0) {
+      if (b >= 0) a.means[s * a.means_ld + b] = make_double2(__ddiv_rn(acc, cnt), __ddiv_rn(sy, cnt));
+      if (a.yrange) a.yrange[s * k3 + b + 1] = make_double2(ymn, ymx);
+    }
+  } else if (lane == 0) {
+    a.means[s * a.means_ld + b] = make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
   }
-  if (lane == 0) a.means[s * a.means_ld + b] = c;
 }
 
 // K3b, part 2: one CTA per series carries the bucket-to-bucket dependency.
@@ -1057,6 +1162,141 @@ __global__ void __launch_bounds__(64) k_lttb_hull(LttbArgs a) {
   a.cand_cnt[s * k3 + b] = c;
 }
 
+// Direction-sampled candidates (default K3c heuristic; cheaper than hulls).
+// Over anchors a in bucket b-1's bounding box and the fixed mean c_b+1, the
+// area functional is f(j) = dx*x_j + dy*y_j + const with (dx, dy) = (cy-ay,
+// ax-cx) ranging over a rectangle, whose angular span is set by its corners.
+// D directions sampled across that span, argmax and argmin of each (the
+// maximiser of |f| is one of them) -> <= 2D candidates per bucket.  Exact
+// only in the limit; k_lttb_verify / k_lttb_repair make the result exact.
+template <typename XT, typename YT, int HMAX, int D>
+__global__ void __launch_bounds__(128) k_lttb_dircand(LttbArgs a) {
+  static_assert(2 * D <= HMAX && 2 * D <= 32, "candidates must fit");
+  __shared__ float s_v[4][2 * D];
+  __shared__ int s_i[4][2 * D];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t s = blockIdx.y, b = blockIdx.x;  // one 4-warp CTA per bucket
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t blo = lbound(a, m, b), bhi = lbound(a, m, b + 1);
+  const double2 c = a.means[s * a.means_ld + b];
+  // anchor box of bucket b-1 (or the fixed first point)
+  double ax0, ax1, ay0, ay1;
+  if (b == 0) {
+    ax0 = ax1 = to_f64(xs, 0);
+    ay0 = ay1 = to_f64(ys, 0);
+  } else {
+    ax0 = to_f64(xs, lbound(a, m, b - 1));
+    ax1 = to_f64(xs, blo - 1);
+    const double2 r = a.yrange[s * k3 + b - 1];
+    ay0 = r.x;
+    ay1 = r.y;
+  }
+  float th_lo = 1e30f, th_hi = -1e30f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double dxv = c.y - ((q & 1) ? ay1 : ay0);
+    const double dyv = ((q & 2) ? ax1 : ax0) - c.x;
+    float th = atan2f((float)dyv, (float)dxv);
+    if (th > 3.0f) th -= 6.2831853f;  // keep the (x <= c.x) half-plane contiguous
+    th_lo = fminf(th_lo, th);
+    th_hi = fmaxf(th_hi, th);
+  }
+  float cs[D], sn[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float th = D > 1 ? th_lo + (th_hi - th_lo) * (float)k / (float)(D - 1) : th_lo;
+    sincosf(th, &sn[k], &cs[k]);
+  }
+  const XT xr = xs[blo];
+  const double yr = c.y;
+  float vmax[D], vmin[D];
+  int imax[D], imin[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) { vmax[k] = -INFINITY; vmin[k] = INFINITY; imax[k] = INT_MAX; imin[k] = INT_MAX; }
+  constexpr int UN = 4;
+  for (int64_t j0 = blo + threadIdx.x; j0 < bhi; j0 += 128 * UN) {
+    XT rx[UN];
+    YT ry[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {  // UN points' loads in flight before any use
+      const int64_t j = j0 + 128 * u < bhi ? j0 + 128 * u : blo;
+      rx[u] = xs[j];
+      ry[u] = ys[j];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      if (j0 + 128 * u < bhi) {
+        const float X = (float)(rx[u] - xr), Y = (float)((double)ry[u] - yr);
+        const int o = (int)(j0 + 128 * u - blo);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const float v = fmaf(cs[k], X, sn[k] * Y);
+          if (v > vmax[k]) { vmax[k] = v; imax[k] = o; }
+          if (v < vmin[k]) { vmin[k] = v; imin[k] = o; }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const float ov = __shfl_xor_sync(FULL, vmax[k], off);
+      const int oi = __shfl_xor_sync(FULL, imax[k], off);
+      if (ov > vmax[k] || (ov == vmax[k] && oi < imax[k])) { vmax[k] = ov; imax[k] = oi; }
+      const float ow = __shfl_xor_sync(FULL, vmin[k], off);
+      const int oj = __shfl_xor_sync(FULL, imin[k], off);
+      if (ow < vmin[k] || (ow == vmin[k] && oj < imin[k])) { vmin[k] = ow; imin[k] = oj; }
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      s_v[wid][2 * k] = vmax[k]; s_i[wid][2 * k] = imax[k];
+      s_v[wid][2 * k + 1] = -vmin[k]; s_i[wid][2 * k + 1] = imin[k];  // both as "max"
+    }
+  }
+  __syncthreads();
+  if (wid != 0) return;
+  int ci = INT_MAX;
+  if (lane < 2 * D) {
+    float bv = s_v[0][lane];
+    ci = s_i[0][lane];
+#pragma unroll
+    for (int w = 1; w < 4; ++w) {
+      const float v = s_v[w][lane];
+      const int i = s_i[w][lane];
+      if (v > bv || (v == bv && i < ci)) { bv = v; ci = i; }
+    }
+  }
+  // sort the <= 32 candidate offsets across the warp (bitonic), then dedup
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int o = __shfl_xor_sync(FULL, ci, j);
+      const bool up = ((lane & k) == 0);
+      const bool lower = (lane & j) == 0;
+      ci = (lower == up) ? min(ci, o) : max(ci, o);
+    }
+  }
+  const int prev = __shfl_up_sync(FULL, ci, 1);
+  const bool keep = ci != INT_MAX && (lane == 0 || prev != ci);
+  const unsigned km = __ballot_sync(FULL, keep);
+  const int rank = __popc(km & ((1u << lane) - 1));
+  const int cap = a.cand_cap > 0 && a.cand_cap < HMAX ? a.cand_cap : HMAX;
+  int64_t* cand = a.cand + s * a.cand_ld + b * HMAX;
+  if (keep && rank < cap) cand[rank] = blo + ci;
+  if (lane == 0) {
+    const int w = min(__popc(km), cap);
+    if (w == 0) cand[0] = blo;
+    a.cand_cnt[s * k3 + b] = w ? w : 1;
+  }
+}
+
 // T_b[p] over candidates: exact reference area (lttb_area), strict '>' in
 // ascending index order = lowest index on ties, NaN never wins.
 template <typename XT, typename YT, int HMAX>
@@ -1097,9 +1337,24 @@ __device__ __forceinline__ int64_t block_bucket_argmax(const XT* xs, const YT* y
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double bestv = -1.0;
   long long bi = LLONG_MAX;
-  for (int64_t j = lo + threadIdx.x; j < hi; j += NT) {
-    const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
-    if (ar > bestv) { bestv = ar; bi = j; }
+  constexpr int UN = 4;
+  for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += (int64_t)NT * UN) {
+    XT rx[UN];
+    YT ry[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {  // loads in flight before the area math
+      const int64_t j = j0 + (int64_t)NT * u < hi ? j0 + (int64_t)NT * u : lo;
+      rx[u] = xs[j];
+      ry[u] = ys[j];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int64_t j = j0 + (int64_t)NT * u;
+      if (j < hi) {
+        const double ar = lttb_area(ax, ay, c.x, c.y, (double)rx[u], (double)ry[u]);
+        if (ar > bestv) { bestv = ar; bi = j; }
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -1147,6 +1402,8 @@ __global__ void __launch_bounds__(NT) k_lttb_verify(LttbArgs a) {
   }
 }
 
+__device__ unsigned long long g_repair_scans;  // exact bucket scans done by k_lttb_repair (stats)
+
 template <typename XT, typename YT, int NT>
 __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
   __shared__ double s_a[NT / 32];
@@ -1173,7 +1430,10 @@ __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
       __syncthreads();
       if (nb == LLONG_MAX) break;
       b = nb;
-      if (threadIdx.x == 0) pos[b + 1] = best[b];  // exact: prev pos[b] is on the true chain
+      if (threadIdx.x == 0) {
+        pos[b + 1] = best[b];  // exact: prev pos[b] is on the true chain
+        atomicAdd(&g_repair_scans, 1ull);
+      }
       synced = false;
       ++b;
       __syncthreads();
@@ -1184,7 +1444,10 @@ __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
                                                       to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
     const int64_t was = pos[b + 1];
     __syncthreads();
-    if (threadIdx.x == 0) pos[b + 1] = r;
+    if (threadIdx.x == 0) {
+      pos[b + 1] = r;
+      atomicAdd(&g_repair_scans, 1ull);
+    }
     synced = r == was;  // re-joined the candidate chain: later buckets were verified with this prev
     ++b;
     __syncthreads();
