@@ -19,6 +19,7 @@
 
 #include "../../include/mmlttb.h"
 #include "kernels.cuh"
+#include "fused.cuh"
 
 using namespace mm;
 
@@ -397,6 +398,63 @@ int launch_pairs(PairArgs pa, int64_t B, cudaStream_t st) {
   return check_launch("k_compact_pairs");
 }
 
+// ---- fused per-series path (batches of medium series) --------------------
+constexpr int64_t FUSED_SMEM_MAX = 110 * 1024;
+constexpr int64_t FUSED_MIN_B = 148;
+
+bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt) {
+  static const bool off = env_i64("MMLTTB_NO_FUSED", 0) != 0;  // A/B knob
+  const int64_t k = (n_out - 2) * (r_ps / 2);
+  return !off && B >= FUSED_MIN_B && r_ps >= 2 && r_ps <= 8 && N < (1LL << 31) &&
+         fused_smem(k, n_out - 2, 8, esize(ydt)) <= FUSED_SMEM_MAX;
+}
+
+template <typename XT, typename YT, int SMAX, int NT, int MINB, int U>
+int launch_fused_v(const FusedArgs& fa, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)FUSED_SMEM_MAX) != cudaSuccess)
+      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_mmlttb_fused)");
+    attr = true;
+  }
+  const int64_t k = (fa.n_out - 2) * (fa.r_ps / 2);
+  const size_t smem = (size_t)fused_smem(k, fa.n_out - 2, SMAX, (int)sizeof(YT));
+  k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U><<<(unsigned)fa.B, NT, smem, st>>>(fa);
+  return check_launch("k_mmlttb_fused");
+}
+
+template <typename XT, typename YT, int SMAX>
+int launch_fused_t(const FusedArgs& fa, cudaStream_t st) {
+  static const int64_t v = env_i64("MMLTTB_FUSED_VARIANT", 0);  // tuning knob (tools/)
+  switch (v) {  // tools/fused_sweep.sh on B200: (512 thr, 2 CTA/SM, U=8) is best on C4
+    case 1: return launch_fused_v<XT, YT, SMAX, 512, 2, 4>(fa, st);
+    case 2: return launch_fused_v<XT, YT, SMAX, 384, 3, 4>(fa, st);
+    case 3: return launch_fused_v<XT, YT, SMAX, 256, 4, 4>(fa, st);
+    case 4: return launch_fused_v<XT, YT, SMAX, 512, 3, 2>(fa, st);
+    default: return launch_fused_v<XT, YT, SMAX, 512, 2, 8>(fa, st);
+  }
+}
+
+template <typename XT, typename YT>
+int launch_fused_y(const FusedArgs& fa, cudaStream_t st) {
+  return fa.r_ps <= 4 ? launch_fused_t<XT, YT, 4>(fa, st) : launch_fused_t<XT, YT, 8>(fa, st);
+}
+
+template <typename XT>
+int launch_fused_x(const FusedArgs& fa, int ydt, cudaStream_t st) {
+  return ydt == MM_F32 ? launch_fused_y<XT, float>(fa, st) : launch_fused_y<XT, double>(fa, st);
+}
+
+int launch_fused(const FusedArgs& fa, int xdt, int ydt, cudaStream_t st) {
+  switch (xdt) {
+    case MM_F32: return launch_fused_x<float>(fa, ydt, st);
+    case MM_F64: return launch_fused_x<double>(fa, ydt, st);
+    case MM_I64: return launch_fused_x<long long>(fa, ydt, st);
+    default: return launch_fused_x<int>(fa, ydt, st);
+  }
+}
+
 int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
   if (!y) return fail(MM_EINVAL, "y is null");
   if (!ydt_ok(ydt)) return fail(MM_EINVAL, "y dtype must be f32 or f64");
@@ -545,6 +603,19 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   const int64_t k = (n_out - 2) * (r_ps / 2);
   if (k > N - 2) return fail(MM_EINVAL, "sub-buckets exceed interior");
   if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
+  if (fused_ok(B, N, n_out, r_ps, y_dtype)) {  // one CTA per series, everything on chip
+    FusedArgs fa{x, x_ld, y, y_ld, B, N, n_out, r_ps, out};
+    stage_mark(st, 0);
+    if ((rc = launch_fused(fa, x_dtype, y_dtype, st))) return rc;
+    stage_mark(st, 1);
+    stage_mark(st, 2);
+    stage_mark(st, 3);
+    if (out_count) {
+      k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
+      return check_launch("k_fill");
+    }
+    return MM_OK;
+  }
   const int64_t S = cdiv(N - 2, k);
   const ExPlan p = plan_extrema(B * k, S, y_dtype);
   const int64_t cap = 2 + 2 * k;

@@ -134,48 +134,21 @@ __device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k,
   return start + (b * len) / k;  // core.py:173 (host guarantees k*len < 2^63)
 }
 
-// One warp per (series, bucket, chunk).  Lanes stream 16-byte vectors
-// (U in flight per lane), keep a per-lane running min/max KEY plus the
-// position of the vector that first reached it (strict < / >, lane order is
-// index order => lane-local first occurrence), recover the exact element
-// from that vector at the end, then reduce (key, index) lexicographically
-// across the warp -- the same first-occurrence argmin/argmax as
-// _argminmax_range (_kernels.py:28-60) independent of evaluation order.
-//
-// G < 32: a G-lane group per item (small buckets, C == 1): 32/G buckets per
-// warp, each group still reading G*16 contiguous bytes per load, so a warp's
-// fixed costs (bounds, reduction, stores) are shared by several buckets.
-template <typename T, int U, int LDV, int MINB = 1, int G = 32>
-__global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
+// First-occurrence argmin/argmax (total-order keys) of y[lo, hi) by a group
+// of G lanes (lane = index within the group).  Offsets are int32 relative to
+// lo (INT_MAX = empty range); results are reduced across the group.  When a
+// vector improves the running extreme its raw 16 bytes are kept in
+// registers, so the exact element is recovered without re-reading memory (a
+// re-read would miss L2 on a long stream and cost extra DRAM traffic).
+template <typename T, int U, int LDV, int G>
+__device__ __forceinline__ void group_extrema(const T* y, int64_t lo, int64_t hi, int lane, typename YTr<T>::K& mn,
+                                              int& omn, typename YTr<T>::K& mx, int& omx) {
   typedef YTr<T> Tr;
   typedef typename Tr::K K;
-  const int lane = threadIdx.x & (G - 1);  // lane within the item's group
-  const int64_t w = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G) + (threadIdx.x & 31) / G;
-  const int64_t total = a.B * a.nb * a.C;
-  const bool live = w < total;
-  if (G == 32 && !live) return;  // warp-uniform
-  const int64_t c = live ? w % a.C : 0;
-  const int64_t t = live ? w / a.C : 0;
-  const int64_t b = a.b0 + t % a.nb;
-  const int64_t s = t / a.nb;
-  int64_t blo, bhi;
-  if (a.bounds) {
-    blo = a.bounds[b];
-    bhi = a.bounds[b + 1];
-  } else {
-    blo = pbound(a.start, a.len, a.k, b);
-    bhi = pbound(a.start, a.len, a.k, b + 1);
-  }
-  const int64_t lo = blo + c * a.chunk;
-  const int64_t hi = live ? min(bhi, lo + a.chunk) : lo;
-  const T* y = (const T*)a.y + s * a.y_ld;
-
-  // Offsets are int32 relative to the chunk start (host keeps chunk < 2^30).
-  // When a vector improves the running extreme its raw 16 bytes are kept in
-  // registers, so the exact element is recovered without re-reading memory
-  // (a re-read would miss L2 on a 4 GB stream and cost extra DRAM traffic).
-  K mn = Tr::kmax(), mx = Tr::kmin();
-  int omn = INT_MAX, omx = INT_MAX;
+  mn = Tr::kmax();
+  mx = Tr::kmin();
+  omn = INT_MAX;
+  omx = INT_MAX;
   bool vmn = false, vmx = false;
   uint4 rmn = make_uint4(0, 0, 0, 0), rmx = make_uint4(0, 0, 0, 0);
   if (lo < hi) {
@@ -244,6 +217,47 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
     const int oq = __shfl_xor_sync(FULL, omx, off);
     if (omx2 > mx || (omx2 == mx && oq < omx)) { mx = omx2; omx = oq; }
   }
+}
+
+// One warp per (series, bucket, chunk).  Lanes stream 16-byte vectors
+// (U in flight per lane), keep a per-lane running min/max KEY plus the
+// position of the vector that first reached it (strict < / >, lane order is
+// index order => lane-local first occurrence), recover the exact element
+// from that vector at the end, then reduce (key, index) lexicographically
+// across the warp -- the same first-occurrence argmin/argmax as
+// _argminmax_range (_kernels.py:28-60) independent of evaluation order.
+//
+// G < 32: a G-lane group per item (small buckets, C == 1): 32/G buckets per
+// warp, each group still reading G*16 contiguous bytes per load, so a warp's
+// fixed costs (bounds, reduction, stores) are shared by several buckets.
+template <typename T, int U, int LDV, int MINB = 1, int G = 32>
+__global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
+  typedef YTr<T> Tr;
+  typedef typename Tr::K K;
+  const int lane = threadIdx.x & (G - 1);  // lane within the item's group
+  const int64_t w = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G) + (threadIdx.x & 31) / G;
+  const int64_t total = a.B * a.nb * a.C;
+  const bool live = w < total;
+  if (G == 32 && !live) return;  // warp-uniform
+  const int64_t c = live ? w % a.C : 0;
+  const int64_t t = live ? w / a.C : 0;
+  const int64_t b = a.b0 + t % a.nb;
+  const int64_t s = t / a.nb;
+  int64_t blo, bhi;
+  if (a.bounds) {
+    blo = a.bounds[b];
+    bhi = a.bounds[b + 1];
+  } else {
+    blo = pbound(a.start, a.len, a.k, b);
+    bhi = pbound(a.start, a.len, a.k, b + 1);
+  }
+  const int64_t lo = blo + c * a.chunk;
+  const int64_t hi = live ? min(bhi, lo + a.chunk) : lo;
+  const T* y = (const T*)a.y + s * a.y_ld;
+
+  K mn, mx;
+  int omn, omx;
+  group_extrema<T, U, LDV, G>(y, lo, hi, lane, mn, omn, mx, omx);
   const int64_t pmn = omn == INT_MAX ? INT64_MAX : lo + omn;
   const int64_t pmx = omx == INT_MAX ? INT64_MAX : lo + omx;
   // publish: one chunk per bucket -> final; otherwise the last-arriving warp

@@ -325,3 +325,19 @@ def test_lttb_large_bucket_degenerate():
     yr = np.random.Generator(np.random.PCG64(1)).standard_normal(n)
     got = mm.lttb(torch.from_numpy(xr).to(DEV), torch.from_numpy(yr).to(DEV), 120).cpu().numpy()
     assert np.array_equal(got, O.lttb(xr, yr, 120))
+
+
+@pytest.mark.parametrize("r,ydt,xkind", [(2, np.float32, "i64"), (4, np.float64, "f64"), (6, np.float32, "f32"),
+                                          (8, np.float64, "i32")])
+def test_fused_batch_path(r, ydt, xkind):
+    """B >= 148 series, r_ps <= 8: the one-CTA-per-series fused kernel."""
+    rng = np.random.Generator(np.random.PCG64(r * 7))
+    B, n, n_out = 160, 30_011, 257
+    y = np.cumsum(rng.standard_normal((B, n)), axis=1).astype(ydt)
+    y[3, ::7] = -0.0
+    y[5] = 1.0  # constant row: every argmin == argmax
+    x = {"i64": np.arange(n, dtype=np.int64), "f64": np.cumsum(rng.exponential(1.0, n)),
+         "f32": np.arange(n, dtype=np.float32), "i32": np.arange(n, dtype=np.int32) * 3}[xkind]
+    out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out, minmax_ratio=r).cpu().numpy()
+    for i in range(B):
+        assert np.array_equal(out[i], O.minmaxlttb(x, y[i].astype(np.float64), n_out, r)), i
