@@ -387,8 +387,12 @@ int launch_pairs(PairArgs pa, int64_t B, cudaStream_t st) {
   const int64_t tiles = std::max<int64_t>(1, cdiv(pa.nb, PAIR_NT * PAIR_ITEMS));
   if (B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
   const dim3 g((unsigned)tiles, (unsigned)B);
-  if (!pa.out_x) { pa.x = pa.y = nullptr; pairs_t<double, double>(pa, g, st); return check_launch("k_compact_pairs"); }
   const bool y32 = pa.ydt == MM_F32;
+  if (!pa.out_x) {  // no gather: x unused; y only read for the endpoint finite check
+    pa.x = nullptr;
+    y32 ? pairs_t<double, float>(pa, g, st) : pairs_t<double, double>(pa, g, st);
+    return check_launch("k_compact_pairs");
+  }
   switch (pa.xdt) {
     case MM_F32: y32 ? pairs_t<float, float>(pa, g, st) : pairs_t<float, double>(pa, g, st); break;
     case MM_F64: y32 ? pairs_t<double, float>(pa, g, st) : pairs_t<double, double>(pa, g, st); break;
@@ -455,6 +459,14 @@ int launch_fused(const FusedArgs& fa, int xdt, int ydt, cudaStream_t st) {
   }
 }
 
+// First 256 bytes of every fused entry's workspace: status word (bit 0 =
+// non-finite y seen), zeroed on the stream at entry.
+int* take_status(Carve& cv, cudaStream_t st) {
+  int* p = cv.take<int>(1);
+  if (p && cudaMemsetAsync(p, 0, sizeof(int), st) != cudaSuccess) return nullptr;
+  return p;
+}
+
 int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
   if (!y) return fail(MM_EINVAL, "y is null");
   if (!ydt_ok(ydt)) return fail(MM_EINVAL, "y dtype must be f32 or f64");
@@ -507,17 +519,17 @@ int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int6
     case MM_OP_MINMAXLTTB:
       if (r_ps == 1) return mmlttb_workspace_bytes(MM_OP_MINMAX, B, N, n_out, 0, y_dtype);
       if (r_ps < 2 || r_ps % 2) return 0;
-      return preselect_ws(B, N, n_out, r_ps, y_dtype, true);
+      return ALIGN + preselect_ws(B, N, n_out, r_ps, y_dtype, true);
     case MM_OP_PRESELECT:
       if (r_ps < 2 || r_ps % 2) return 0;
-      return preselect_ws(B, N, n_out, r_ps, y_dtype, false);
+      return ALIGN + preselect_ws(B, N, n_out, r_ps, y_dtype, false);
     case MM_OP_LTTB:
       return lttb_ws(B, n_out, cdiv(N - 2, n_out - 2));
     case MM_OP_MINMAX:
     case MM_OP_M4: {
       const int64_t k = op == MM_OP_MINMAX ? n_out / 2 : n_out / 4;
       if (k < 1) return 0;
-      return ex_ws(B * k, plan_extrema(B * k, cdiv(N, k), y_dtype));
+      return ALIGN + ex_ws(B * k, plan_extrema(B * k, cdiv(N, k), y_dtype));
     }
   }
   return 0;
@@ -537,13 +549,15 @@ int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B,
   const int64_t S = cdiv(N - 2, k);
   const ExPlan p = plan_extrema(B * k, S, y_dtype);
   Carve cv{(char*)workspace, workspace_bytes};
+  int* status = take_status(cv, st);
   ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
-  if (!carve_ex(cv, B * k, p, ea)) return fail(MM_EWORKSPACE, "workspace too small");
+  if (!carve_ex(cv, B * k, p, ea) || !status) return fail(MM_EWORKSPACE, "workspace too small");
   if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
   PairArgs pa{};
   pa.ext = ea.ext; pa.cnt8 = ea.cnt8; pa.nb = k;
   pa.emit_first = 0; pa.emit_last = N - 1;
   pa.out_idx = out; pa.out_ld = out_ld; pa.out_count = out_count;
+  pa.y = y; pa.ydt = y_dtype; pa.y_ld = y_ld; pa.status = status;
   return launch_pairs(pa, B, st);
 }
 
@@ -557,18 +571,21 @@ static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t 
   if (!mul_ok(k + 1, N)) return fail(MM_ERANGE, "k*N overflows int64");
   const ExPlan p = plan_extrema(B * k, cdiv(N, k), ydt);
   Carve cv{(char*)ws, wsb};
+  int* status = take_status(cv, st);
   ExArgs ea{y, y_ld, B, 0, N, k, nullptr, 0, k, p.C, p.chunk};
-  if (!carve_ex(cv, B * k, p, ea)) return fail(MM_EWORKSPACE, "workspace too small");
+  if (!carve_ex(cv, B * k, p, ea) || !status) return fail(MM_EWORKSPACE, "workspace too small");
   if ((rc = launch_extrema(ea, ydt, st))) return rc;
   if (!m4 && force_n_out == 0) {
     PairArgs pa{};
     pa.ext = ea.ext; pa.cnt8 = ea.cnt8; pa.nb = k;
     pa.emit_first = -1; pa.emit_last = -1;
     pa.out_idx = out; pa.out_ld = n_out; pa.out_count = out_count;
+    pa.y = y; pa.ydt = ydt; pa.y_ld = y_ld; pa.status = status;
     return launch_pairs(pa, B, st);
   }
   CompactArgs ca{};
   ca.ext = ea.ext; ca.nb = k; ca.mode = m4 ? 1 : 0;
+  ca.ydt = ydt; ca.status = status;
   ca.emit_first = -1; ca.emit_last = -1; ca.force_n_out = force_n_out; ca.last_index = N - 1;
   ca.start = 0; ca.len = N; ca.k = k; ca.b0 = 0;
   ca.out_idx = out; ca.out_ld = n_out; ca.out_count = out_count;
@@ -603,8 +620,11 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   const int64_t k = (n_out - 2) * (r_ps / 2);
   if (k > N - 2) return fail(MM_EINVAL, "sub-buckets exceed interior");
   if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
+  Carve cv0{(char*)workspace, workspace_bytes};
+  int* status = take_status(cv0, st);
+  if (!status) return fail(MM_EWORKSPACE, "workspace too small");
   if (fused_ok(B, N, n_out, r_ps, y_dtype)) {  // one CTA per series, everything on chip
-    FusedArgs fa{x, x_ld, y, y_ld, B, N, n_out, r_ps, out};
+    FusedArgs fa{x, x_ld, y, y_ld, B, N, n_out, r_ps, out, status};
     stage_mark(st, 0);
     if ((rc = launch_fused(fa, x_dtype, y_dtype, st))) return rc;
     stage_mark(st, 1);
@@ -619,7 +639,7 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   const int64_t S = cdiv(N - 2, k);
   const ExPlan p = plan_extrema(B * k, S, y_dtype);
   const int64_t cap = 2 + 2 * k;
-  Carve cv{(char*)workspace, workspace_bytes};
+  Carve cv = cv0;
   ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
   carve_ex(cv, B * k, p, ea);
   int64_t* cnt = cv.take<int64_t>(B);
@@ -639,7 +659,7 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   pa.out_idx = pre; pa.out_ld = cap; pa.out_count = cnt;
   pa.x = x; pa.xdt = x_dtype; pa.x_ld = x_ld;
   pa.y = y; pa.ydt = y_dtype; pa.y_ld = y_ld;
-  pa.out_x = px; pa.out_y = py;
+  pa.out_x = px; pa.out_y = py; pa.status = status;
   if ((rc = launch_pairs(pa, B, st))) return rc;
   stage_mark(st, 2);
   // K3: LTTB over the compacted sub-series, mapped back (:208-209)

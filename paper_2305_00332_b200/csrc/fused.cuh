@@ -23,6 +23,7 @@ struct FusedArgs {
   const void* y; int64_t y_ld;
   int64_t B, N, n_out, r_ps;
   int64_t* out;                 // [B][n_out]
+  int* status;                  // bit 0: non-finite y seen (may be null)
 };
 
 // shared-memory bytes for a series with k sub-buckets (m <= 2k + 2 points);
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused(FusedArgs a) {
     int omn, omx;
     group_extrema<YT, U, 3, G>(ys, lo, hi, lane8, mn, omn, mx, omx);
     if (lane8 == 0 && b < k) {
+      if (a.status && keys_nonfinite((long long)mn, (long long)mx, sizeof(YT) == 4 ? 0 : 1)) atomicOr(a.status, 1);
       const bool mfirst = omn <= omx;
       s_lo[b] = (int)(lo + (mfirst ? omn : omx));
       s_hi[b] = (int)(lo + (mfirst ? omx : omn));
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused(FusedArgs a) {
     carry += tot;
   }
   if (threadIdx.x == 0) {
+    if (a.status && (!isfinite((double)ys[0]) || !isfinite((double)ys[N - 1]))) atomicOr(a.status, 1);
     s_pre[0] = 0; s_py[0] = ys[0];
     s_pre[carry] = (int)(N - 1); s_py[carry] = ys[N - 1];
   }

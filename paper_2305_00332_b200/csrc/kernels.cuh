@@ -94,6 +94,14 @@ template <> __device__ __forceinline__ double to_f64<long long>(const long long*
 }
 template <> __device__ __forceinline__ double to_f64<int>(const int* p, int64_t i) { return (double)__ldg(p + i); }
 
+// Non-finite detection for free: every NaN/inf maps outside the open key
+// interval (key(-inf), key(+inf)), so a bucket holds one iff its min key is
+// <= key(-inf) or its max key >= key(+inf) (TimeSeries check, core.py:89-90).
+__device__ __forceinline__ bool keys_nonfinite(long long kmin, long long kmax, int ydt) {
+  if (ydt == 0) return kmin <= (long long)(int32_t)0x807fffff || kmax >= 0x7f800000LL;
+  return kmin <= (long long)0x800fffffffffffffULL || kmax >= 0x7ff0000000000000LL;
+}
+
 // ------------------------------------------------------- K1 partials ----
 struct Partial {
   long long kmin, kmax;  // total-order keys (sign-extended for f32)
@@ -358,6 +366,7 @@ struct CompactArgs {
   const void* y; int ydt; int64_t y_ld; int64_t y_off;
   double* out_x;            // may be null
   double* out_y;
+  int* status;              // bit 0: non-finite y seen (may be null)
 };
 
 __device__ __forceinline__ double load_any(const void* p, int dt, int64_t i) {
@@ -388,6 +397,7 @@ __global__ void __launch_bounds__(NT) k_compact(CompactArgs a) {
   };
   auto items_of = [&](int64_t bl, int64_t* it) -> int {
     const int64_t imin = ext[bl].imin, imax = ext[bl].imax;
+    if (a.status && keys_nonfinite(ext[bl].kmin, ext[bl].kmax, a.ydt)) atomicOr(a.status, 1);
     const int64_t lo = min(imin, imax), hi = max(imin, imax);
     if (a.mode == 0) {  // downsamplers.py:60-69
       it[0] = lo; it[1] = hi;
@@ -477,6 +487,7 @@ struct PairArgs {
   const void* x; int xdt; int64_t x_ld;
   const void* y; int ydt; int64_t y_ld;
   double* out_x; double* out_y;    // may be null (no gather)
+  int* status;                     // bit 0: non-finite y seen (may be null)
 };
 
 template <typename XT, typename YT, int NT, int ITEMS>
@@ -511,6 +522,7 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
     Ext e;
     e.imin = e.imax = e.kmin = e.kmax = 0;
     if (ok) e = ext[bl];
+    if (ok && a.status && keys_nonfinite(e.kmin, e.kmax, a.ydt)) atomicOr(a.status, 1);
     const bool mfirst = e.imin <= e.imax;
     v[2 * i] = mfirst ? e.imin : e.imax;  // downsamplers.py:60-69
     v[2 * i + 1] = mfirst ? e.imax : e.imin;
@@ -554,7 +566,12 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
         a.out_y[s * a.out_ld + pos] = to_f64(ys, v);
       }
     };
-    if (blockIdx.x == 0 && a.emit_first >= 0) emit(0, a.emit_first);
+    if (blockIdx.x == 0 && a.emit_first >= 0) {
+      emit(0, a.emit_first);
+      if (a.status && !isfinite(to_f64(ys, a.emit_first))) atomicOr(a.status, 1);
+    }
+    if (blockIdx.x == gridDim.x - 1 && a.emit_last >= 0 && a.status && !isfinite(to_f64(ys, a.emit_last)))
+      atomicOr(a.status, 1);
     if (blockIdx.x == gridDim.x - 1) {
       int64_t end = (a.emit_first >= 0 ? 1 : 0) + off + tot;
       if (a.emit_last >= 0) emit(end++, a.emit_last);

@@ -27,6 +27,8 @@ from . import _native as N
 from .core import Algorithm, DownsampleConfig, TimeSeries, validate
 from .errors import (
     BadPreselectionRatio,
+    NonFiniteValue,
+    NonMonotonicX,
     NotParallelizable,
     NOutNotDivisibleBy4,
     NOutOfRange,
@@ -52,9 +54,12 @@ class Batch:
     ``ready()``, after the reference's O(1) checks have passed.
     """
 
-    def __init__(self, x, y, device=None):
+    def __init__(self, x, y, device=None, validate=None):
         self._x_in, self._y_in, self._dev_in = x, y, device
         self.host = not (isinstance(y, torch.Tensor) and y.is_cuda)
+        # None: host inputs get the free non-finite-y check (raised after the
+        # call, which syncs anyway); True: full TimeSeries invariants first
+        self.validate = validate
         self.numpy = not isinstance(y, torch.Tensor)
         shape = tuple(y.shape) if hasattr(y, "shape") else np.shape(y)
         if len(shape) not in (1, 2):
@@ -92,7 +97,35 @@ class Batch:
             self.x = xt
             self.x_ld = self.n if xt.dim() == 2 else 0
         self._ready = True
+        if self.validate:
+            self._full_validate()
         return self
+
+    def _full_validate(self):
+        """TimeSeries invariants (core.py:80-94) on device, per row: one sync."""
+        if self.x is None:
+            return
+        xs = self.x if self.x.is_cuda else self.x.to(self.device)
+        flags = torch.zeros(1, dtype=torch.int32, device=self.device)
+        acc = 0
+        with torch.cuda.device(self.device):
+            for i in range(self.B):
+                xi = xs if xs.dim() == 1 else xs[i]
+                N.check(N.lib().mmlttb_validate(xi.data_ptr(), N.DTYPE_CODE[xi.dtype], self.y[i].data_ptr(),
+                                                N.DTYPE_CODE[self.y.dtype], self.n, flags.data_ptr(),
+                                                N.stream_ptr(self.device)), "validate", self.n)
+                acc |= int(flags.item())
+        if acc & 1:
+            raise NonFiniteValue("series contains NaN or infinite values")
+        if acc & 2:
+            raise NonMonotonicX("xs must be sorted in non-decreasing order")
+
+    def post_check(self, ws: torch.Tensor) -> None:
+        """Raise the reference's NonFiniteValue from the kernels' status word."""
+        if self.validate is False or (self.validate is None and not self.host):
+            return
+        if int(ws[:4].view(torch.int32)[0].item()) & 1:
+            raise NonFiniteValue("series contains NaN or infinite values")
 
     def ret(self, t: torch.Tensor):
         if self.squeeze:
@@ -101,10 +134,11 @@ class Batch:
 
 
 class _Series(Batch):
-    """Adapter: a TimeSeries seen as a 1-series Batch."""
+    """Adapter: a TimeSeries seen as a 1-series Batch (already validated)."""
 
     def __init__(self, series: TimeSeries, device=None):
         self._series, self._dev_in = series, device
+        self.validate = False
         self.host = self.numpy = series.is_host
         self.squeeze = True
         self.B, self.n = 1, len(series)
@@ -200,6 +234,7 @@ def _minmax_like(b, n_out, op: str, force: bool = False):
             ws = N.workspace(wsb, b.device, b.n)
             N.check(fn(b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out, out.data_ptr(), cnt.data_ptr(), ws.data_ptr(),
                        wsb, st), op, b.n)
+    b.post_check(ws)
     return _counted(b, out, cnt)
 
 
@@ -209,7 +244,7 @@ def minmax(series, n_out, parallel=False, *args, **kw):
     Flat form: ``minmax(x, y, n_out)``.
     """
     if _is_flat(series):
-        b, n_out = Batch(series, n_out, kw.get("device")), parallel
+        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), parallel
     else:
         b = _Series(series)
     _check_n_out(b.n, n_out)
@@ -221,7 +256,7 @@ def minmax(series, n_out, parallel=False, *args, **kw):
 def m4(series, n_out, parallel=False, *args, **kw):
     """First, min, max and last sample per bucket (downsamplers.py:95-112)."""
     if _is_flat(series):
-        b, n_out = Batch(series, n_out, kw.get("device")), parallel
+        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), parallel
     else:
         b = _Series(series)
     _check_n_out(b.n, n_out)
@@ -236,7 +271,7 @@ def lttb(series, n_out, *args, **kw):
     Flat form: ``lttb(x, y, n_out)``.
     """
     if _is_flat(series):
-        b, n_out = Batch(series, n_out, kw.get("device")), args[0]
+        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), args[0]
     else:
         b = _Series(series)
     _check_n_out(b.n, n_out)
@@ -260,7 +295,7 @@ def minmax_preselect(series, n_out, r_ps, parallel=False, *args, **kw):
     Flat form: ``minmax_preselect(x, y, n_out, r_ps)``.
     """
     if _is_flat(series):
-        b, n_out, r_ps = Batch(series, n_out, kw.get("device")), r_ps, parallel
+        b, n_out, r_ps = Batch(series, n_out, kw.get("device"), kw.get("validate")), r_ps, parallel
     else:
         b = _Series(series)
     k = _check_preselect(b.n, n_out, r_ps)
@@ -275,6 +310,7 @@ def minmax_preselect(series, n_out, r_ps, parallel=False, *args, **kw):
         N.check(N.lib().mmlttb_minmax_preselect(b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out, r_ps, out.data_ptr(),
                                                 cap, cnt.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(b.device)),
                 "minmax_preselect", b.n)
+    b.post_check(ws)
     return _counted(b, out, cnt)
 
 
@@ -288,10 +324,11 @@ def _minmaxlttb_batch(b, n_out: int, r_ps: int):
         N.check(N.lib().mmlttb_minmaxlttb(N.ptr(b.x), xdt, b.x_ld, b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out,
                                           r_ps, out.data_ptr(), None, ws.data_ptr(), wsb, N.stream_ptr(b.device)),
                 "minmaxlttb", b.n)
+    b.post_check(ws)
     return b.ret(out)
 
 
-def minmaxlttb(series, n_out, r_ps=4, parallel=False, *args, minmax_ratio=None, device=None):
+def minmaxlttb(series, n_out, r_ps=4, parallel=False, *args, minmax_ratio=None, device=None, validate=None):
     """MinMax preselection, then LTTB on the candidates (downsamplers.py:182-209).
 
     Reference form: ``minmaxlttb(series, n_out, r_ps=4, parallel=False)``.
@@ -302,7 +339,7 @@ def minmaxlttb(series, n_out, r_ps=4, parallel=False, *args, minmax_ratio=None, 
         x, y = series, n_out
         n_out = r_ps
         ratio = minmax_ratio if minmax_ratio is not None else (parallel if not isinstance(parallel, bool) else 4)
-        b = Batch(x, y, device)
+        b = Batch(x, y, device, validate)
         r_ps = int(ratio)
     else:
         if minmax_ratio is not None:

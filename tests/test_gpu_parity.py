@@ -341,3 +341,34 @@ def test_fused_batch_path(r, ydt, xkind):
     out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out, minmax_ratio=r).cpu().numpy()
     for i in range(B):
         assert np.array_equal(out[i], O.minmaxlttb(x, y[i].astype(np.float64), n_out, r)), i
+
+
+def test_flat_api_nonfinite_parity():
+    """The reference rejects NaN/inf at TimeSeries construction (core.py:89-90);
+    the flat form detects it for free from the K1 keys (host inputs) or on
+    request (validate=True for device inputs)."""
+    n = 50_000
+    x = np.arange(n, dtype=np.int64)
+    for ydt in (np.float32, np.float64):
+        for bad in (np.nan, np.inf, -np.inf):
+            for pos in (0, 777, n - 1):
+                y = np.cumsum(np.ones(n)).astype(ydt)
+                y[pos] = bad
+                with pytest.raises(errors.NonFiniteValue):
+                    mm.minmaxlttb(x, y, 100, minmax_ratio=4)
+                with pytest.raises(errors.NonFiniteValue):
+                    mm.minmax(x, y, 100)
+                with pytest.raises(errors.NonFiniteValue):
+                    mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), 100, minmax_ratio=4,
+                                  validate=True)
+    yb = torch.randn(4, n, device=DEV)
+    yb[2, 5] = float("nan")
+    with pytest.raises(errors.NonFiniteValue):
+        mm.minmaxlttb(torch.from_numpy(x).to(DEV), yb, 100, minmax_ratio=4, validate=True)
+    xd = torch.from_numpy(x.copy()).to(DEV)
+    xd[100] = 5
+    with pytest.raises(errors.NonMonotonicX):
+        mm.minmaxlttb(xd, torch.randn(n, device=DEV), 100, minmax_ratio=4, validate=True)
+    # device inputs without validate: no sync, no raise (garbage in, indices out)
+    out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), yb, 100, minmax_ratio=4)
+    assert out.shape == (4, 100)
