@@ -96,27 +96,43 @@ struct Carve {
 // ---- K1 planning --------------------------------------------------------
 struct ExPlan {
   int64_t C, chunk, Cmax;
+  int64_t E = 0, Ws = 0, CP = 0;  // flat mode (E > 0): elements/warp, warps/series, partial stride
 };
 
 // Chunks per bucket: enough warps for ~4 waves over 148 SMs x 32 resident
 // warps, never a chunk under MIN_CHUNK elements; buckets of <= 4096 points
-// are one item each (8-lane groups).  The partial buffer is
-// sized for Cmax, which depends only on the bucket count (not on N), so the
-// auxiliary memory stays O(B*k) (acceptance #11).
+// are one item each (8-lane groups).  Large buckets of closed-form partitions
+// use the flat split (k_extrema_flat): equal element ranges per warp.
 constexpr int64_t SMALL_BUCKET = 4096;  // elements: <= this -> one 8-lane group per bucket
 
 int64_t env_i64(const char* name, int64_t dflt) {
-  const char* e = getenv(name);  // tuning knobs for tools/k1_sweep.sh only
+  const char* e = getenv(name);  // tuning knobs for tools/*.sh only
   return e ? atoll(e) : dflt;
 }
 
-ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt) {
+ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, int64_t B = 0, bool closed_form = false) {
   // tuned on B200 (tools/plan_sweep.sh): ~4 waves of 148 SMs x 32 resident
   // warps, chunks of >= 4096 float32 elements
   static const int64_t want = env_i64("MMLTTB_K1_WANT_WARPS", 148LL * 128);
   static const int64_t minc32 = env_i64("MMLTTB_K1_MIN_CHUNK", 4096);
+  // flat split: one wave of 148 SMs x 24 resident warps (80 regs), two for
+  // very long series (tools/flat_sweep.sh)
+  static const int64_t flat_env = env_i64("MMLTTB_K1_FLAT_WARPS", -1);
   const int64_t min_chunk = ydt == MM_F32 ? minc32 : minc32 / 2;
   ExPlan p;
+  const int64_t nb_ = B > 0 ? buckets_total / B : 0;
+  const int64_t flat_warps = flat_env >= 0 ? flat_env : (nb_ * max_bucket > 400000000LL ? 148LL * 48 : 148LL * 24);
+  if (closed_form && B > 0 && max_bucket > SMALL_BUCKET && flat_warps > 0) {
+    const int64_t nb = nb_;
+    p.Ws = std::max<int64_t>(1, flat_warps / B);
+    p.E = std::max<int64_t>(min_chunk, cdiv(nb * max_bucket, p.Ws));
+    p.Ws = cdiv(nb * max_bucket, p.E);
+    p.CP = cdiv(max_bucket, p.E) + 1;
+    p.C = 1;
+    p.chunk = p.E;
+    p.Cmax = p.CP;
+    return p;
+  }
   p.Cmax = std::max<int64_t>(1, std::min<int64_t>(256, cdiv(want, std::max<int64_t>(1, buckets_total))));
   p.C = max_bucket <= SMALL_BUCKET ? 1 : std::max<int64_t>(1, std::min<int64_t>(p.Cmax, cdiv(max_bucket, min_chunk)));
   p.chunk = cdiv(max_bucket, p.C);
@@ -131,6 +147,9 @@ int64_t ex_ws(int64_t nbt, const ExPlan& p) {
 }
 
 bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
+  a.E = p.E;
+  a.Ws = p.Ws;
+  a.CP = p.CP;
   a.ext = cv.take<Ext>(nbt);
   a.cnt8 = cv.take<unsigned char>(nbt);
   a.part = nullptr;
@@ -143,6 +162,16 @@ bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
 }
 
 int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
+  if (a.E > 0) {  // flat split
+    if (cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
+      return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
+    const int64_t blocks = cdiv(a.B * a.Ws, 8);
+    if (ydt == MM_F32)
+      k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else
+      k_extrema_flat<double, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+    return check_launch("k_extrema_flat");
+  }
   const bool small = a.C == 1 && a.chunk <= SMALL_BUCKET;
   if (small) {
     const int64_t blocks = cdiv(a.B * a.nb, 8 * 4);
@@ -368,7 +397,7 @@ int launch_lttb(LttbArgs a, int xdt, int ydt, int64_t s, cudaStream_t st) {
 int64_t preselect_ws(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt, bool with_lttb) {
   const int64_t k = (n_out - 2) * (r_ps / 2);
   const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * k, S, ydt);
+  const ExPlan p = plan_extrema(B * k, S, ydt, B, true);
   const int64_t cap = 2 + 2 * k;
   int64_t bytes = ex_ws(B * k, p) + up(B * 8);
   if (with_lttb) bytes += 3 * up(B * cap * 8) + lttb_ws(B, n_out, r_ps);
@@ -529,7 +558,7 @@ int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int6
     case MM_OP_M4: {
       const int64_t k = op == MM_OP_MINMAX ? n_out / 2 : n_out / 4;
       if (k < 1) return 0;
-      return ALIGN + ex_ws(B * k, plan_extrema(B * k, cdiv(N, k), y_dtype));
+      return ALIGN + ex_ws(B * k, plan_extrema(B * k, cdiv(N, k), y_dtype, B, true));
     }
   }
   return 0;
@@ -547,7 +576,7 @@ int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B,
   if (out_ld < 2 + 2 * k) return fail(MM_EINVAL, "out_ld < 2 + 2k");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * k, S, y_dtype);
+  const ExPlan p = plan_extrema(B * k, S, y_dtype, B, true);
   Carve cv{(char*)workspace, workspace_bytes};
   int* status = take_status(cv, st);
   ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
@@ -569,7 +598,7 @@ static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t 
   const int64_t k = m4 ? n_out / 4 : n_out / 2;
   if ((m4 && n_out % 4) || (!m4 && n_out % 2)) return fail(MM_EINVAL, "n_out divisibility");
   if (!mul_ok(k + 1, N)) return fail(MM_ERANGE, "k*N overflows int64");
-  const ExPlan p = plan_extrema(B * k, cdiv(N, k), ydt);
+  const ExPlan p = plan_extrema(B * k, cdiv(N, k), ydt, B, true);
   Carve cv{(char*)ws, wsb};
   int* status = take_status(cv, st);
   ExArgs ea{y, y_ld, B, 0, N, k, nullptr, 0, k, p.C, p.chunk};
@@ -637,7 +666,7 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
     return MM_OK;
   }
   const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * k, S, y_dtype);
+  const ExPlan p = plan_extrema(B * k, S, y_dtype, B, true);
   const int64_t cap = 2 + 2 * k;
   Carve cv = cv0;
   ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
@@ -737,7 +766,8 @@ int mmlttb_lttb_select(const void* xs, int x_dtype, const void* ys, int y_dtype,
 int64_t mmlttb_shard_workspace_bytes(int64_t N, int64_t n_out, int64_t r_ps, int64_t b0, int64_t b1) {
   const int64_t k = (n_out - 2) * (r_ps / 2);
   if (k < 1 || b1 <= b0) return ALIGN;
-  return ex_ws(b1 - b0, plan_extrema(b1 - b0, cdiv(N - 2, k), MM_F32));
+  return std::max(ex_ws(b1 - b0, plan_extrema(b1 - b0, cdiv(N - 2, k), MM_F32, 1, true)),
+                  ex_ws(b1 - b0, plan_extrema(b1 - b0, cdiv(N - 2, k), MM_F64, 1, true)));
 }
 
 int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard, int y_dtype, int64_t lo, int64_t N,
@@ -753,7 +783,7 @@ int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard
   if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nb = b1 - b0;
-  const ExPlan p = plan_extrema(std::max<int64_t>(nb, 1), cdiv(N - 2, k), y_dtype);
+  const ExPlan p = plan_extrema(std::max<int64_t>(nb, 1), cdiv(N - 2, k), y_dtype, 1, true);
   Carve cv{(char*)workspace, workspace_bytes};
   // virtual base: element i of the global series lives at y_shard[i - lo]
   const void* ybase = (const char*)y_shard - lo * esize(y_dtype);

@@ -121,6 +121,7 @@ struct ExArgs {
   unsigned* arrivals;      // [B][nb]      zeroed per call (C > 1 only)
   struct Ext* ext;         // [B][nb]      final (imin, imax) per bucket
   unsigned char* cnt8;     // [B][nb]      1 + (imin != imax): K2's scan input
+  int64_t E, Ws, CP;       // flat mode: elements per warp, warps per series, partial stride
 };
 
 struct Ext {
@@ -227,6 +228,97 @@ __device__ __forceinline__ void group_extrema(const T* y, int64_t lo, int64_t hi
   }
 }
 
+__device__ __forceinline__ void write_ext(const ExArgs& a, int64_t bkt, int64_t pmn, int64_t pmx, long long kmn,
+                                          long long kmx) {
+  a.ext[bkt].imin = pmn;
+  a.ext[bkt].imax = pmx;
+  a.ext[bkt].kmin = kmn;
+  a.ext[bkt].kmax = kmx;
+  a.cnt8[bkt] = (unsigned char)(pmn != pmx ? 2 : 1);
+}
+
+// Partial `slot` (of `target` contributors) of bucket `bkt`: the last warp to
+// arrive combines all partials lexicographically and writes the Ext (whole
+// warp must call; lane 0 publishes).
+__device__ __forceinline__ void publish_partial(const ExArgs& a, int64_t bkt, int64_t slot, int64_t stride,
+                                                int64_t target, long long mn, long long mx, int64_t pmn,
+                                                int64_t pmx, int lane) {
+  if (target == 1) {
+    if (lane == 0) write_ext(a, bkt, pmn, pmx, mn, mx);
+    return;
+  }
+  unsigned last = 0;
+  if (lane == 0) {
+    Partial p;
+    p.kmin = mn; p.kmax = mx; p.imin = pmn; p.imax = pmx;
+    a.part[bkt * stride + slot] = p;
+    __threadfence();
+    last = atomicAdd(&a.arrivals[bkt], 1u) == (unsigned)(target - 1);
+  }
+  last = __shfl_sync(FULL, last, 0);
+  if (!last) return;
+  __threadfence();
+  long long cmn = LLONG_MAX, cmx = LLONG_MIN;
+  int64_t cimn = INT64_MAX, cimx = INT64_MAX;
+  const Partial* pp = a.part + bkt * stride;
+  for (int64_t c2 = lane; c2 < target; c2 += 32) {
+    const long long kmn = __ldcg(&pp[c2].kmin), kmx = __ldcg(&pp[c2].kmax);
+    const long long qmn = __ldcg(&pp[c2].imin), qmx = __ldcg(&pp[c2].imax);
+    if (kmn < cmn || (kmn == cmn && qmn < cimn)) { cmn = kmn; cimn = qmn; }
+    if (kmx > cmx || (kmx == cmx && qmx < cimx)) { cmx = kmx; cimx = qmx; }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const long long omn = __shfl_xor_sync(FULL, cmn, off);
+    const int64_t oimn = __shfl_xor_sync(FULL, cimn, off);
+    if (omn < cmn || (omn == cmn && oimn < cimn)) { cmn = omn; cimn = oimn; }
+    const long long omx = __shfl_xor_sync(FULL, cmx, off);
+    const int64_t oimx = __shfl_xor_sync(FULL, cimx, off);
+    if (omx > cmx || (omx == cmx && oimx < cimx)) { cmx = omx; cimx = oimx; }
+  }
+  if (lane == 0) {
+    write_ext(a, bkt, cimn, cimx, cmn, cmx);
+    a.arrivals[bkt] = 0;  // leave the counter reusable
+  }
+}
+
+// Flat K1 (large buckets): warp w of series s streams the contiguous element
+// range [E_lo + w*E, E_lo + (w+1)*E) whatever the bucket edges, so every warp
+// does the same work (no last-wave tail); a range spanning bucket edges
+// publishes one partial per intersected bucket (slot = w - first warp of the
+// bucket), combined by the bucket's last-arriving warp.
+template <typename T, int U, int LDV>
+__global__ void __launch_bounds__(256, 3) k_extrema_flat(ExArgs a) {
+  typedef YTr<T> Tr;
+  typedef typename Tr::K K;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= a.B * a.Ws) return;  // warp-uniform
+  const int64_t s = w / a.Ws, wl = w % a.Ws;
+  const T* y = (const T*)a.y + s * a.y_ld;
+  const int64_t E_lo = pbound(a.start, a.len, a.k, a.b0), E_hi = pbound(a.start, a.len, a.k, a.b0 + a.nb);
+  const int64_t e0 = E_lo + wl * a.E;
+  const int64_t e1 = min(E_hi, e0 + a.E);
+  if (e0 >= e1) return;
+  // bucket of e0 in partition(start, start+len, k): floor(((e0-start+1)*k - 1) / len)
+  int64_t b = (((e0 - a.start + 1) * a.k) - 1) / a.len;
+  for (;;) {
+    const int64_t blo = pbound(a.start, a.len, a.k, b), bhi = pbound(a.start, a.len, a.k, b + 1);
+    const int64_t lo = max(e0, blo), hi = min(e1, bhi);
+    K mn, mx;
+    int omn, omx;
+    group_extrema<T, U, LDV, 32>(y, lo, hi, lane, mn, omn, mx, omx);
+    const int64_t pmn = omn == INT_MAX ? INT64_MAX : lo + omn;
+    const int64_t pmx = omx == INT_MAX ? INT64_MAX : lo + omx;
+    const int64_t wf = (max(blo, E_lo) - E_lo) / a.E;
+    const int64_t wt = (min(bhi, E_hi) - 1 - E_lo) / a.E;
+    publish_partial(a, s * a.nb + (b - a.b0), wl - wf, a.CP, wt - wf + 1, (long long)mn, (long long)mx, pmn, pmx,
+                    lane);
+    if (bhi >= e1) break;
+    ++b;
+  }
+}
+
 // One warp per (series, bucket, chunk).  Lanes stream 16-byte vectors
 // (U in flight per lane), keep a per-lane running min/max KEY plus the
 // position of the vector that first reached it (strict < / >, lane order is
@@ -271,54 +363,11 @@ __global__ void __launch_bounds__(256, MINB) k_extrema(ExArgs a) {
   // publish: one chunk per bucket -> final; otherwise the last-arriving warp
   // of the bucket combines all C partials (threadfence-reduction pattern), so
   // no separate combine pass and no single-CTA bottleneck downstream.
-  const int64_t bkt = t;  // s * nb + (b - b0)
   if (G < 32 || a.C == 1) {  // (G < 32 is only launched with C == 1)
-    if (lane == 0 && live) {
-      a.ext[bkt].imin = pmn;
-      a.ext[bkt].imax = pmx;
-      a.ext[bkt].kmin = (long long)mn;
-      a.ext[bkt].kmax = (long long)mx;
-      a.cnt8[bkt] = (unsigned char)(pmn != pmx ? 2 : 1);
-    }
+    if (lane == 0 && live) write_ext(a, t, pmn, pmx, (long long)mn, (long long)mx);
     return;
   }
-  unsigned last = 0;
-  if (lane == 0) {
-    Partial p;
-    p.kmin = (long long)mn; p.kmax = (long long)mx; p.imin = pmn; p.imax = pmx;
-    a.part[w] = p;
-    __threadfence();
-    last = atomicAdd(&a.arrivals[bkt], 1u) == (unsigned)(a.C - 1);
-  }
-  last = __shfl_sync(FULL, last, 0);
-  if (!last) return;
-  __threadfence();
-  long long cmn = LLONG_MAX, cmx = LLONG_MIN;
-  int64_t cimn = INT64_MAX, cimx = INT64_MAX;
-  const Partial* pp = a.part + bkt * a.C;
-  for (int64_t c2 = lane; c2 < a.C; c2 += 32) {
-    const long long kmn = __ldcg(&pp[c2].kmin), kmx = __ldcg(&pp[c2].kmax);
-    const long long qmn = __ldcg(&pp[c2].imin), qmx = __ldcg(&pp[c2].imax);
-    if (kmn < cmn || (kmn == cmn && qmn < cimn)) { cmn = kmn; cimn = qmn; }
-    if (kmx > cmx || (kmx == cmx && qmx < cimx)) { cmx = kmx; cimx = qmx; }
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    const long long omn = __shfl_xor_sync(FULL, cmn, off);
-    const int64_t oimn = __shfl_xor_sync(FULL, cimn, off);
-    if (omn < cmn || (omn == cmn && oimn < cimn)) { cmn = omn; cimn = oimn; }
-    const long long omx = __shfl_xor_sync(FULL, cmx, off);
-    const int64_t oimx = __shfl_xor_sync(FULL, cimx, off);
-    if (omx > cmx || (omx == cmx && oimx < cimx)) { cmx = omx; cimx = oimx; }
-  }
-  if (lane == 0) {
-    a.ext[bkt].imin = cimn;
-    a.ext[bkt].imax = cimx;
-    a.ext[bkt].kmin = cmn;
-    a.ext[bkt].kmax = cmx;
-    a.cnt8[bkt] = (unsigned char)(cimn != cimx ? 2 : 1);
-    a.arrivals[bkt] = 0;  // leave the counter reusable
-  }
+  publish_partial(a, t, c, a.C, a.C, (long long)mn, (long long)mx, pmn, pmx, lane);
 }
 
 // ---------------------------------------------------- block scan helper --
