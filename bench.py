@@ -41,6 +41,9 @@ WORKLOADS = {
     "c3": (100_000_000, 1, 2000, 4, "f32", "i64", "minmaxlttb"),
     "c4": (1_000_000, 4096, 1000, 4, "f32", "i64", "minmaxlttb"),
     "c5": (2_000_000_000, 1, 4000, 4, "f32", "f64", "minmaxlttb"),
+    # one 2e9-point series split by MinMax bucket ranges over the ranks, one
+    # all_gather of the preselected sets; strong scaling
+    "c5s": (2_000_000_000, 1, 4000, 4, "f32", "i64", "minmaxlttb"),
 }
 METRIC = "MinMaxLTTB input points/sec and HBM GB/s (% roofline) at 1/2/4/8 B200"
 UNIT = "points/s"
@@ -117,11 +120,28 @@ def _dist():
 
 
 # ----------------------------------------------------------------- inputs ---
-def make_inputs(name, dev, seed):
+def make_shard(name, dev, seed, lo, hi):
+    """Elements [lo, hi) of a C3-recipe series, generated on this rank's device."""
+    import torch
+
+    g = torch.Generator(device=dev).manual_seed(seed)
+    y = torch.empty(hi - lo, dtype=torch.float32, device=dev)
+    chunk = 1 << 26
+    for a in range(lo, hi, chunk):
+        b = min(hi, a + chunk)
+        i = torch.arange(a, b, device=dev, dtype=torch.float64)
+        v = torch.sin(2 * np.pi * i / 1e3) + torch.sin(2 * np.pi * i / 1e5) + torch.sin(2 * np.pi * i / 1e7)
+        v += torch.randn(b - a, device=dev, dtype=torch.float64, generator=g)
+        y[a - lo:b - lo] = v
+    return torch.arange(lo, hi, dtype=torch.int64, device=dev), y
+
+
+def make_inputs(name, dev, seed, batch=None):
     """Device-side generation of the workload (torch Philox streams)."""
     import torch
 
-    n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
+    n, nb, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
+    batch = nb if batch is None else batch
     g = torch.Generator(device=dev).manual_seed(seed)
     ytype = torch.float32 if ydt == "f32" else torch.float64
     y = torch.empty((batch, n), dtype=ytype, device=dev)
@@ -278,17 +298,27 @@ def run_ours(args):
     name = args.workload
     n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
     scaling = "weak"
+    sharded = name == "c5s"
     if name == "c4" and ws > 1:  # C4: 4096 series sharded across ranks (strong)
-        per = batch // ws
-        batch = per
+        from paper_2305_00332_b200.sharding import batch_range
+
+        lo, hi = batch_range(batch, rank, ws)
+        batch = hi - lo
         scaling = "strong"
-    x, y = make_inputs(name, dev, seed=3 + rank)
-    if name == "c4" and ws > 1:
-        y = y[:batch].contiguous()
+    if sharded:
+        from paper_2305_00332_b200 import sharding
+
+        shard = sharding.bucket_ranges(n, n_out, r_ps, ws)[rank]
+        x, y = make_shard(name, dev, 3 + rank, shard.lo, shard.hi)
+        scaling = "strong"
+    else:
+        x, y = make_inputs(name, dev, seed=3 + rank, batch=batch)
     L = NAT.lib()
     torch.cuda.synchronize()
 
     def step(xx, yy):
+        if sharded:
+            return sharding.minmaxlttb_series_sharded(xx, yy, n, n_out, r_ps)
         if op == "lttb":
             return mm.lttb(xx, yy, n_out)
         return mm.minmaxlttb(xx, yy, n_out, minmax_ratio=r_ps)
@@ -297,7 +327,7 @@ def run_ours(args):
     out = step(x, y)
     torch.cuda.synchronize()
     parity = "unchecked"
-    if rank == 0 and not args.no_check:
+    if rank == 0 and not args.no_check and (not sharded or ws == 1):
         from oracle import oracle as O
 
         xh = x.cpu().numpy()
@@ -344,6 +374,8 @@ def run_ours(args):
     stage_ms = [v / max(1, calls.value) for v in st]
     # ---- end-to-end through the public API with host buffers (e2e) ----
     e2e_steps = min(args.steps, args.e2e_steps)
+    if sharded:
+        e2e_steps = 0  # shards are device-resident by construction
     if e2e_steps <= 0:  # profiling runs (ncu) skip the host path
         clocks.stop()
         e2e_ms = float("nan")
@@ -351,7 +383,7 @@ def run_ours(args):
     else:
         e2e_ms, h2d, d2h = _e2e(step, x, y, e2e_steps, n_out, r_ps, batch, op, ws, dist)
         clocks.stop()
-    pts = n * batch
+    pts = n * batch if not sharded else n / ws  # c5s: the one series is split across ranks
 
     # max over ranks of the device-timed region
     t = torch.tensor([ms, e2e_ms if e2e_steps > 0 else 0.0], dtype=torch.float64, device=dev)
@@ -363,10 +395,14 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = _peaks()
         ysz = 4 if ydt == "f32" else 8
-        if op == "lttb":
+        if sharded:  # whole sharded step: K1+K2 on the shard, all_gather, merge, LTTB
+            alg_bytes = pts * ysz
+            k_ms = ms / args.steps
+            kname = "minmaxlttb_series_sharded (whole step)"
+        elif op == "lttb":
             alg_bytes = pts * (ysz + 8)
             k_ms = sum(stage_ms) or ms / args.steps
-            kname = "k_lttb_chain (+means)"
+            kname = "K3c full LTTB (means, candidates, tables, scan, verify, repair)"
         else:
             alg_bytes = pts * ysz
             k_ms = stage_ms[0]
