@@ -173,6 +173,14 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
     return check_launch("k_extrema_flat");
   }
   const bool small = a.C == 1 && a.chunk <= SMALL_BUCKET;
+  if (small && a.B * a.nb < 16384) {  // few buckets: a whole warp per bucket fills the GPU better
+    const int64_t blocks = cdiv(a.B * a.nb, 8);
+    if (ydt == MM_F32)
+      k_extrema<float, 8, 3, 1, 32><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else
+      k_extrema<double, 8, 3, 1, 32><<<(unsigned)blocks, 256, 0, st>>>(a);
+    return check_launch("k_extrema(warp/bucket)");
+  }
   if (small) {
     const int64_t blocks = cdiv(a.B * a.nb, 8 * 4);
     if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
@@ -496,6 +504,46 @@ int* take_status(Carve& cv, cudaStream_t st) {
   return p;
 }
 
+// ---- fused K2+K3 (single / few series) -----------------------------------
+constexpr int64_t POST_SMEM_MAX = 100 * 1024;
+
+bool post_ok(int64_t k, int64_t n_out, int64_t r_ps) {
+  static const bool off = env_i64("MMLTTB_NO_POST_FUSED", 0) != 0;  // A/B knob
+  // one CTA's latency chains beat two extra launches only for small k
+  // (measured: k = 1996 24 us vs 24 us + a launch; k = 3996 41 us vs 24 us)
+  return !off && k <= 2048 && smax_for(r_ps) > 0 && smax_for(r_ps) <= 8 &&
+         post_smem(n_out - 2, smax_for(r_ps)) <= POST_SMEM_MAX;
+}
+
+template <typename XT, typename YT, int SMAX>
+int launch_post_t(const PostArgs& pa, int64_t B, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_post_fused<XT, YT, SMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)POST_SMEM_MAX) != cudaSuccess)
+      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_post_fused)");
+    attr = true;
+  }
+  k_post_fused<XT, YT, SMAX, 1024><<<(unsigned)B, 1024, (size_t)post_smem(pa.n_out - 2, SMAX), st>>>(pa);
+  return check_launch("k_post_fused");
+}
+
+template <typename XT, typename YT>
+int launch_post_y(const PostArgs& pa, int64_t B, int smax, cudaStream_t st) {
+  return smax <= 4 ? launch_post_t<XT, YT, 4>(pa, B, st) : launch_post_t<XT, YT, 8>(pa, B, st);
+}
+
+int launch_post(const PostArgs& pa, int64_t B, int xdt, int ydt, int smax, cudaStream_t st) {
+  const bool y32 = ydt == MM_F32;
+  switch (xdt) {
+    case MM_F32: return y32 ? launch_post_y<float, float>(pa, B, smax, st) : launch_post_y<float, double>(pa, B, smax, st);
+    case MM_F64: return y32 ? launch_post_y<double, float>(pa, B, smax, st) : launch_post_y<double, double>(pa, B, smax, st);
+    case MM_I64:
+      return y32 ? launch_post_y<long long, float>(pa, B, smax, st) : launch_post_y<long long, double>(pa, B, smax, st);
+    default: return y32 ? launch_post_y<int, float>(pa, B, smax, st) : launch_post_y<int, double>(pa, B, smax, st);
+  }
+}
+
 int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
   if (!y) return fail(MM_EINVAL, "y is null");
   if (!ydt_ok(ydt)) return fail(MM_EINVAL, "y dtype must be f32 or f64");
@@ -681,6 +729,17 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   stage_mark(st, 0);
   if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
   stage_mark(st, 1);
+  if (post_ok(k, n_out, r_ps)) {  // K2 + K3 in one CTA per series
+    PostArgs qa{ea.ext, k, x, x_ld, y, y_ld, N, n_out, pre, px, py, cap, out, status};
+    if ((rc = launch_post(qa, B, x_dtype, y_dtype, smax_for(r_ps), st))) return rc;
+    stage_mark(st, 2);
+    stage_mark(st, 3);
+    if (out_count) {
+      k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
+      return check_launch("k_fill");
+    }
+    return MM_OK;
+  }
   // K2: [0] + interleaved pairs + [N-1], gathered as f64 (:156-160, :207)
   PairArgs pa{};
   pa.ext = ea.ext; pa.cnt8 = ea.cnt8; pa.nb = k;

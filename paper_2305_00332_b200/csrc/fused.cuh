@@ -46,8 +46,6 @@ __global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused(FusedArgs a) {
   constexpr int G = 8, NG = NT / G;
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int sh_scan[NT / 32 + 1];
-  __shared__ M s_warp[NT / 32];
-  __shared__ M s_carry;
 
   const int64_t s = blockIdx.x;
   const int64_t N = a.N;
@@ -161,42 +159,134 @@ __global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused(FusedArgs a) {
     s_tab[it] = r;
   }
   __syncthreads();
-  // chain: block scan of the packed maps (as k_lttb_scan), one map per thread
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // chain: block scan of the packed maps (shared scan_chain)
   int64_t* out = a.out + s * a.n_out;
-  M cm = M::ident();
-  for (int64_t c0 = 0; c0 < k3; c0 += NT) {
-    const int64_t b = c0 + threadIdx.x;
-    const M t = b < k3 ? M::load(s_tab + b * SMAX) : M::ident();
-    M inc = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const M other = inc.shfl_up(o);
-      if (lane >= o) inc = M::comp(inc, other);
-    }
-    if (lane == 31) s_warp[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      M w = lane < NT / 32 ? s_warp[lane] : M::ident();
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const M other = w.shfl_up(o);
-        if (lane >= o) w = M::comp(w, other);
-      }
-      if (lane < NT / 32) s_warp[lane] = w;
-    }
-    __syncthreads();
-    M pre = cm;
-    if (wid > 0) pre = M::comp(s_warp[wid - 1], pre);
-    const M lane_prev = inc.shfl_up(1);
-    if (lane > 0) pre = M::comp(lane_prev, pre);
-    const M cur = M::comp(t, pre);
-    if (b < k3) out[b + 1] = s_pre[lb(b) + cur.at0()];
-    if (threadIdx.x == NT - 1) s_carry = cur;
-    __syncthreads();
-    cm = s_carry;
-    __syncthreads();
+  scan_chain<SMAX, NT, 1>(s_tab, k3, [&](int64_t b, int sel) { out[b + 1] = s_pre[lb(b) + sel]; });
+  if (threadIdx.x == 0) {
+    out[0] = 0;
+    out[k3 + 1] = N - 1;
   }
+}
+
+}  // namespace mm
+
+namespace mm {
+
+// ---------------------------------------------------------------------------
+// K2+K3 in one CTA per series (single / few large series): compaction of the
+// K1 bucket extrema, gather, means, transition tables and the chain scan in
+// one launch -- removes two kernel boundaries (~20 us of fixed latency) from
+// every call.  px/py are written and re-read inside the kernel, so they are
+// read with ld.global.cg (never the non-coherent path).
+struct PostArgs {
+  const Ext* ext;
+  int64_t k;                       // sub-buckets per series
+  const void* x; int64_t x_ld;
+  const void* y; int64_t y_ld;
+  int64_t N, n_out;
+  int64_t* pre; double* px; double* py; int64_t cap;  // [B][cap] preselected set
+  int64_t* out;                    // [B][n_out]
+  int* status;
+};
+
+__host__ __device__ inline int64_t post_smem(int64_t k3, int smax) {
+  return k3 * 16 + ((k3 * smax + 15) / 16) * 16;
+}
+
+template <typename XT, typename YT, int SMAX, int NT>
+__global__ void __launch_bounds__(NT) k_post_fused(PostArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int sh[NT / 32 + 1];
+  __shared__ long long s_m;
+  const int64_t s = blockIdx.x;
+  const int64_t k = a.k, N = a.N, k3 = a.n_out - 2;
+  const Ext* ext = a.ext + s * k;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  int64_t* pre = a.pre + s * a.cap;
+  double* px = a.px + s * a.cap;
+  double* py = a.py + s * a.cap;
+  double2* s_mean = reinterpret_cast<double2*>(sm);
+  unsigned char* s_tab = sm + k3 * 16;
+  const int ydt = sizeof(YT) == 4 ? 0 : 1;
+  // ---- compaction: [0] + (lo, hi)... + [N-1]  (downsamplers.py:60-69, 157-160)
+  int64_t carry = 1;
+  for (int64_t c0 = 0; c0 < k; c0 += NT) {
+    const int64_t b = c0 + threadIdx.x;
+    int n = 0;
+    int64_t lo = 0, hi = 0;
+    long long klo = 0, khi = 0;
+    if (b < k) {
+      const Ext e = ext[b];
+      if (a.status && keys_nonfinite(e.kmin, e.kmax, ydt)) atomicOr(a.status, 1);
+      const bool mfirst = e.imin <= e.imax;
+      lo = mfirst ? e.imin : e.imax;
+      hi = mfirst ? e.imax : e.imin;
+      klo = mfirst ? e.kmin : e.kmax;
+      khi = mfirst ? e.kmax : e.kmin;
+      n = hi != lo ? 2 : 1;
+    }
+    int tot;
+    const int ex = block_excl_scan<NT>(n, tot, sh);
+    if (b < k) {
+      const int64_t p = carry + ex;
+      const double xl = to_f64(xs, lo), xh = n == 2 ? to_f64(xs, hi) : 0.0;  // both gathers in flight
+      pre[p] = lo; px[p] = xl; py[p] = key_value<YT>(klo);
+      if (n == 2) { pre[p + 1] = hi; px[p + 1] = xh; py[p + 1] = key_value<YT>(khi); }
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    const double y0 = to_f64(ys, 0), yl = to_f64(ys, N - 1);
+    if (a.status && (!isfinite(y0) || !isfinite(yl))) atomicOr(a.status, 1);
+    pre[0] = 0; px[0] = to_f64(xs, 0); py[0] = y0;
+    pre[carry] = N - 1; px[carry] = to_f64(xs, N - 1); py[carry] = yl;
+    s_m = carry + 1;
+  }
+  __syncthreads();
+  const int64_t m = s_m;
+  auto lb = [&](int64_t b) -> int64_t { return 1 + (b * (m - 2)) / k3; };
+  auto X = [&](int64_t p) -> double { return __ldcg(px + p); };
+  auto Y = [&](int64_t p) -> double { return __ldcg(py + p); };
+  // ---- LTTB over the m points (_kernels.py:81-119): means, tables, chain
+  for (int64_t b = threadIdx.x; b < k3; b += NT) {
+    double2 c;
+    if (b + 1 < k3) {
+      const int64_t nlo = lb(b + 1), nhi = lb(b + 2);
+      double sx = 0.0, sy = 0.0;
+      for (int64_t j = nlo; j < nhi; ++j) {
+        sx = __dadd_rn(sx, X(j));
+        sy = __dadd_rn(sy, Y(j));
+      }
+      const double cnt = (double)(nhi - nlo);
+      c = make_double2(__ddiv_rn(sx, cnt), __ddiv_rn(sy, cnt));
+    } else {
+      c = make_double2(X(m - 1), Y(m - 1));
+    }
+    s_mean[b] = c;
+  }
+  __syncthreads();
+  for (int64_t it = threadIdx.x; it < k3 * SMAX; it += NT) {
+    const int64_t b = it / SMAX;
+    const int p = (int)(it % SMAX);
+    const int64_t blo = lb(b), bhi = lb(b + 1);
+    const bool valid = b == 0 ? p == 0 : p < blo - lb(b - 1);
+    const int64_t ap = b == 0 ? 0 : lb(b - 1) + p;
+    unsigned char r = 0;
+    if (valid) {
+      const double ax = X(ap), ay = Y(ap);
+      const double2 c = s_mean[b];
+      double best = -1.0;
+      for (int64_t j = blo; j < bhi; ++j) {
+        const double ar = lttb_area(ax, ay, c.x, c.y, X(j), Y(j));
+        if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
+      }
+    }
+    s_tab[it] = r;
+  }
+  __syncthreads();
+  int64_t* out = a.out + s * a.n_out;
+  scan_chain<SMAX, NT, 4>(s_tab, k3, [&](int64_t b, int sel) { out[b + 1] = __ldcg(pre + lb(b) + sel); });
   if (threadIdx.x == 0) {
     out[0] = 0;
     out[k3 + 1] = N - 1;

@@ -548,9 +548,23 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
   const int64_t b_lo = (int64_t)blockIdx.x * TB;
   const unsigned char* cnt = a.cnt8 + s * a.nb;
   const Ext* ext = a.ext + s * a.nb;
-  // 1. offset of this tile = items of buckets [0, b_lo)
+  // 1. offset of this tile = items of buckets [0, b_lo): the 1-byte counts
+  //    are summed as masked 32-bit words (independent loads, no byte chain)
   long long pre = 0;
-  for (int64_t i = threadIdx.x; i < b_lo; i += NT) pre += cnt[i];
+  {
+    const uintptr_t base = (uintptr_t)cnt;
+    const uintptr_t wb = base & ~(uintptr_t)3, we = (base + (uintptr_t)b_lo + 3) & ~(uintptr_t)3;
+    const int64_t nw = (int64_t)((we - wb) >> 2);
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(wb);
+    for (int64_t i = threadIdx.x; i < nw; i += NT) {
+      uint32_t w = words[i];
+      const uintptr_t a0 = wb + 4 * (uintptr_t)i;  // bytes [a0, a0+4)
+      if (a0 < base) w &= 0xFFFFFFFFu << (8 * (base - a0));
+      const uintptr_t end = base + (uintptr_t)b_lo;
+      if (a0 + 4 > end) w &= (end > a0) ? (0xFFFFFFFFu >> (8 * (a0 + 4 - end))) : 0u;
+      pre += (w & 0xFFu) + ((w >> 8) & 0xFFu) + ((w >> 16) & 0xFFu) + (w >> 24);
+    }
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(FULL, pre, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pre;
@@ -904,19 +918,14 @@ template <> struct PMap<32> : PMapN<32> {
   static __device__ __forceinline__ PMap load(const unsigned char* t) { return PMapN<32>::load(t); }
 };
 
-template <int W, int NT, int ITEMS>
-__global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
+// Resolve the LTTB chain over k3 packed transition maps (tab + b*W) with a
+// block-wide inclusive scan under map composition; emit(b, sel) receives
+// bucket b's local pick.  All NT threads must call.
+template <int W, int NT, int ITEMS, typename Emit>
+__device__ __forceinline__ void scan_chain(const unsigned char* tab, int64_t k3, Emit emit) {
   typedef PMap<W> M;
   __shared__ M s_warp[NT / 32];
   __shared__ M s_carry;
-  const int64_t s = blockIdx.x;
-  const int64_t k3 = a.n_out - 2;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const unsigned char* tab = a.tables + s * a.tab_ld;
-  int64_t* out = a.out + s * a.n_out;
-  int64_t* pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
-  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
-  const int64_t* cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   M carry = M::ident();
   for (int64_t c0 = 0; c0 < k3; c0 += (int64_t)NT * ITEMS) {
@@ -955,20 +964,30 @@ __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
     M cur = pre;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      const int64_t b = b0 + i;
       cur = M::comp(t[i], cur);
-      if (b < k3) {
-        const int sel = cur.at0();
-        const int64_t p = cand ? cand[b * W + sel] : lbound(a, m, b) + sel;
-        if (pos) pos[b + 1] = p;
-        else out[b + 1] = map ? map[p] : p;
-      }
+      if (b0 + i < k3) emit(b0 + i, cur.at0());
     }
     if (threadIdx.x == NT - 1) s_carry = cur;
     __syncthreads();
     carry = s_carry;
     __syncthreads();
   }
+}
+
+template <int W, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
+  const int64_t s = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  int64_t* out = a.out + s * a.n_out;
+  int64_t* pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  const int64_t* cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
+  scan_chain<W, NT, ITEMS>(a.tables + s * a.tab_ld, k3, [&](int64_t b, int sel) {
+    const int64_t p = cand ? cand[b * W + sel] : lbound(a, m, b) + sel;
+    if (pos) pos[b + 1] = p;
+    else out[b + 1] = map ? map[p] : p;
+  });
   if (threadIdx.x == 0) {
     if (pos) {
       pos[0] = 0;
