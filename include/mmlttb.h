@@ -151,6 +151,10 @@ int mmlttb_lttb_preselected(const int64_t *pre_idx, const double *pre_x, const d
                             const int64_t *m, int64_t B, int64_t ld, int64_t n_out, int64_t r_ps,
                             int64_t *out, void *workspace, int64_t workspace_bytes, void *stream);
 
+/* TSB1 ingest (seriesio.py:20-21,75-95): n interleaved f64 (x, y) pairs (device
+ * buffer, 16-byte aligned) -> x[n], y[n]. */
+int mmlttb_deinterleave_f64(const void *pairs, int64_t n, double *x, double *y, void *stream);
+
 /* TimeSeries invariants (core.py:80-94) on device: bit 0 set if any x or y
  * is NaN/inf, bit 1 if x decreases anywhere.  flags: one device int32,
  * zeroed by this call. */

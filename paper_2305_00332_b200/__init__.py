@@ -7,6 +7,7 @@ sharding lives in :mod:`paper_2305_00332_b200.sharding`.
 """
 from . import errors
 from .core import Algorithm, BucketPartition, DownsampleConfig, TimeSeries, partition, validate
+from .seriesio import read_series, write_series
 from .downsamplers import (
     Batch,
     downsample,
@@ -36,6 +37,8 @@ __all__ = [
     "minmax_preselect",
     "minmaxlttb",
     "partition",
+    "read_series",
     "run_parallel",
     "validate",
+    "write_series",
 ]

@@ -56,6 +56,7 @@ _SIGS = {
     "mmlttb_lttb_preselected_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "mmlttb_lttb_preselected": (_i32, [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _i64, _p]),
     "mmlttb_validate": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
+    "mmlttb_deinterleave_f64": (_i32, [_p, _i64, _p, _p, _p]),
 }
 EXPORTED = tuple(_SIGS)
 

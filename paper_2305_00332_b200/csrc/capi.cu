@@ -884,6 +884,15 @@ int mmlttb_lttb_preselected(const int64_t* pre_idx, const double* pre_x, const d
   return launch_lttb(la, MM_F64, MM_F64, r_ps, (cudaStream_t)stream);
 }
 
+int mmlttb_deinterleave_f64(const void* pairs, int64_t n, double* x, double* y, void* stream) {
+  if (!pairs || !x || !y || n < 0) return fail(MM_EINVAL, "bad arguments");
+  if (n == 0) return MM_OK;
+  if ((uintptr_t)pairs % 16) return fail(MM_EINVAL, "pairs must be 16-byte aligned");
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32);
+  k_deinterleave_f64<<<blocks, 256, 0, (cudaStream_t)stream>>>((const double2*)pairs, x, y, n);
+  return check_launch("k_deinterleave_f64");
+}
+
 int mmlttb_validate(const void* x, int x_dtype, const void* y, int y_dtype, int64_t N, int32_t* flags, void* stream) {
   if (!x || !y || !flags || N < 1 || !xdt_ok(x_dtype) || !ydt_ok(y_dtype)) return fail(MM_EINVAL, "bad arguments");
   cudaStream_t st = (cudaStream_t)stream;

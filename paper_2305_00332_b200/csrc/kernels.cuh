@@ -1582,6 +1582,17 @@ __global__ void k_validate(const XT* x, const YT* y, int64_t n, int* flags) {
   if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
 }
 
+// TSB1 ingest (seriesio.py:75-95): interleaved little-endian f64 (x, y)
+// pairs -> separate x and y arrays on the device.
+__global__ void k_deinterleave_f64(const double2* __restrict__ in, double* __restrict__ x, double* __restrict__ y,
+                                   int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldcs(in + i);
+    x[i] = v.x;
+    y[i] = v.y;
+  }
+}
+
 __global__ void k_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts,
                                int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy, int64_t* om) {
   const int64_t g = blockIdx.x;
