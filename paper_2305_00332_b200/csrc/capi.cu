@@ -544,6 +544,62 @@ int launch_post(const PostArgs& pa, int64_t B, int xdt, int ydt, int smax, cudaS
   }
 }
 
+// ---- cooperative K2+K3a ----------------------------------------------------
+template <typename XT, typename YT, int SMAX>
+int launch_coop_t(PairArgs pa, LttbArgs la, int64_t B, cudaStream_t st, bool* launched) {
+  constexpr int NT = PAIR_NT, IT = PAIR_ITEMS;
+  auto fn = k_post_coop<XT, YT, SMAX, NT, IT>;
+  static int cap = -1;
+  if (cap < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, NT, 0);
+    cap = sms * per;
+  }
+  int64_t ntiles = std::max<int64_t>(1, cdiv(pa.nb, NT * IT));
+  if (ntiles * B > cap || B > 65535) { *launched = false; return MM_OK; }
+  *launched = true;
+  la.tab_ld = tab_ld(la.n_out - 2, SMAX);
+  void* args[] = {(void*)&pa, (void*)&la, (void*)&ntiles};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)ntiles, (unsigned)B), dim3(NT),
+                                                    args, 0, st);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e != cudaSuccess) return fail(MM_ECUDA, "k_post_coop: %s", cudaGetErrorString(e));
+  return MM_OK;
+}
+
+template <typename XT, typename YT>
+int launch_coop_y(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched) {
+  return smax <= 4 ? launch_coop_t<XT, YT, 4>(pa, la, B, st, launched)
+                   : launch_coop_t<XT, YT, 8>(pa, la, B, st, launched);
+}
+
+// Try the cooperative K2+K3a; *launched = false when it does not apply.
+int launch_coop(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched) {
+  // opt-in (MMLTTB_COOP=1): measured neutral-to-slower than the separate
+  // launches on B200 (c3_1e9 28 vs 26 us, c3 1e8 27 vs 24 us) -- the fixed
+  // cost is the phases' dependent memory round trips, not the launches
+  static const bool on = env_i64("MMLTTB_COOP", 0) != 0;
+  *launched = false;
+  if (!on || smax <= 0 || smax > 8) return MM_OK;
+  const bool y32 = pa.ydt == MM_F32;
+  switch (pa.xdt) {
+    case MM_F32:
+      return y32 ? launch_coop_y<float, float>(pa, la, B, smax, st, launched)
+                 : launch_coop_y<float, double>(pa, la, B, smax, st, launched);
+    case MM_F64:
+      return y32 ? launch_coop_y<double, float>(pa, la, B, smax, st, launched)
+                 : launch_coop_y<double, double>(pa, la, B, smax, st, launched);
+    case MM_I64:
+      return y32 ? launch_coop_y<long long, float>(pa, la, B, smax, st, launched)
+                 : launch_coop_y<long long, double>(pa, la, B, smax, st, launched);
+    default:
+      return y32 ? launch_coop_y<int, float>(pa, la, B, smax, st, launched)
+                 : launch_coop_y<int, double>(pa, la, B, smax, st, launched);
+  }
+}
+
 int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
   if (!y) return fail(MM_EINVAL, "y is null");
   if (!ydt_ok(ydt)) return fail(MM_EINVAL, "y dtype must be f32 or f64");
@@ -748,6 +804,23 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   pa.x = x; pa.xdt = x_dtype; pa.x_ld = x_ld;
   pa.y = y; pa.ydt = y_dtype; pa.y_ld = y_ld;
   pa.out_x = px; pa.out_y = py; pa.status = status;
+  {  // K2 + K3a in one cooperative launch when it fits (small B, r_ps <= 8)
+    LttbArgs la{};
+    la.x = px; la.x_ld = cap; la.y = py; la.y_ld = cap;
+    la.m_dev = cnt; la.n = 0; la.bounds = nullptr; la.map = pre; la.map_ld = cap;
+    la.B = B; la.n_out = n_out; la.out = out; la.tables = lt;
+    bool launched = false;
+    if ((rc = launch_coop(pa, la, B, smax_for(r_ps), st, &launched))) return rc;
+    if (launched) {
+      stage_mark(st, 2);
+      stage_mark(st, 3);
+      if (out_count) {
+        k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
+        return check_launch("k_fill");
+      }
+      return MM_OK;
+    }
+  }
   if ((rc = launch_pairs(pa, B, st))) return rc;
   stage_mark(st, 2);
   // K3: LTTB over the compacted sub-series, mapped back (:208-209)

@@ -294,3 +294,74 @@ __global__ void __launch_bounds__(NT) k_post_fused(PostArgs a) {
 }
 
 }  // namespace mm
+
+#include <cooperative_groups.h>
+
+namespace mm {
+
+// ---------------------------------------------------------------------------
+// K2 + K3a as ONE cooperative launch (single / few series): the multi-CTA
+// compaction (compact_pairs_tile), a grid barrier, the transition tables
+// split over the same CTAs (next-bucket means recomputed per item: <= SMAX
+// points), a grid barrier, then CTA 0 of each series resolves the chain.
+// Replaces three dependent launches (and their fixed latencies) by one.
+template <typename XT, typename YT, int SMAX, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_post_coop(PairArgs pa, LttbArgs la, int64_t ntiles) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t s = blockIdx.y, tile = blockIdx.x;
+  compact_pairs_tile<XT, YT, NT, ITEMS>(pa, s, tile, ntiles);
+  grid.sync();
+  const int64_t k3 = la.n_out - 2;
+  const int64_t m = __ldcg(la.m_dev + s);
+  const double* px = (const double*)la.x + s * la.x_ld;
+  const double* py = (const double*)la.y + s * la.y_ld;
+  auto lb = [&](int64_t b) -> int64_t { return 1 + (b * (m - 2)) / k3; };
+  const int64_t items = k3 * SMAX;
+  const int64_t per = (items + ntiles - 1) / ntiles;
+  const int64_t i0 = tile * per, i1 = min(items, i0 + per);
+  unsigned char* tab = la.tables + s * la.tab_ld;
+  for (int64_t it = i0 + threadIdx.x; it < i1; it += NT) {
+    const int64_t b = it / SMAX;
+    const int p = (int)(it % SMAX);
+    const int64_t blo = lb(b), bhi = lb(b + 1);
+    const bool valid = b == 0 ? p == 0 : p < blo - lb(b - 1);
+    unsigned char r = 0;
+    if (valid) {
+      const int64_t ap = b == 0 ? 0 : lb(b - 1) + p;
+      double cx, cy;  // mean of bucket b+1, in-order sums (_kernels.py:95-104), or the last point
+      if (b + 1 < k3) {
+        const int64_t nlo = bhi, nhi = lb(b + 2);
+        double sx = 0.0, sy = 0.0;
+        for (int64_t j = nlo; j < nhi; ++j) {
+          sx = __dadd_rn(sx, __ldcg(px + j));
+          sy = __dadd_rn(sy, __ldcg(py + j));
+        }
+        const double cnt = (double)(nhi - nlo);
+        cx = __ddiv_rn(sx, cnt);
+        cy = __ddiv_rn(sy, cnt);
+      } else {
+        cx = __ldcg(px + m - 1);
+        cy = __ldcg(py + m - 1);
+      }
+      const double ax = __ldcg(px + ap), ay = __ldcg(py + ap);
+      double best = -1.0;
+      for (int64_t j = blo; j < bhi; ++j) {
+        const double ar = lttb_area(ax, ay, cx, cy, __ldcg(px + j), __ldcg(py + j));
+        if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
+      }
+    }
+    tab[it] = r;
+  }
+  grid.sync();
+  if (tile != 0) return;
+  int64_t* out = la.out + s * la.n_out;
+  const int64_t* map = la.map + s * la.map_ld;
+  scan_chain<SMAX, NT, 8>(tab, k3, [&](int64_t b, int sel) { out[b + 1] = __ldcg(map + lb(b) + sel); });
+  if (threadIdx.x == 0) {
+    out[0] = __ldcg(map);
+    out[k3 + 1] = __ldcg(map + m - 1);
+  }
+}
+
+}  // namespace mm

@@ -539,13 +539,13 @@ struct PairArgs {
   int* status;                     // bit 0: non-finite y seen (may be null)
 };
 
+// One tile (TB = NT*ITEMS buckets) of series s; `ntiles` tiles per series.
 template <typename XT, typename YT, int NT, int ITEMS>
-__global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
+__device__ __forceinline__ void compact_pairs_tile(const PairArgs& a, int64_t s, int64_t tile, int64_t ntiles) {
   __shared__ int sh[NT / 32 + 1];
   __shared__ long long s_red[NT / 32];
   constexpr int TB = NT * ITEMS;
-  const int64_t s = blockIdx.y;
-  const int64_t b_lo = (int64_t)blockIdx.x * TB;
+  const int64_t b_lo = tile * TB;
   const unsigned char* cnt = a.cnt8 + s * a.nb;
   const Ext* ext = a.ext + s * a.nb;
   // 1. offset of this tile = items of buckets [0, b_lo): the 1-byte counts
@@ -629,19 +629,25 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
         a.out_y[s * a.out_ld + pos] = to_f64(ys, v);
       }
     };
-    if (blockIdx.x == 0 && a.emit_first >= 0) {
+    if (tile == 0 && a.emit_first >= 0) {
       emit(0, a.emit_first);
       if (a.status && !isfinite(to_f64(ys, a.emit_first))) atomicOr(a.status, 1);
     }
-    if (blockIdx.x == gridDim.x - 1 && a.emit_last >= 0 && a.status && !isfinite(to_f64(ys, a.emit_last)))
+    if (tile == ntiles - 1 && a.emit_last >= 0 && a.status && !isfinite(to_f64(ys, a.emit_last)))
       atomicOr(a.status, 1);
-    if (blockIdx.x == gridDim.x - 1) {
+    if (tile == ntiles - 1) {
       int64_t end = (a.emit_first >= 0 ? 1 : 0) + off + tot;
       if (a.emit_last >= 0) emit(end++, a.emit_last);
       if (a.out_count) a.out_count[s] = end;
     }
   }
 }
+
+template <typename XT, typename YT, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
+  compact_pairs_tile<XT, YT, NT, ITEMS>(a, blockIdx.y, blockIdx.x, gridDim.x);
+}
+
 
 // -------------------------------------------------------------- LTTB -----
 // Points of series s: x/y typed (XT/YT), count m (device per series or
