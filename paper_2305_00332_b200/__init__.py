@@ -7,6 +7,7 @@ sharding lives in :mod:`paper_2305_00332_b200.sharding`.
 """
 from . import errors
 from .core import Algorithm, BucketPartition, DownsampleConfig, TimeSeries, partition, validate
+from .plan import MinMaxLTTBPlan
 from .seriesio import read_series, write_series
 from .downsamplers import (
     Batch,
@@ -25,6 +26,7 @@ __version__ = "0.1.0"
 __all__ = [
     "Algorithm",
     "Batch",
+    "MinMaxLTTBPlan",
     "BucketPartition",
     "DownsampleConfig",
     "TimeSeries",

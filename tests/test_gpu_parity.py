@@ -372,3 +372,21 @@ def test_flat_api_nonfinite_parity():
     # device inputs without validate: no sync, no raise (garbage in, indices out)
     out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), yb, 100, minmax_ratio=4)
     assert out.shape == (4, 100)
+
+
+def test_plan_graph_replay():
+    x, y = recipes.c1(200_000)
+    xd, yd = torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV)
+    plan = mm.MinMaxLTTBPlan(200_000, 500, 4, y_dtype=torch.float64, device=DEV)
+    a = plan(xd, yd).clone()
+    assert np.array_equal(a.cpu().numpy(), O.minmaxlttb(x, y, 500, 4))
+    y2 = np.cumsum(np.random.default_rng(1).standard_normal(200_000))
+    yd.copy_(torch.from_numpy(y2))  # same buffer, new contents: graph replays on the new data
+    b = plan(xd, yd).clone()
+    assert np.array_equal(b.cpu().numpy(), O.minmaxlttb(x, y2, 500, 4))
+    yd3 = torch.from_numpy(y).to(DEV)  # new buffer: new graph
+    assert np.array_equal(plan(xd, yd3).cpu().numpy(), a.cpu().numpy())
+    with pytest.raises(errors.ValidationError):
+        plan(xd, yd.float())
+    with pytest.raises(errors.NOutOfRange):
+        mm.MinMaxLTTBPlan(100, 101, 4)
