@@ -450,30 +450,35 @@ bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt) {
          fused_smem(k, n_out - 2, 8, esize(ydt)) <= FUSED_SMEM_MAX;
 }
 
-template <typename XT, typename YT, int SMAX, int NT, int MINB, int U>
+template <typename XT, typename YT, int SMAX, int NT, int MINB, int U, int LDV = 3, bool KR = true>
 int launch_fused_v(const FusedArgs& fa, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)FUSED_SMEM_MAX) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U, LDV, KR>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_MAX) != cudaSuccess)
       return fail(MM_ECUDA, "cudaFuncSetAttribute(k_mmlttb_fused)");
     attr = true;
   }
   const int64_t k = (fa.n_out - 2) * (fa.r_ps / 2);
   const size_t smem = (size_t)fused_smem(k, fa.n_out - 2, SMAX, (int)sizeof(YT));
-  k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U><<<(unsigned)fa.B, NT, smem, st>>>(fa);
+  k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U, LDV, KR><<<(unsigned)fa.B, NT, smem, st>>>(fa);
   return check_launch("k_mmlttb_fused");
 }
 
 template <typename XT, typename YT, int SMAX>
 int launch_fused_t(const FusedArgs& fa, cudaStream_t st) {
   static const int64_t v = env_i64("MMLTTB_FUSED_VARIANT", 0);  // tuning knob (tools/)
-  switch (v) {  // tools/fused_sweep.sh on B200: (512 thr, 2 CTA/SM, U=8) is best on C4
+  switch (v) {  // tools/fused_sweep.sh on B200 (variant 0 = default)
     case 1: return launch_fused_v<XT, YT, SMAX, 512, 2, 4>(fa, st);
     case 2: return launch_fused_v<XT, YT, SMAX, 384, 3, 4>(fa, st);
     case 3: return launch_fused_v<XT, YT, SMAX, 256, 4, 4>(fa, st);
     case 4: return launch_fused_v<XT, YT, SMAX, 512, 3, 2>(fa, st);
-    default: return launch_fused_v<XT, YT, SMAX, 512, 2, 8>(fa, st);
+    case 5: return launch_fused_v<XT, YT, SMAX, 512, 2, 8>(fa, st);
+    case 6: return launch_fused_v<XT, YT, SMAX, 512, 3, 4, 2, false>(fa, st);
+    case 7: return launch_fused_v<XT, YT, SMAX, 512, 2, 8, 2, true>(fa, st);
+    case 8: return launch_fused_v<XT, YT, SMAX, 384, 3, 8, 2, false>(fa, st);
+    // measured best on C4: normal-policy loads, winners re-read from L1/L2
+    default: return launch_fused_v<XT, YT, SMAX, 512, 2, 8, 2, false>(fa, st);
   }
 }
 

@@ -38,7 +38,7 @@ __host__ __device__ inline int64_t fused_smem(int64_t k, int64_t k3, int smax, i
   return fused_region1(k, k3, smax, ysize) + ((m * ysize + 15) / 16) * 16 + ((m * 4 + 15) / 16) * 16;
 }
 
-template <typename XT, typename YT, int SMAX, int NT, int MINB, int U>
+template <typename XT, typename YT, int SMAX, int NT, int MINB, int U, int LDV = 3, bool KEEPRAW = true>
 __global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused(FusedArgs a) {
   typedef YTr<YT> Tr;
   typedef typename Tr::K K;
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused(FusedArgs a) {
     }
     K mn, mx;
     int omn, omx;
-    group_extrema<YT, U, 3, G>(ys, lo, hi, lane8, mn, omn, mx, omx);
+    group_extrema<YT, U, LDV, G, KEEPRAW>(ys, lo, hi, lane8, mn, omn, mx, omx);
     if (lane8 == 0 && b < k) {
       if (a.status && keys_nonfinite((long long)mn, (long long)mx, sizeof(YT) == 4 ? 0 : 1)) atomicOr(a.status, 1);
       const bool mfirst = omn <= omx;

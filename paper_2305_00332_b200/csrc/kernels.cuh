@@ -149,7 +149,7 @@ __device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k,
 // vector improves the running extreme its raw 16 bytes are kept in
 // registers, so the exact element is recovered without re-reading memory (a
 // re-read would miss L2 on a long stream and cost extra DRAM traffic).
-template <typename T, int U, int LDV, int G>
+template <typename T, int U, int LDV, int G, bool KEEPRAW = true>
 __device__ __forceinline__ void group_extrema(const T* y, int64_t lo, int64_t hi, int lane, typename YTr<T>::K& mn,
                                               int& omn, typename YTr<T>::K& mx, int& omx) {
   typedef YTr<T> Tr;
@@ -188,10 +188,14 @@ __device__ __forceinline__ void group_extrema(const T* y, int64_t lo, int64_t hi
           K vl = kk[0], vh = kk[0];
 #pragma unroll
           for (int e = 1; e < Tr::VEC; ++e) { vl = min(vl, kk[e]); vh = max(vh, kk[e]); }
-          if (vl < mn) { mn = vl; omn = head + v * Tr::VEC; vmn = true; rmn = r[u]; }
-          if (vh > mx) { mx = vh; omx = head + v * Tr::VEC; vmx = true; rmx = r[u]; }
+          if (vl < mn) { mn = vl; omn = head + v * Tr::VEC; vmn = true; if (KEEPRAW) rmn = r[u]; }
+          if (vh > mx) { mx = vh; omx = head + v * Tr::VEC; vmx = true; if (KEEPRAW) rmx = r[u]; }
         }
       }
+    }
+    if (!KEEPRAW) {  // short ranges read with normal L2 policy: the vectors are still cached
+      if (vmn) rmn = __ldg(reinterpret_cast<const uint4*>(base + omn));
+      if (vmx) rmx = __ldg(reinterpret_cast<const uint4*>(base + omx));
     }
     const int tp = head + nvec * Tr::VEC + lane;
     if (tp < n) {
