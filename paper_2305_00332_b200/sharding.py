@@ -43,9 +43,9 @@ def minmaxlttb_batch_sharded(x, y_local, n_out: int, r_ps: int = 4, *, B: int | 
     ``gather=True`` the [B, n_out] result is all-gathered to every rank.
     """
     out = _minmaxlttb_batch(_prepared(x, y_local), n_out, r_ps)
-    if not gather:
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if not gather or world == 1:
         return out
-    world = dist.get_world_size(group)
     B = B if B is not None else out.shape[0] * world
     per = -(-B // world)
     buf = torch.full((per, n_out), -1, dtype=torch.int64, device=out.device)
