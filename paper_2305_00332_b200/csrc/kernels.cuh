@@ -673,6 +673,7 @@ struct LttbArgs {
   int64_t* pos; int64_t pos_ld;           // [B][k3+2] chosen positions (pre-map)
   int64_t* best;                          // [B][k3] exact argmax given pos[b] (verify)
   int* flag;                              // [B][k3] best != pos[b+1]
+  int64_t* best2;                         // [B][k3] exact pick of b given anchor best[b-1] (if flag[b-1])
   int cand_cap;                           // <= HMAX (tests lower it to force repairs)
   double2* yrange;                        // [B][k3] per-bucket (ymin, ymax) (K3c candidates)
 };
@@ -1511,6 +1512,27 @@ __global__ void __launch_bounds__(NT) k_lttb_verify(LttbArgs a) {
   }
 }
 
+// Speculative second step: for every bucket right after a mismatch, the
+// exact pick given the EXACT previous pick (best[b-1]) -- in parallel, so an
+// isolated mismatch is repaired without any sequential re-scan.
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_verify2(LttbArgs a) {
+  __shared__ double s_a[NT / 32];
+  __shared__ long long s_i[NT / 32];
+  const int64_t s = blockIdx.y;
+  const int64_t b = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  if (b == 0 || !a.flag[s * k3 + b - 1]) return;  // block-uniform
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t prev = a.best[s * k3 + b - 1];
+  const double2 c = a.means[s * a.means_ld + b];
+  const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
+                                                    to_f64(ys, prev), c, s_a, s_i);
+  if (threadIdx.x == 0) a.best2[s * k3 + b] = r;
+}
+
 __device__ unsigned long long g_repair_scans;  // exact bucket scans done by k_lttb_repair (stats)
 
 template <typename XT, typename YT, int NT>
@@ -1539,24 +1561,24 @@ __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
       __syncthreads();
       if (nb == LLONG_MAX) break;
       b = nb;
-      if (threadIdx.x == 0) {
-        pos[b + 1] = best[b];  // exact: prev pos[b] is on the true chain
-        atomicAdd(&g_repair_scans, 1ull);
-      }
+      if (threadIdx.x == 0) pos[b + 1] = best[b];  // exact: prev pos[b] is on the true chain
       synced = false;
       ++b;
       __syncthreads();
       continue;
     }
     const int64_t prev = pos[b];
-    const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
-                                                      to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+    int64_t r;
+    if (b >= 1 && flag[b - 1] && prev == best[b - 1]) {
+      r = a.best2[s * k3 + b];  // precomputed by k_lttb_verify2
+    } else {
+      r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
+                                          to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+      if (threadIdx.x == 0) atomicAdd(&g_repair_scans, 1ull);
+    }
     const int64_t was = pos[b + 1];
     __syncthreads();
-    if (threadIdx.x == 0) {
-      pos[b + 1] = r;
-      atomicAdd(&g_repair_scans, 1ull);
-    }
+    if (threadIdx.x == 0) pos[b + 1] = r;
     synced = r == was;  // re-joined the candidate chain: later buckets were verified with this prev
     ++b;
     __syncthreads();
