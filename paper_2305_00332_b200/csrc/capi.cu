@@ -275,7 +275,7 @@ int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s) {
   if (use_chain()) return up(B * k3 * (int64_t)sizeof(double2));
   return up(B * k3 * (int64_t)sizeof(double2)) + up(B * k3 * HMAX * 8) + up(B * k3 * 4) + up(B * tab_ld(k3, HMAX)) +
          up(B * (k3 + 2) * 8) + up(B * k3 * 8) + up(B * k3 * 4) + up(B * k3 * (int64_t)sizeof(double2)) +
-         up(B * k3 * 8);
+         up(B * k3 * 8) + up(B * k3 * 4) + up(B * 4);
 }
 
 template <int SMAX> int jump_attr() {
@@ -334,6 +334,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   a.flag = cv.take<int>(a.B * k3);
   a.yrange = cv.take<double2>(a.B * k3);
   a.best2 = cv.take<int64_t>(a.B * k3);
+  a.flist = cv.take<int>(a.B * k3);
+  a.fcount = cv.take<int>(a.B);
   a.tables = tabs;
   a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", H);  // test knob: a poor heuristic must still be exact
   // one warp per bucket, 8 KB of tiles each: every bucket's chain resident at once
@@ -351,9 +353,10 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   if ((rc = check_launch("k_lttb_ctables"))) return rc;
   k_lttb_scan<H, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_scan"))) return rc;
+  if (cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
   k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_verify"))) return rc;
-  k_lttb_verify2<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
+  k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_verify2"))) return rc;
   k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
   return check_launch("k_lttb_repair");

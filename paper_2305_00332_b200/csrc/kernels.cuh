@@ -674,6 +674,7 @@ struct LttbArgs {
   int64_t* best;                          // [B][k3] exact argmax given pos[b] (verify)
   int* flag;                              // [B][k3] best != pos[b+1]
   int64_t* best2;                         // [B][k3] exact pick of b given anchor best[b-1] (if flag[b-1])
+  int* flist; int* fcount;                // [B][k3] flagged buckets (unordered), [B] their count (zeroed)
   int cand_cap;                           // <= HMAX (tests lower it to force repairs)
   double2* yrange;                        // [B][k3] per-bucket (ymin, ymax) (K3c candidates)
 };
@@ -1508,7 +1509,9 @@ __global__ void __launch_bounds__(NT) k_lttb_verify(LttbArgs a) {
                                                     to_f64(ys, prev), c, s_a, s_i);
   if (threadIdx.x == 0) {
     a.best[s * k3 + b] = r;
-    a.flag[s * k3 + b] = r != pos[b + 1];
+    const bool f = r != pos[b + 1];
+    a.flag[s * k3 + b] = f;
+    if (f) a.flist[s * k3 + atomicAdd(&a.fcount[s], 1)] = (int)b;
   }
 }
 
@@ -1520,25 +1523,29 @@ __global__ void __launch_bounds__(NT) k_lttb_verify2(LttbArgs a) {
   __shared__ double s_a[NT / 32];
   __shared__ long long s_i[NT / 32];
   const int64_t s = blockIdx.y;
-  const int64_t b = blockIdx.x;
   const int64_t k3 = a.n_out - 2;
-  if (b == 0 || !a.flag[s * k3 + b - 1]) return;  // block-uniform
+  const int nf = a.fcount[s];
   const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
   const XT* xs = (const XT*)a.x + s * a.x_ld;
   const YT* ys = (const YT*)a.y + s * a.y_ld;
-  const int64_t prev = a.best[s * k3 + b - 1];
-  const double2 c = a.means[s * a.means_ld + b];
-  const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
-                                                    to_f64(ys, prev), c, s_a, s_i);
-  if (threadIdx.x == 0) a.best2[s * k3 + b] = r;
+  for (int q = blockIdx.x; q < nf; q += gridDim.x) {  // one flagged bucket f per CTA: bucket f+1
+    const int64_t b = (int64_t)a.flist[s * k3 + q] + 1;
+    if (b >= k3) continue;
+    const int64_t prev = a.best[s * k3 + b - 1];
+    const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
+                                                      to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+    if (threadIdx.x == 0) a.best2[s * k3 + b] = r;
+  }
 }
 
 __device__ unsigned long long g_repair_scans;  // exact bucket scans done by k_lttb_repair (stats)
 
 template <typename XT, typename YT, int NT>
 __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
+  constexpr int LMAX = 2048;  // flagged buckets sorted in shared memory (more: linear search)
   __shared__ double s_a[NT / 32];
   __shared__ long long s_i[NT / 32];
+  __shared__ int s_f[LMAX];
   __shared__ long long s_next;
   const int64_t s = blockIdx.x;
   const int64_t k3 = a.n_out - 2;
@@ -1548,41 +1555,61 @@ __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
   int64_t* pos = a.pos + s * a.pos_ld;
   const int* flag = a.flag + s * k3;
   const int64_t* best = a.best + s * k3;
+  const int nf = a.fcount[s];
+  const bool listed = nf <= LMAX;
+  if (listed) {
+    for (int i = threadIdx.x; i < nf; i += NT) s_f[i] = a.flist[s * k3 + i];
+    __syncthreads();
+    // odd-even transposition sort of the (few) flagged buckets
+    for (int ph = 0; ph < nf; ++ph) {
+      for (int i = 2 * threadIdx.x + (ph & 1); i + 1 < nf; i += 2 * NT)
+        if (s_f[i] > s_f[i + 1]) { const int t = s_f[i]; s_f[i] = s_f[i + 1]; s_f[i + 1] = t; }
+      __syncthreads();
+    }
+  }
   int64_t b = 0;
-  bool synced = true;
+  int qi = 0;
   while (b < k3) {
-    if (synced) {  // next verified mismatch at or after b
+    // next verified mismatch at or after b (the chain is synced up to b)
+    int64_t nb;
+    if (listed) {
+      while (qi < nf && s_f[qi] < b) ++qi;
+      nb = qi < nf ? s_f[qi] : LLONG_MAX;
+    } else {
       if (threadIdx.x == 0) s_next = LLONG_MAX;
       __syncthreads();
       for (int64_t i = b + threadIdx.x; i < k3; i += NT)
         if (flag[i]) atomicMin(&s_next, (long long)i);
       __syncthreads();
-      const long long nb = s_next;
+      nb = s_next;
       __syncthreads();
-      if (nb == LLONG_MAX) break;
-      b = nb;
-      if (threadIdx.x == 0) pos[b + 1] = best[b];  // exact: prev pos[b] is on the true chain
-      synced = false;
-      ++b;
-      __syncthreads();
-      continue;
     }
-    const int64_t prev = pos[b];
-    int64_t r;
-    if (b >= 1 && flag[b - 1] && prev == best[b - 1]) {
-      r = a.best2[s * k3 + b];  // precomputed by k_lttb_verify2
-    } else {
-      r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
-                                          to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
-      if (threadIdx.x == 0) atomicAdd(&g_repair_scans, 1ull);
-    }
-    const int64_t was = pos[b + 1];
+    if (nb >= k3) break;
+    b = nb;
     __syncthreads();
-    if (threadIdx.x == 0) pos[b + 1] = r;
-    synced = r == was;  // re-joined the candidate chain: later buckets were verified with this prev
+    if (threadIdx.x == 0) pos[b + 1] = best[b];  // exact: prev pos[b] is on the true chain
+    __syncthreads();
     ++b;
-    __syncthreads();
+    // walk exactly until the chain re-joins the (verified) candidate chain
+    while (b < k3) {
+      const int64_t prev = pos[b];
+      int64_t r;
+      if (flag[b - 1] && prev == best[b - 1]) {
+        r = a.best2[s * k3 + b];  // precomputed by k_lttb_verify2
+      } else {
+        r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
+                                            to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+        if (threadIdx.x == 0) atomicAdd(&g_repair_scans, 1ull);
+      }
+      const int64_t was = pos[b + 1];
+      __syncthreads();
+      if (threadIdx.x == 0) pos[b + 1] = r;
+      __syncthreads();
+      ++b;
+      if (r == was) break;  // synced: later buckets were verified with this prev
+    }
   }
+  __syncthreads();
   int64_t* out = a.out + s * a.n_out;
   const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
   for (int64_t i = threadIdx.x; i < k3 + 2; i += NT) {
