@@ -155,6 +155,22 @@ int mmlttb_lttb_preselected(const int64_t *pre_idx, const double *pre_x, const d
  * buffer, 16-byte aligned) -> x[n], y[n]. */
 int mmlttb_deinterleave_f64(const void *pairs, int64_t n, double *x, double *y, void *stream);
 
+/* ---- evaluation step after the path ----------------
+ * rasterize (raster.py:87-118, _kernels.py:122-163): draws points idx[0..n)
+ * (or 0..n when idx is null) of (x, y) as the reference's anti-aliased width-2
+ * polyline onto a w x h uint8 canvas mapping [x0,x1] x [y0,y1]; bit-identical
+ * pixels.  conv_mask (metrics.py:69-82): dilated union of both images' ink.
+ * pixel_metrics (metrics.py:85-132): out4 = {pem(margin), dssim, mse, mask
+ * size}; pem and the SSIM map are exact, the dssim/mse means are summed in a
+ * fixed order (not numpy's pairwise order). */
+int64_t mmlttb_raster_workspace_bytes(int64_t n, int64_t w, int64_t h);
+int mmlttb_rasterize(const void *x, int x_dtype, const void *y, int y_dtype, const int64_t *idx, int64_t n,
+                     double x0, double x1, double y0, double y1, int64_t w, int64_t h, uint8_t *pixels,
+                     void *workspace, int64_t workspace_bytes, void *stream);
+int mmlttb_conv_mask(const uint8_t *a, const uint8_t *b, int64_t h, int64_t w, int kernel, uint8_t *mask, void *stream);
+int mmlttb_pixel_metrics(const uint8_t *a, const uint8_t *b, const uint8_t *mask, int64_t h, int64_t w, int margin,
+                         double *out4, void *workspace, int64_t workspace_bytes, void *stream);
+
 /* TimeSeries invariants (core.py:80-94) on device: bit 0 set if any x or y
  * is NaN/inf, bit 1 if x decreases anywhere.  flags: one device int32,
  * zeroed by this call. */

@@ -7,7 +7,10 @@ sharding lives in :mod:`paper_2305_00332_b200.sharding`.
 """
 from . import errors
 from .core import Algorithm, BucketPartition, DownsampleConfig, TimeSeries, partition, validate
+from . import metrics, raster
+from .metrics import ConvMask, conv_mask, dssim, mse, pem
 from .plan import MinMaxLTTBPlan
+from .raster import Canvas, RasterImage, fit_canvas, rasterize, read_pgm, write_pgm
 from .seriesio import read_series, write_series
 from .downsamplers import (
     Batch,
@@ -26,6 +29,17 @@ __version__ = "0.1.0"
 __all__ = [
     "Algorithm",
     "Batch",
+    "Canvas",
+    "ConvMask",
+    "RasterImage",
+    "conv_mask",
+    "dssim",
+    "fit_canvas",
+    "mse",
+    "pem",
+    "rasterize",
+    "read_pgm",
+    "write_pgm",
     "MinMaxLTTBPlan",
     "BucketPartition",
     "DownsampleConfig",

@@ -57,6 +57,11 @@ _SIGS = {
     "mmlttb_lttb_preselected": (_i32, [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _i64, _p]),
     "mmlttb_validate": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
     "mmlttb_deinterleave_f64": (_i32, [_p, _i64, _p, _p, _p]),
+    "mmlttb_raster_workspace_bytes": (_i64, [_i64, _i64, _i64]),
+    "mmlttb_rasterize": (_i32, [_p, _i32, _p, _i32, _p, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                ctypes.c_double, _i64, _i64, _p, _p, _i64, _p]),
+    "mmlttb_conv_mask": (_i32, [_p, _p, _i64, _i64, _i32, _p, _p]),
+    "mmlttb_pixel_metrics": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p, _p, _i64, _p]),
 }
 EXPORTED = tuple(_SIGS)
 

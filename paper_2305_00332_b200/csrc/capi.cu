@@ -20,6 +20,7 @@
 #include "../../include/mmlttb.h"
 #include "kernels.cuh"
 #include "fused.cuh"
+#include "raster.cuh"
 
 using namespace mm;
 
@@ -976,6 +977,56 @@ int mmlttb_deinterleave_f64(const void* pairs, int64_t n, double* x, double* y, 
   const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32);
   k_deinterleave_f64<<<blocks, 256, 0, (cudaStream_t)stream>>>((const double2*)pairs, x, y, n);
   return check_launch("k_deinterleave_f64");
+}
+
+int64_t mmlttb_raster_workspace_bytes(int64_t n, int64_t w, int64_t h) {
+  return up(n * 8) * 2 + up(std::max<int64_t>(n - 1, 1) * 16) + up(5 * w * h * 8) + up(cdiv(w * h, 256) * 16) + ALIGN;
+}
+
+int mmlttb_rasterize(const void* x, int x_dtype, const void* y, int y_dtype, const int64_t* idx, int64_t n, double x0,
+                     double x1, double y0, double y1, int64_t w, int64_t h, uint8_t* pixels, void* workspace,
+                     int64_t workspace_bytes, void* stream) {
+  if (!x || !y || !pixels || n < 2 || w < 1 || h < 1 || !xdt_ok(x_dtype) || !xdt_ok(y_dtype) ||
+      w * h > (int64_t)INT32_MAX)
+    return fail(MM_EINVAL, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  Carve cv{(char*)workspace, workspace_bytes};
+  RasterCoordArgs a{x, x_dtype, y, y_dtype, idx, n, x0, x1, y0, y1, w, h, nullptr, nullptr, nullptr};
+  a.us = cv.take<double>(n);
+  a.vs = cv.take<double>(n);
+  a.box = cv.take<int>(4 * (n - 1));
+  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
+  k_raster_coords<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(a);
+  int rc = check_launch("k_raster_coords");
+  if (rc) return rc;
+  k_raster_boxes<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(a);
+  if ((rc = check_launch("k_raster_boxes"))) return rc;
+  k_rasterize<<<(unsigned)cdiv(w * h, 256), 256, 0, st>>>(a.us, a.vs, a.box, n, w, h, pixels);
+  return check_launch("k_rasterize");
+}
+
+int mmlttb_conv_mask(const uint8_t* a, const uint8_t* b, int64_t h, int64_t w, int kernel, uint8_t* mask, void* stream) {
+  if (!a || !b || !mask || kernel < 1 || kernel % 2 == 0 || w * h < 1) return fail(MM_EINVAL, "bad arguments");
+  k_conv_mask<<<(unsigned)cdiv(w * h, 256), 256, 0, (cudaStream_t)stream>>>(a, b, h, w, kernel, mask);
+  return check_launch("k_conv_mask");
+}
+
+int mmlttb_pixel_metrics(const uint8_t* a, const uint8_t* b, const uint8_t* mask, int64_t h, int64_t w, int margin,
+                         double* out4, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!a || !b || !mask || !out4 || h < 8 || w < 8 || margin < 0 || margin > 255) return fail(MM_EINVAL, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  Carve cv{(char*)workspace, workspace_bytes};
+  double* m5 = cv.take<double>(5 * w * h);
+  const int64_t nb = cdiv(w * h, 256);
+  double* part = cv.take<double>(2 * nb);
+  if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small");
+  k_ssim_rows<<<(unsigned)nb, 256, 0, st>>>(a, b, h, w, m5);
+  int rc = check_launch("k_ssim_rows");
+  if (rc) return rc;
+  k_ssim_cols<<<(unsigned)nb, 256, 0, st>>>(a, b, mask, h, w, m5, part);
+  if ((rc = check_launch("k_ssim_cols"))) return rc;
+  k_metrics_final<<<1, 256, 0, st>>>(a, b, mask, w * h, margin, part, nb, out4);
+  return check_launch("k_metrics_final");
 }
 
 int mmlttb_validate(const void* x, int x_dtype, const void* y, int y_dtype, int64_t N, int32_t* flags, void* stream) {
