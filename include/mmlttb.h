@@ -142,6 +142,21 @@ int mmlttb_merge_shards(const int64_t *idx, const double *xs, const double *ys, 
                         int64_t G, int64_t cap, int64_t *out_idx, double *out_x, double *out_y,
                         int64_t *out_m, void *stream);
 
+/* Device-initiated exchange over peer memory (NVLink stores + epoch flags)
+ * in place of the NCCL all_gather: each rank's symmetric buffer is int64
+ * [2][G][3*cap+1] (slot = epoch & 1, row = writer rank) with a uint32 signal
+ * pad [2G] (data flags, then acks); peer_bufs / peer_pads are device arrays
+ * of the G peers' addresses (e.g. torch symmetric memory buffer_ptrs_dev /
+ * signal_pad_ptrs_dev).  publish: wait for peer g's ack of epoch-2, store the
+ * set into peer g's row, release its flag.  merge: acquire all G flags of
+ * this epoch, concatenate the rows in rank order, ack the writers. */
+int mmlttb_p2p_publish(const int64_t *idx, const double *xs, const double *ys, const int64_t *count, int64_t cap,
+                       const uint64_t *peer_bufs, const uint64_t *peer_pads, const uint32_t *own_pad, int64_t G,
+                       int64_t rank, uint32_t epoch, void *stream);
+int mmlttb_p2p_merge(const int64_t *own_buf, const uint32_t *own_pad, const uint64_t *peer_pads, int64_t G,
+                     int64_t rank, int64_t cap, uint32_t epoch, int64_t *out_idx, double *out_x, double *out_y,
+                     int64_t *out_m, void *stream);
+
 /* LTTB over preselected sets: series s has m[s] points (device counts)
  * pre_x/pre_y (f64, row stride ld) and maps position p -> pre_idx[p].
  * out[s*n_out + i] = pre_idx[lttb position].  r_ps bounds the bucket size

@@ -954,6 +954,30 @@ int mmlttb_merge_shards(const int64_t* idx, const double* xs, const double* ys, 
   return check_launch("k_merge_shards");
 }
 
+int mmlttb_p2p_publish(const int64_t* idx, const double* xs, const double* ys, const int64_t* count, int64_t cap,
+                       const uint64_t* peer_bufs, const uint64_t* peer_pads, const uint32_t* own_pad, int64_t G,
+                       int64_t rank, uint32_t epoch, void* stream) {
+  if (!idx || !xs || !ys || !count || !peer_bufs || !peer_pads || !own_pad || G < 1 || rank < 0 || rank >= G ||
+      cap < 1 || epoch == 0)
+    return fail(MM_EINVAL, "bad arguments");
+  k_p2p_publish<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>(idx, xs, ys, count, cap,
+                                                              (const unsigned long long*)peer_bufs,
+                                                              (const unsigned long long*)peer_pads, own_pad, G, rank,
+                                                              epoch);
+  return check_launch("k_p2p_publish");
+}
+
+int mmlttb_p2p_merge(const int64_t* own_buf, const uint32_t* own_pad, const uint64_t* peer_pads, int64_t G,
+                     int64_t rank, int64_t cap, uint32_t epoch, int64_t* out_idx, double* out_x, double* out_y,
+                     int64_t* out_m, void* stream) {
+  if (!own_buf || !own_pad || !peer_pads || !out_idx || !out_x || !out_y || !out_m || G < 1 || cap < 1 || epoch == 0)
+    return fail(MM_EINVAL, "bad arguments");
+  k_p2p_merge<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>((const long long*)own_buf, own_pad,
+                                                            (const unsigned long long*)peer_pads, G, rank, cap, epoch,
+                                                            out_idx, out_x, out_y, out_m);
+  return check_launch("k_p2p_merge");
+}
+
 int64_t mmlttb_lttb_preselected_workspace_bytes(int64_t B, int64_t n_out, int64_t r_ps) {
   return lttb_ws(B, n_out, r_ps);
 }

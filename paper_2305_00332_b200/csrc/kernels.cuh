@@ -1652,6 +1652,76 @@ __global__ void k_deinterleave_f64(const double2* __restrict__ in, double* __res
   }
 }
 
+// ---- device-initiated exchange over peer memory (replaces the NCCL
+// all_gather of the sharded single-series path).  Symmetric
+// buffer per rank: int64 [2][G][W] (slot = epoch & 1, row = writer rank,
+// W = 3*cap + 1: idx | x bits | y bits | count).  Signal pad (uint32) per
+// rank: [g] = last epoch whose row from rank g is complete, [G + g] = last
+// epoch rank g has consumed from this rank's rows (ack).
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void spin_until_ge(const unsigned* p, unsigned want) {
+  while ((int)(ld_acquire_sys(p) - want) < 0) __nanosleep(64);
+}
+
+// CTA g: store this rank's preselected set into peer g's buffer, then raise
+// the peer's data flag.  Waits first for peer g's ack of epoch-2 (same slot).
+__global__ void k_p2p_publish(const int64_t* idx, const double* xs, const double* ys, const int64_t* count, int64_t cap,
+                              const unsigned long long* peer_bufs, const unsigned long long* peer_pads,
+                              const unsigned* own_pad, int64_t G, int64_t rank, unsigned epoch) {
+  const int64_t g = blockIdx.x;
+  const int64_t W = 3 * cap + 1;
+  if (threadIdx.x == 0 && epoch > 2) spin_until_ge(own_pad + G + g, epoch - 2);
+  __syncthreads();
+  long long* dst = reinterpret_cast<long long*>(peer_bufs[g]) + ((int64_t)(epoch & 1) * G + rank) * W;
+  const int64_t n = min(*count, cap);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    dst[i] = idx[i];
+    dst[cap + i] = __double_as_longlong(xs[i]);
+    dst[2 * cap + i] = __double_as_longlong(ys[i]);
+  }
+  if (threadIdx.x == 0) dst[3 * cap] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(reinterpret_cast<unsigned*>(peer_pads[g]) + rank, epoch);
+  }
+}
+
+// CTA g: wait for every row of this epoch, append row g at its offset (rank
+// order), then ack rank g.
+__global__ void k_p2p_merge(const long long* own_buf, const unsigned* own_pad, const unsigned long long* peer_pads,
+                            int64_t G, int64_t rank, int64_t cap, unsigned epoch, int64_t* oi, double* ox, double* oy,
+                            int64_t* om) {
+  const int64_t g = blockIdx.x;
+  const int64_t W = 3 * cap + 1;
+  if (threadIdx.x == 0)
+    for (int64_t h = 0; h < G; ++h) spin_until_ge(own_pad + h, epoch);
+  __syncthreads();
+  const long long* rows = own_buf + (int64_t)(epoch & 1) * G * W;
+  int64_t off = 0;
+  for (int64_t h = 0; h < g; ++h) off += rows[h * W + 3 * cap];
+  const long long* row = rows + g * W;
+  const int64_t n = row[3 * cap];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    oi[off + i] = row[i];
+    ox[off + i] = __longlong_as_double(row[cap + i]);
+    oy[off + i] = __longlong_as_double(row[2 * cap + i]);
+  }
+  if (g == G - 1 && threadIdx.x == 0) om[0] = off + n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(reinterpret_cast<unsigned*>(peer_pads[g]) + G + rank, epoch);
+  }
+}
+
 __global__ void k_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts,
                                int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy, int64_t* om) {
   const int64_t g = blockIdx.x;

@@ -136,6 +136,74 @@ def exchange(buf: torch.Tensor, world: int, group=None) -> torch.Tensor:
     return allbuf
 
 
+class PeerExchange:
+    """Device-initiated replacement for :func:`exchange` + :func:`unpack` +
+    ``mmlttb_merge_shards``: every rank stores its preselected set straight
+    into each peer's symmetric buffer over NVLink (``mmlttb_p2p_publish``)
+    and the peers concatenate the rows in rank order as soon as their epoch
+    flags arrive (``mmlttb_p2p_merge``) -- no NCCL launch, no host sync, and
+    the merged set lands directly in the LTTB stage's input.  Double-buffered
+    by epoch parity with per-peer acks, so back-to-back calls never overwrite
+    a row a peer has not consumed.  Opt-in (``exchange="p2p"``); built on
+    ``torch.distributed._symmetric_memory`` for allocation + rendezvous only.
+    """
+
+    def __init__(self, cap: int, device, group=None):
+        from torch.distributed import _symmetric_memory as symm
+        self.cap, self.device = cap, torch.device(device)
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        W = 3 * cap + 1
+        self.buf = symm.empty(2 * self.world * W, dtype=torch.int64, device=self.device)
+        self.handle = symm.rendezvous(self.buf, dist.group.WORLD if group is None else group)
+        # the flags live at the END of the signal pad, clear of the channel
+        # slots torch's own barrier()/put_signal use at its start
+        words = self.handle.signal_pad_size // 4
+        if words < 2 * self.world + 64 * self.world:
+            raise RuntimeError("symmetric-memory signal pad too small for the exchange flags")
+        off = words - 2 * self.world
+        pads = [self.handle.get_signal_pad(r, (2 * self.world,), dtype=torch.int32, storage_offset=off)
+                for r in range(self.world)]
+        bufs = [self.handle.get_remote_tensor(r, (2 * self.world * W,), torch.int64) for r in range(self.world)]
+        self.own_pad = pads[self.rank]
+        self.own_pad.zero_()
+        self.peer_bufs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=self.device)
+        self.peer_pads = torch.tensor([p.data_ptr() for p in pads], dtype=torch.int64, device=self.device)
+        self.epoch = 0
+        self.handle.barrier()
+
+    def __call__(self, idx, xs, ys, cnt):
+        """Publish this rank's set, return the merged (idx, x, y, m) of all ranks."""
+        self.epoch += 1
+        G, cap = self.world, self.cap
+        tot = G * cap
+        oi = torch.empty(tot, dtype=torch.int64, device=self.device)
+        ox = torch.empty(tot, dtype=torch.float64, device=self.device)
+        oy = torch.empty(tot, dtype=torch.float64, device=self.device)
+        om = torch.empty(1, dtype=torch.int64, device=self.device)
+        L = N.lib()
+        with torch.cuda.device(self.device):
+            st = N.stream_ptr(self.device)
+            N.check(L.mmlttb_p2p_publish(idx.data_ptr(), xs.data_ptr(), ys.data_ptr(), cnt.data_ptr(), cap,
+                                         self.peer_bufs.data_ptr(), self.peer_pads.data_ptr(),
+                                         self.own_pad.data_ptr(), G, self.rank, self.epoch, st), "p2p_publish")
+            N.check(L.mmlttb_p2p_merge(self.buf.data_ptr(), self.own_pad.data_ptr(), self.peer_pads.data_ptr(), G,
+                                       self.rank, cap, self.epoch, oi.data_ptr(), ox.data_ptr(), oy.data_ptr(),
+                                       om.data_ptr(), st), "p2p_merge")
+        return oi, ox, oy, om
+
+
+_PEER_EXCHANGES: dict = {}
+
+
+def _peer_exchange(cap: int, device, group) -> PeerExchange:
+    key = (cap, str(device), id(group))
+    ex = _PEER_EXCHANGES.get(key)
+    if ex is None:
+        ex = _PEER_EXCHANGES[key] = PeerExchange(cap, device, group)
+    return ex
+
+
 def shard_preselect(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out: int, r_ps: int, shard: Shard):
     """K1 + K2 on this rank's elements -> (idx, x f64, y f64, count) on device."""
     dev = y_shard.device
@@ -154,6 +222,20 @@ def shard_preselect(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out:
                                          ys.data_ptr(), cnt.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(dev)),
                 "shard_preselect", n)
     return idx, xs, ys, cnt
+
+
+def lttb_merged(oi, ox, oy, om, n_out: int, r_ps: int) -> torch.Tensor:
+    """The LTTB stage over an already merged preselected set (m on device)."""
+    dev = oi.device
+    out = torch.empty(n_out, dtype=torch.int64, device=dev)
+    L = N.lib()
+    with torch.cuda.device(dev):
+        wsb = L.mmlttb_lttb_preselected_workspace_bytes(1, n_out, r_ps)
+        ws = N.workspace(wsb, dev)
+        N.check(L.mmlttb_lttb_preselected(oi.data_ptr(), ox.data_ptr(), oy.data_ptr(), om.data_ptr(), 1, oi.numel(),
+                                          n_out, r_ps, out.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(dev)),
+                "lttb_preselected")
+    return out
 
 
 def merge_and_lttb(idx, xs, ys, counts, n_out: int, r_ps: int) -> torch.Tensor:
@@ -179,13 +261,17 @@ def merge_and_lttb(idx, xs, ys, counts, n_out: int, r_ps: int) -> torch.Tensor:
 
 
 def minmaxlttb_series_sharded(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out: int, r_ps: int = 4,
-                              group=None) -> torch.Tensor:
+                              group=None, exchange_mode: str = "nccl") -> torch.Tensor:
     """minmaxlttb of ONE series split by bucket ranges across the ranks.
 
     ``x_shard``/``y_shard`` hold elements ``[shard.lo, shard.hi)`` of the
     series for this rank (see :func:`bucket_ranges`).  Returns the n_out
     indices (identical to the single-device result) on every rank.
+    ``exchange_mode``: "nccl" (one all_gather, default) or "p2p" (device-
+    initiated stores into the peers' symmetric buffers, :class:`PeerExchange`).
     """
+    if exchange_mode not in ("nccl", "p2p"):
+        raise ValueError(f"exchange_mode must be 'nccl' or 'p2p', got {exchange_mode!r}")
     _check_n_out(n, n_out)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -193,6 +279,10 @@ def minmaxlttb_series_sharded(x_shard: torch.Tensor, y_shard: torch.Tensor, n: i
     if y_shard.shape[0] != shard.hi - shard.lo or x_shard.shape[0] != y_shard.shape[0]:
         raise ValueError(f"rank {rank} must hold elements [{shard.lo}, {shard.hi}) of the series")
     idx, xs, ys, cnt = shard_preselect(x_shard, y_shard, n, n_out, r_ps, shard)
+    if exchange_mode == "p2p":
+        if not dist.is_initialized():
+            raise RuntimeError("exchange_mode='p2p' needs an initialised process group")
+        return lttb_merged(*_peer_exchange(shard.cap, y_shard.device, group)(idx, xs, ys, cnt), n_out, r_ps)
     buf = pack(idx, xs, ys, cnt, shard.cap)
     allbuf = exchange(buf, world, group) if world > 1 else buf
     gi, gx, gy, gc = unpack(allbuf, world, shard.cap)
