@@ -390,3 +390,81 @@ def test_plan_graph_replay():
         plan(xd, yd.float())
     with pytest.raises(errors.NOutOfRange):
         mm.MinMaxLTTBPlan(100, 101, 4)
+
+
+def _minmaxlttb_abi(x, y2d, n, n_out, r, y_ld):
+    """mmlttb_minmaxlttb through the C ABI on a [B, y_ld] buffer (rows padded)."""
+    from paper_2305_00332_b200 import _native as NN
+    B = y2d.shape[0]
+    out = torch.empty((B, n_out), dtype=torch.int64, device=DEV)
+    ydt = NN.DTYPE_CODE[y2d.dtype]
+    L = NN.lib()
+    wsb = L.mmlttb_workspace_bytes(NN.OP_MINMAXLTTB, B, n, n_out, r, ydt)
+    ws = NN.workspace(wsb, DEV, n)
+    NN.check(L.mmlttb_minmaxlttb(x.data_ptr(), NN.DTYPE_CODE[x.dtype], 0, y2d.data_ptr(), ydt, y_ld, B, n, n_out, r,
+                                 out.data_ptr(), None, ws.data_ptr(), wsb, NN.stream_ptr(DEV)), "minmaxlttb", n)
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("ydt,n,pad,r,n_out", [(np.float32, 20_000, 0, 4, 257), (np.float32, 20_003, 1, 2, 300),
+                                               (np.float64, 16_001, 1, 8, 130), (np.float64, 24_000, 2, 6, 201),
+                                               (np.float32, 9_001, 3, 4, 1000)])
+def test_fused_padded_rows(ydt, n, pad, r, n_out):
+    """Fused per-series kernel through the C ABI with B > resident CTAs and a
+    padded row stride (y_ld > n, padding = NaN that must never be read)."""
+    rng = np.random.Generator(np.random.PCG64(n + r))
+    B, y_ld = 420, n + pad
+    y = np.zeros((B, y_ld), dtype=ydt)
+    y[:, :n] = np.cumsum(rng.standard_normal((B, n)), axis=1)
+    y[:, n:] = np.nan  # padding must never be read
+    y[7, ::5] = -0.0
+    y[9, :n] = 2.5
+    y[11, n - 1] = 1e30
+    x = np.arange(n, dtype=np.int64)
+    out = _minmaxlttb_abi(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n, n_out, r, y_ld)
+    for i in range(B):
+        assert np.array_equal(out[i], O.minmaxlttb(x, y[i, :n].astype(np.float64), n_out, r)), i
+
+
+TMA_KNOBS = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+import paper_2305_00332_b200 as mm
+from oracle import oracle as O
+from test_gpu_parity import _minmaxlttb_abi
+rng = np.random.Generator(np.random.PCG64(5))
+B, n = 350, 12_000
+y = np.cumsum(rng.standard_normal((B, n)), axis=1).astype(np.float32)
+x = np.arange(n, dtype=np.int64)
+out = mm.minmaxlttb(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), 400, minmax_ratio=4).cpu().numpy()
+for i in range(B):
+    assert np.array_equal(out[i], O.minmaxlttb(x, y[i].astype(np.float64), 400, 4)), i
+for ydt, n, pad, r in ((np.float32, 12_003, 1, 2), (np.float64, 9_001, 1, 8)):  # row tails past the aligned end
+    yp = np.full((B, n + pad), np.nan, dtype=ydt)
+    yp[:, :n] = np.cumsum(rng.standard_normal((B, n)), axis=1)
+    x = np.arange(n, dtype=np.int64)
+    out = _minmaxlttb_abi(torch.from_numpy(x).cuda(), torch.from_numpy(yp).cuda(), n, 300, r, n + pad)
+    for i in range(B):
+        assert np.array_equal(out[i], O.minmaxlttb(x, yp[i, :n].astype(np.float64), 300, r)), (n, i)
+print("TMA_OK")
+'''
+
+
+@pytest.mark.parametrize("env", [{"MMLTTB_TMA_VARIANT": "0"},
+                                 {"MMLTTB_TMA_VARIANT": "0", "MMLTTB_TMA_TILE": "512", "MMLTTB_TMA_STAGES": "2"},
+                                 {"MMLTTB_TMA_VARIANT": "5", "MMLTTB_TMA_TILE": "3000", "MMLTTB_TMA_STAGES": "5"},
+                                 {"MMLTTB_TMA_VARIANT": "1", "MMLTTB_TMA_STAGES": "3"},
+                                 {"MMLTTB_TMA_VARIANT": "4"}, {"MMLTTB_TMA_VARIANT": "2", "MMLTTB_TMA_STAGES": "8"}])
+def test_fused_tma_knobs(env):
+    """Opt-in TMA-fed persistent fused kernel (MMLTTB_TMA_VARIANT >= 0):
+    several series per CTA, ring slots reused across series, ring geometry
+    extremes (tiny tiles, 2..8 slots), 128-byte-widened bulk copies and row
+    tails past the last 16-byte-aligned element."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", TMA_KNOBS], cwd=root, env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "TMA_OK" in p.stdout, p.stdout[-2000:] + p.stderr[-4000:]
