@@ -448,6 +448,11 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg_bytes},
             "stage_ms": {"k1_extrema": stage_ms[0], "k2_compact": stage_ms[1], "k3_lttb": stage_ms[2]},
+            # LTTB stage latency per output bucket (the sequential chain the
+            # tables + scan resolve); fused / graph paths do not split stages
+            "lttb_stage": None if stage_ms[2] <= 0 else {
+                "ms": stage_ms[2], "buckets": (n_out - 2) * batch,
+                "ns_per_bucket": stage_ms[2] * 1e6 / max(1, (n_out - 2) * batch)},
             "cpu_baseline": cpu,
             "e2e": None if e2e_value is None else {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": e2e_ms, "steps": e2e_steps,
