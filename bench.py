@@ -291,10 +291,10 @@ def run_ours(args):
     from paper_2305_00332_b200 import _native as NAT
 
     ws, rank, local = _dist()
-    if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local)  # before the process group: NCCL binds each rank to its device
     dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
     name = args.workload
     n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
     scaling = "weak"

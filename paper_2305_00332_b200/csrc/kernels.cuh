@@ -1185,6 +1185,15 @@ __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
 //                   bucket scans until the chain re-joins the candidate
 //                   chain (whose later buckets were verified), then writes
 //                   the output.  So the result never depends on the heuristic.
+// points in flight per thread in the K3c streaming scans (candidate search,
+// verification): these kernels are load-latency-bound, not issue-bound
+#ifndef K3C_UN_DIR
+#define K3C_UN_DIR 4
+#endif
+#ifndef K3C_UN_VER
+#define K3C_UN_VER 4
+#endif
+
 __device__ __forceinline__ double hcross(double ox, double oy, double ax, double ay, double bx, double by) {
   return (ax - ox) * (by - oy) - (ay - oy) * (bx - ox);
 }
@@ -1327,7 +1336,7 @@ __global__ void __launch_bounds__(128) k_lttb_dircand(LttbArgs a) {
   int imax[D], imin[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) { vmax[k] = -INFINITY; vmin[k] = INFINITY; imax[k] = INT_MAX; imin[k] = INT_MAX; }
-  constexpr int UN = 4;
+  constexpr int UN = K3C_UN_DIR;
   for (int64_t j0 = blo + threadIdx.x; j0 < bhi; j0 += 128 * UN) {
     XT rx[UN];
     YT ry[UN];
@@ -1448,7 +1457,7 @@ __device__ __forceinline__ int64_t block_bucket_argmax(const XT* xs, const YT* y
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double bestv = -1.0;
   long long bi = LLONG_MAX;
-  constexpr int UN = 4;
+  constexpr int UN = K3C_UN_VER;
   for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += (int64_t)NT * UN) {
     XT rx[UN];
     YT ry[UN];
