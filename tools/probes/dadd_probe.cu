@@ -41,6 +41,18 @@ __global__ void chain_smem(const double* v, int n, double* out, long long* cyc) 
   cyc[0] = t1 - t0;
 }
 
+__global__ void chain_many(double a, int n, double* out, long long* cyc) {
+  // lanes 0/1 of every warp run a dependent DADD chain, like k_lttb_means_staged
+  double acc = 0.0, b = a * 0.5;
+  long long t0 = clock64();
+  if ((threadIdx.x & 31) < 2) {
+#pragma unroll 16
+    for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, (i & 1) ? a : b);
+  }
+  long long t1 = clock64();
+  if ((threadIdx.x & 31) == 0) { out[blockIdx.x] = acc; if (blockIdx.x == 0) cyc[0] = t1 - t0; }
+}
+
 int main() {
   double *v, *out;
   long long* cyc;
@@ -60,6 +72,14 @@ int main() {
     chain<<<1, 1>>>(v, n, out, cyc);
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("global-fed chain (L1 hits): %.2f cycles/add\n", (double)c / n);
+  }
+  double* out2;
+  cudaMalloc(&out2, 8 * 8192);
+  for (int ctas : {1, 148, 148 * 4, 148 * 8, 148 * 14, 148 * 28}) {
+    chain_many<<<ctas, 32>>>(1.0, n, out2, cyc);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%5d one-warp CTAs (%.1f warps/SM), lanes 0/1 chain: %.2f cycles/add\n", ctas, ctas / 148.0, (double)c / n);
   }
   return 0;
 }
