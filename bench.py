@@ -10,8 +10,12 @@ minmax_ratio = 4) -- the north star's "10^9-point series".
 Inputs are generated ON the device (torch Philox, seed 3; a 4 GB float32 y
 is larger than the 126 MB L2, so consecutive steps never hit in L2) and the
 warm-up output is checked index-exactly against the CPU oracle on the same
-data.  Under torchrun every rank runs its own independent series (batch
-sharding, no collective): "scaling": "weak".
+data.  Under torchrun (N > 1) the default workload becomes ONE series of
+N x 1e9 points split by MinMax bucket ranges across the ranks (SURVEY 8(e)
+single-series path: K1 + K2 on each rank's 1e9-point shard, one NCCL
+all_gather of the preselected sets, device merge, LTTB): per-GPU work is
+fixed, "scaling": "weak".  c4 shards its 4096 series across ranks (no
+collective, "strong"); c5s splits the 2e9-point C5 series ("strong").
 
 --impl reference times the reference algorithm's CPU restatement
 (oracle/, OpenMP over all host threads, float64 inputs as tsdown.TimeSeries
@@ -298,7 +302,9 @@ def run_ours(args):
     name = args.workload
     n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
     scaling = "weak"
-    sharded = name == "c5s"
+    sharded = name == "c5s" or (name == "c3_1e9" and ws > 1)
+    if name == "c3_1e9" and ws > 1:  # one N x 1e9-point series, bucket-range sharded (weak)
+        n = n * ws
     if name == "c4" and ws > 1:  # C4: 4096 series sharded across ranks (strong)
         from paper_2305_00332_b200.sharding import batch_range
 
@@ -310,7 +316,7 @@ def run_ours(args):
 
         shard = sharding.bucket_ranges(n, n_out, r_ps, ws)[rank]
         x, y = make_shard(name, dev, 3 + rank, shard.lo, shard.hi)
-        scaling = "strong"
+        scaling = "strong" if name == "c5s" else "weak"
     else:
         x, y = make_inputs(name, dev, seed=3 + rank, batch=batch)
     L = NAT.lib()
@@ -438,6 +444,9 @@ def run_ours(args):
             "dtype": ydt,
             "data": "synthetic (device-generated, torch Philox; BASELINE.json recipe shapes)",
             "config": {"workload": name, "n": n, "batch": batch, "n_out": n_out, "minmax_ratio": r_ps, "op": op,
+                       "sharding": ("bucket-range shards of one series + NCCL all_gather" if sharded
+                                    else "batch rows per rank" if name == "c4" and ws > 1 else
+                                    "independent replica per rank" if ws > 1 else "none"),
                        "x_dtype": xdt, "graph": bool(plan is not None),
                        "l2": "inputs larger than L2 (no flush needed)" if n * batch * (4 if ydt == "f32" else 8) > 126e6
                        else "inputs smaller than L2: steady-state L2-resident repeat calls",
