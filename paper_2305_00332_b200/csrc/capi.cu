@@ -340,8 +340,11 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   a.tables = tabs;
   a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", H);  // test knob: a poor heuristic must still be exact
   // one warp per bucket, 8 KB of tiles each: every bucket's chain resident at once
-  k_lttb_means_staged<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
-  int rc = check_launch("k_lttb_means_staged");
+  // loads two tiles ahead (59 vs 64 us on C2); MMLTTB_K3C_MEANS=1: one tile ahead (A/B knob)
+  static const int64_t mv = env_i64("MMLTTB_K3C_MEANS", 0);
+  if (mv == 1) k_lttb_means_staged<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
+  else k_lttb_means_staged2<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
+  int rc = check_launch("k_lttb_means");
   if (rc) return rc;
   if (use_hull()) {
     k_lttb_hull<XT, YT, H><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);

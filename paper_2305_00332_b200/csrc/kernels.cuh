@@ -1109,6 +1109,94 @@ __global__ void __launch_bounds__(32) k_lttb_means_staged(LttbArgs a) {
   }
 }
 
+// Same as k_lttb_means_staged with the global loads issued TWO tiles ahead
+// (two register buffers), so a tile's loads have two chain segments to land.
+template <typename XT, typename YT, int TILE>
+__global__ void __launch_bounds__(32) k_lttb_means_staged2(LttbArgs a) {
+  __shared__ double s_t[2][2][TILE];  // [buffer][x|y][i]
+  const int lane = threadIdx.x & 31;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t g = (int64_t)blockIdx.x;
+  if (g >= a.B * (k3 + 1)) return;
+  const int64_t s = g / (k3 + 1), b = g % (k3 + 1) - 1;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  if (b + 1 >= k3) {
+    if (lane == 0) a.means[s * a.means_ld + b] = make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
+    return;
+  }
+  const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
+  constexpr int PER = TILE / 32;
+  XT ax[PER], bx[PER];
+  YT ay[PER], by[PER];
+  double ymn = INFINITY, ymx = -INFINITY;
+  auto fetch = [&](XT* rx, YT* ry, int64_t t0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t j = t0 + q * 32 + lane;
+      rx[q] = j < nhi ? xs[j] : (XT)0;
+      ry[q] = j < nhi ? ys[j] : (YT)0;
+    }
+  };
+  auto stash = [&](int buf, const XT* rx, const YT* ry, int64_t t0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const double vy = (double)ry[q];
+      s_t[buf][0][q * 32 + lane] = (double)rx[q];
+      s_t[buf][1][q * 32 + lane] = vy;
+      if (t0 + q * 32 + lane < nhi) { ymn = fmin(ymn, vy); ymx = fmax(ymx, vy); }
+    }
+  };
+  double acc = 0.0;
+  const int which = lane & 1;
+  auto chain = [&](int buf, int64_t t0) {
+    if (lane < 2) {
+      const int n = (int)(nhi - t0 < TILE ? nhi - t0 : (int64_t)TILE);
+      const double* src = s_t[buf][which];
+      int i = 0;
+      for (; i + 8 <= n; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = src[i + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
+      }
+      for (; i < n; ++i) acc = __dadd_rn(acc, src[i]);
+    }
+  };
+  fetch(ax, ay, nlo);
+  fetch(bx, by, nlo + TILE);
+  stash(0, ax, ay, nlo);
+  fetch(ax, ay, nlo + 2 * TILE);
+  __syncwarp();
+  for (int64_t t0 = nlo; t0 < nhi; t0 += 2 * TILE) {
+    chain(0, t0);  // tile t0; b* holds t0+T, a* holds t0+2T (in flight)
+    __syncwarp();
+    if (t0 + TILE >= nhi) break;
+    stash(1, bx, by, t0 + TILE);
+    fetch(bx, by, t0 + 3 * TILE);
+    __syncwarp();
+    chain(1, t0 + TILE);
+    __syncwarp();
+    if (t0 + 2 * TILE >= nhi) break;
+    stash(0, ax, ay, t0 + 2 * TILE);
+    fetch(ax, ay, t0 + 4 * TILE);
+    __syncwarp();
+  }
+  const double cnt = (double)(nhi - nlo);
+  const double sy = __shfl_sync(FULL, acc, 1);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    ymn = fmin(ymn, __shfl_xor_sync(FULL, ymn, o));
+    ymx = fmax(ymx, __shfl_xor_sync(FULL, ymx, o));
+  }
+  if (lane == 0) {
+    if (b >= 0) a.means[s * a.means_ld + b] = make_double2(__ddiv_rn(acc, cnt), __ddiv_rn(sy, cnt));
+    if (a.yrange) a.yrange[s * k3 + b + 1] = make_double2(ymn, ymx);
+  }
+}
+
 // K3b, part 2: one CTA per series carries the bucket-to-bucket dependency.
 template <typename XT, typename YT, int NT>
 __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
