@@ -584,17 +584,32 @@ int* take_status(Carve& cv, cudaStream_t st) {
 
 // ---- fused K2+K3 (single / few series) -----------------------------------
 constexpr int64_t POST_SMEM_MAX = 100 * 1024;
+constexpr int64_t POST_SMEM2_MAX = 200 * 1024;
 
 bool post_ok(int64_t k, int64_t n_out, int64_t r_ps) {
   static const bool off = env_i64("MMLTTB_NO_POST_FUSED", 0) != 0;  // A/B knob
   // one CTA's latency chains beat two extra launches only for small k
-  // (measured: k = 1996 24 us vs 24 us + a launch; k = 3996 41 us vs 24 us)
+  // (measured: k = 1996 24 us vs 24 us + a launch; k = 3996 41 us vs 24 us;
+  // with the set staged in shared memory, k_post_smem, C1 takes 14.6 us)
   return !off && k <= 2048 && smax_for(r_ps) > 0 && smax_for(r_ps) <= 8 &&
          post_smem(n_out - 2, smax_for(r_ps)) <= POST_SMEM_MAX;
 }
 
 template <typename XT, typename YT, int SMAX>
 int launch_post_t(const PostArgs& pa, int64_t B, cudaStream_t st) {
+  static const bool global_staging = env_i64("MMLTTB_POST_GLOBAL", 0) != 0;  // A/B knob
+  const int64_t sm2 = post_smem2(pa.n_out - 2, SMAX, pa.cap);
+  if (!global_staging && sm2 <= POST_SMEM2_MAX) {  // preselected set staged in shared memory
+    static bool attr2 = false;
+    if (!attr2) {
+      if (cudaFuncSetAttribute(k_post_smem<XT, YT, SMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)POST_SMEM2_MAX) != cudaSuccess)
+        return fail(MM_ECUDA, "cudaFuncSetAttribute(k_post_smem)");
+      attr2 = true;
+    }
+    k_post_smem<XT, YT, SMAX, 1024><<<(unsigned)B, 1024, (size_t)sm2, st>>>(pa);
+    return check_launch("k_post_smem");
+  }
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(k_post_fused<XT, YT, SMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -577,6 +577,113 @@ __global__ void __launch_bounds__(NT) k_post_fused(PostArgs a) {
   }
 }
 
+// Same as k_post_fused with the preselected set staged in SHARED memory
+// (positions, x and y as f64): the LTTB phases then make no global round
+// trips -- one L2 gather of x in the compaction, everything else on chip.
+__host__ __device__ inline int64_t post_smem2(int64_t k3, int smax, int64_t cap) {
+  return k3 * 16 + ((k3 * smax + 15) / 16) * 16 + cap * 24;
+}
+
+template <typename XT, typename YT, int SMAX, int NT>
+__global__ void __launch_bounds__(NT) k_post_smem(PostArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int sh[NT / 32 + 1];
+  const int64_t s = blockIdx.x;
+  const int64_t k = a.k, N = a.N, k3 = a.n_out - 2;
+  const Ext* ext = a.ext + s * k;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  double2* s_mean = reinterpret_cast<double2*>(sm);
+  unsigned char* s_tab = sm + k3 * 16;
+  double* s_px = reinterpret_cast<double*>(sm + k3 * 16 + ((k3 * SMAX + 15) / 16) * 16);
+  double* s_py = s_px + a.cap;
+  long long* s_pre = reinterpret_cast<long long*>(s_py + a.cap);
+  const int ydt = sizeof(YT) == 4 ? 0 : 1;
+  // ---- compaction: [0] + (lo, hi)... + [N-1]  (downsamplers.py:60-69, 157-160)
+  int64_t carry = 1;
+  for (int64_t c0 = 0; c0 < k; c0 += NT) {
+    const int64_t b = c0 + threadIdx.x;
+    int n = 0;
+    int64_t lo = 0, hi = 0;
+    long long klo = 0, khi = 0;
+    double xl = 0.0, xh = 0.0;
+    if (b < k) {
+      const Ext e = ext[b];
+      if (a.status && keys_nonfinite(e.kmin, e.kmax, ydt)) atomicOr(a.status, 1);
+      const bool mfirst = e.imin <= e.imax;
+      lo = mfirst ? e.imin : e.imax;
+      hi = mfirst ? e.imax : e.imin;
+      klo = mfirst ? e.kmin : e.kmax;
+      khi = mfirst ? e.kmax : e.kmin;
+      n = hi != lo ? 2 : 1;
+      xl = to_f64(xs, lo);  // both gathers in flight across the scan
+      if (n == 2) xh = to_f64(xs, hi);
+    }
+    int tot;
+    const int ex = block_excl_scan<NT>(n, tot, sh);
+    if (b < k) {
+      const int64_t p = carry + ex;
+      s_pre[p] = lo; s_px[p] = xl; s_py[p] = key_value<YT>(klo);
+      if (n == 2) { s_pre[p + 1] = hi; s_px[p + 1] = xh; s_py[p + 1] = key_value<YT>(khi); }
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    const double y0 = to_f64(ys, 0), yl = to_f64(ys, N - 1);
+    if (a.status && (!isfinite(y0) || !isfinite(yl))) atomicOr(a.status, 1);
+    s_pre[0] = 0; s_px[0] = to_f64(xs, 0); s_py[0] = y0;
+    s_pre[carry] = N - 1; s_px[carry] = to_f64(xs, N - 1); s_py[carry] = yl;
+  }
+  const int64_t m = carry + 1;
+  __syncthreads();
+  // b * (m - 2) < 2^32 (m <= 2k + 2 and k is small on this path)
+  const unsigned um = (unsigned)(m - 2), uk3 = (unsigned)k3;
+  auto lb = [&](int64_t b) -> int64_t { return 1 + (int64_t)(((unsigned)b * um) / uk3); };
+  // ---- LTTB over the m points (_kernels.py:81-119): means, tables, chain
+  for (int64_t b = threadIdx.x; b < k3; b += NT) {
+    double2 c;
+    if (b + 1 < k3) {
+      const int64_t nlo = lb(b + 1), nhi = lb(b + 2);
+      double sx = 0.0, sy = 0.0;
+      for (int64_t j = nlo; j < nhi; ++j) {
+        sx = __dadd_rn(sx, s_px[j]);
+        sy = __dadd_rn(sy, s_py[j]);
+      }
+      const double cnt = (double)(nhi - nlo);
+      c = make_double2(__ddiv_rn(sx, cnt), __ddiv_rn(sy, cnt));
+    } else {
+      c = make_double2(s_px[m - 1], s_py[m - 1]);
+    }
+    s_mean[b] = c;
+  }
+  __syncthreads();
+  for (int64_t it = threadIdx.x; it < k3 * SMAX; it += NT) {
+    const int64_t b = it / SMAX;
+    const int p = (int)(it % SMAX);
+    const int64_t blo = lb(b), bhi = lb(b + 1);
+    const bool valid = b == 0 ? p == 0 : p < blo - lb(b - 1);
+    const int64_t ap = b == 0 ? 0 : lb(b - 1) + p;
+    unsigned char r = 0;
+    if (valid) {
+      const double ax = s_px[ap], ay = s_py[ap];
+      const double2 c = s_mean[b];
+      double best = -1.0;
+      for (int64_t j = blo; j < bhi; ++j) {
+        const double ar = lttb_area(ax, ay, c.x, c.y, s_px[j], s_py[j]);
+        if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
+      }
+    }
+    s_tab[it] = r;
+  }
+  __syncthreads();
+  int64_t* out = a.out + s * a.n_out;
+  scan_chain<SMAX, NT, 4>(s_tab, k3, [&](int64_t b, int sel) { out[b + 1] = s_pre[lb(b) + sel]; });
+  if (threadIdx.x == 0) {
+    out[0] = 0;
+    out[k3 + 1] = N - 1;
+  }
+}
+
 }  // namespace mm
 
 #include <cooperative_groups.h>
