@@ -93,10 +93,18 @@ def lib() -> ctypes.CDLL:
     return _lib if _lib is not None else load()
 
 
+_cuda_ok = False
+
+
 def require_cuda(device=None) -> torch.device:
-    if not torch.cuda.is_available():
-        raise errors.CudaError("no CUDA device: the MinMaxLTTB device path has no CPU fallback")
-    lib()
+    global _cuda_ok
+    if not _cuda_ok:  # availability cannot change once the driver has initialised
+        if not torch.cuda.is_available():
+            raise errors.CudaError("no CUDA device: the MinMaxLTTB device path has no CPU fallback")
+        lib()
+        _cuda_ok = True
+    if isinstance(device, torch.device) and device.type == "cuda" and device.index is not None:
+        return device
     if device is None:
         return torch.device("cuda", torch.cuda.current_device())
     d = torch.device(device)
@@ -106,7 +114,11 @@ def require_cuda(device=None) -> torch.device:
 
 
 def stream_ptr(device: torch.device) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
+    """Raw cudaStream_t of the device's current torch stream (per-call hot path)."""
+    try:
+        return torch._C._cuda_getCurrentRawStream(device.index)
+    except (AttributeError, TypeError):  # pragma: no cover - older torch
+        return torch.cuda.current_stream(device).cuda_stream
 
 
 def ptr(t) -> int | None:

@@ -20,6 +20,8 @@ is always bucket-parallel and byte-identical to the sequential reference.
 """
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 import torch
 
@@ -72,8 +74,7 @@ class Batch:
         if self._ready:
             return self
         y, x = self._y_in, self._x_in
-        dev = y.device if not self.host else N.require_cuda(self._dev_in)
-        N.require_cuda(dev)
+        dev = N.require_cuda(y.device if not self.host else self._dev_in)
         yt = torch.as_tensor(y) if not isinstance(y, torch.Tensor) else y
         if yt.dtype not in (torch.float32, torch.float64):
             yt = yt.to(torch.float64)
@@ -161,6 +162,9 @@ def _codes(b):
 
 
 def _ctx(b):
+    # switching devices costs two driver calls; skip it when already there
+    if torch.cuda.current_device() == b.device.index:
+        return contextlib.nullcontext()
     return torch.cuda.device(b.device)
 
 
