@@ -350,7 +350,11 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
     k_lttb_hull<XT, YT, H><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_hull"))) return rc;
   } else {
-    k_lttb_dircand<XT, YT, H, H / 2><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
+    static const int64_t dnt = env_i64("MMLTTB_K3C_DIRCAND_NT", 64);  // A/B knob (64: 64 vs 68 us at 128 on C2)
+    if (dnt == 32) k_lttb_dircand<XT, YT, H, H / 2, 32><<<dim3((unsigned)k3, (unsigned)a.B), 32, 0, st>>>(a);
+    else if (dnt == 64) k_lttb_dircand<XT, YT, H, H / 2, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
+    else if (dnt == 256) k_lttb_dircand<XT, YT, H, H / 2, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
+    else k_lttb_dircand<XT, YT, H, H / 2, 128><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_dircand"))) return rc;
   }
   k_lttb_ctables<XT, YT, H><<<dim3((unsigned)cdiv(k3, 1024 / H), (unsigned)a.B), 1024, 0, st>>>(a);
@@ -358,7 +362,12 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   k_lttb_scan<H, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_scan"))) return rc;
   if (cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
-  k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
+  static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);  // A/B knob (64: 30 vs 37.5 us at 256 on C2)
+  if (vnt == 512) k_lttb_verify<XT, YT, 512><<<dim3((unsigned)k3, (unsigned)a.B), 512, 0, st>>>(a);
+  else if (vnt == 128) k_lttb_verify<XT, YT, 128><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
+  else if (vnt == 64) k_lttb_verify<XT, YT, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
+  else if (vnt == 32) k_lttb_verify<XT, YT, 32><<<dim3((unsigned)k3, (unsigned)a.B), 32, 0, st>>>(a);
+  else k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_verify"))) return rc;
   k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_verify2"))) return rc;

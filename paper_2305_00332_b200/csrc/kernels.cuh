@@ -1276,10 +1276,10 @@ __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
 // points in flight per thread in the K3c streaming scans (candidate search,
 // verification): these kernels are load-latency-bound, not issue-bound
 #ifndef K3C_UN_DIR
-#define K3C_UN_DIR 4
+#define K3C_UN_DIR 8
 #endif
 #ifndef K3C_UN_VER
-#define K3C_UN_VER 4
+#define K3C_UN_VER 8
 #endif
 
 __device__ __forceinline__ double hcross(double ox, double oy, double ax, double ay, double bx, double by) {
@@ -1377,14 +1377,15 @@ __global__ void __launch_bounds__(64) k_lttb_hull(LttbArgs a) {
 // D directions sampled across that span, argmax and argmin of each (the
 // maximiser of |f| is one of them) -> <= 2D candidates per bucket.  Exact
 // only in the limit; k_lttb_verify / k_lttb_repair make the result exact.
-template <typename XT, typename YT, int HMAX, int D>
-__global__ void __launch_bounds__(128) k_lttb_dircand(LttbArgs a) {
+template <typename XT, typename YT, int HMAX, int D, int NT = 128>
+__global__ void __launch_bounds__(NT) k_lttb_dircand(LttbArgs a) {
   static_assert(2 * D <= HMAX && 2 * D <= 32, "candidates must fit");
-  __shared__ float s_v[4][2 * D];
-  __shared__ int s_i[4][2 * D];
+  constexpr int NWC = NT / 32;
+  __shared__ float s_v[NWC][2 * D];
+  __shared__ int s_i[NWC][2 * D];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k3 = a.n_out - 2;
-  const int64_t s = blockIdx.y, b = blockIdx.x;  // one 4-warp CTA per bucket
+  const int64_t s = blockIdx.y, b = blockIdx.x;  // one CTA per bucket
   const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
   const XT* xs = (const XT*)a.x + s * a.x_ld;
   const YT* ys = (const YT*)a.y + s * a.y_ld;
@@ -1425,20 +1426,20 @@ __global__ void __launch_bounds__(128) k_lttb_dircand(LttbArgs a) {
 #pragma unroll
   for (int k = 0; k < D; ++k) { vmax[k] = -INFINITY; vmin[k] = INFINITY; imax[k] = INT_MAX; imin[k] = INT_MAX; }
   constexpr int UN = K3C_UN_DIR;
-  for (int64_t j0 = blo + threadIdx.x; j0 < bhi; j0 += 128 * UN) {
+  for (int64_t j0 = blo + threadIdx.x; j0 < bhi; j0 += NT * UN) {
     XT rx[UN];
     YT ry[UN];
 #pragma unroll
     for (int u = 0; u < UN; ++u) {  // UN points' loads in flight before any use
-      const int64_t j = j0 + 128 * u < bhi ? j0 + 128 * u : blo;
+      const int64_t j = j0 + NT * u < bhi ? j0 + NT * u : blo;
       rx[u] = xs[j];
       ry[u] = ys[j];
     }
 #pragma unroll
     for (int u = 0; u < UN; ++u) {
-      if (j0 + 128 * u < bhi) {
+      if (j0 + NT * u < bhi) {
         const float X = (float)(rx[u] - xr), Y = (float)((double)ry[u] - yr);
-        const int o = (int)(j0 + 128 * u - blo);
+        const int o = (int)(j0 + NT * u - blo);
 #pragma unroll
         for (int k = 0; k < D; ++k) {
           const float v = fmaf(cs[k], X, sn[k] * Y);
@@ -1474,7 +1475,7 @@ __global__ void __launch_bounds__(128) k_lttb_dircand(LttbArgs a) {
     float bv = s_v[0][lane];
     ci = s_i[0][lane];
 #pragma unroll
-    for (int w = 1; w < 4; ++w) {
+    for (int w = 1; w < NWC; ++w) {
       const float v = s_v[w][lane];
       const int i = s_i[w][lane];
       if (v > bv || (v == bv && i < ci)) { bv = v; ci = i; }
