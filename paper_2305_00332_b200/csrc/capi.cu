@@ -369,9 +369,15 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   else if (vnt == 32) k_lttb_verify<XT, YT, 32><<<dim3((unsigned)k3, (unsigned)a.B), 32, 0, st>>>(a);
   else k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_verify"))) return rc;
-  k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
+  static const int64_t v2 = env_i64("MMLTTB_K3C_VERIFY2_NT", 256);  // A/B knob
+  if (v2 == 64) k_lttb_verify2<XT, YT, 64><<<dim3(148, (unsigned)a.B), 64, 0, st>>>(a);
+  else if (v2 == 128) k_lttb_verify2<XT, YT, 128><<<dim3(148, (unsigned)a.B), 128, 0, st>>>(a);
+  else k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_verify2"))) return rc;
-  k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
+  static const int64_t rp = env_i64("MMLTTB_K3C_REPAIR_NT", 512);  // A/B knob (512: 22.1 vs 24.4 us at 1024 on C2)
+  if (rp == 256) k_lttb_repair<XT, YT, 256><<<(unsigned)a.B, 256, 0, st>>>(a);
+  else if (rp == 512) k_lttb_repair<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
+  else k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
   return check_launch("k_lttb_repair");
 }
 
