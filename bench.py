@@ -43,6 +43,11 @@ WORKLOADS = {
     "c1": (1_000_000, 1, 1000, 4, "f64", "i64", "minmaxlttb"),
     "c2": (10_000_000, 1, 2000, 0, "f64", "i64", "lttb"),
     "c3": (100_000_000, 1, 2000, 4, "f32", "i64", "minmaxlttb"),
+    # C3's other preselection ratios (BASELINE.json: minmax_ratio in {2,4,8,16,32})
+    "c3r2": (100_000_000, 1, 2000, 2, "f32", "i64", "minmaxlttb"),
+    "c3r8": (100_000_000, 1, 2000, 8, "f32", "i64", "minmaxlttb"),
+    "c3r16": (100_000_000, 1, 2000, 16, "f32", "i64", "minmaxlttb"),
+    "c3r32": (100_000_000, 1, 2000, 32, "f32", "i64", "minmaxlttb"),
     "c4": (1_000_000, 4096, 1000, 4, "f32", "i64", "minmaxlttb"),
     "c5": (2_000_000_000, 1, 4000, 4, "f32", "f64", "minmaxlttb"),
     # one 2e9-point series split by MinMax bucket ranges over the ranks, one
