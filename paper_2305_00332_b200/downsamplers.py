@@ -107,15 +107,16 @@ class Batch:
         if self.x is None:
             return
         xs = self.x if self.x.is_cuda else self.x.to(self.device)
-        flags = torch.zeros(1, dtype=torch.int32, device=self.device)
-        acc = 0
+        flags = torch.zeros(self.B, dtype=torch.int32, device=self.device)  # one word per row: one sync in all
         with torch.cuda.device(self.device):
+            st = N.stream_ptr(self.device)
             for i in range(self.B):
                 xi = xs if xs.dim() == 1 else xs[i]
                 N.check(N.lib().mmlttb_validate(xi.data_ptr(), N.DTYPE_CODE[xi.dtype], self.y[i].data_ptr(),
-                                                N.DTYPE_CODE[self.y.dtype], self.n, flags.data_ptr(),
-                                                N.stream_ptr(self.device)), "validate", self.n)
-                acc |= int(flags.item())
+                                                N.DTYPE_CODE[self.y.dtype], self.n, flags[i:].data_ptr(), st),
+                        "validate", self.n)
+        bad = torch.stack([(flags & 1).any(), (flags & 2).any()]).tolist()
+        acc = (1 if bad[0] else 0) | (2 if bad[1] else 0)
         if acc & 1:
             raise NonFiniteValue("series contains NaN or infinite values")
         if acc & 2:
