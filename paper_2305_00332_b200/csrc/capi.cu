@@ -167,10 +167,19 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
     if (cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
     const int64_t blocks = cdiv(a.B * a.Ws, 8);
-    if (ydt == MM_F32)
-      k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
-    else
+    static const int64_t fv = env_i64("MMLTTB_K1_FLAT_VARIANT", 0);  // A/B knob (tools/flat_sweep.sh)
+    if (ydt == MM_F32) {
+      switch (fv) {
+        case 1: k_extrema_flat<float, 6, 3, 4><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+        case 2: k_extrema_flat<float, 4, 3, 4><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+        case 3: k_extrema_flat<float, 8, 1, 3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+        case 4: k_extrema_flat<float, 12, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+        case 5: k_extrema_flat<float, 16, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+        default: k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+      }
+    } else {
       k_extrema_flat<double, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+    }
     return check_launch("k_extrema_flat");
   }
   const bool small = a.C == 1 && a.chunk <= SMALL_BUCKET;

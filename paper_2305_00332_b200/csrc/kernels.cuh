@@ -291,8 +291,8 @@ __device__ __forceinline__ void publish_partial(const ExArgs& a, int64_t bkt, in
 // does the same work (no last-wave tail); a range spanning bucket edges
 // publishes one partial per intersected bucket (slot = w - first warp of the
 // bucket), combined by the bucket's last-arriving warp.
-template <typename T, int U, int LDV>
-__global__ void __launch_bounds__(256, 3) k_extrema_flat(ExArgs a) {
+template <typename T, int U, int LDV, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) k_extrema_flat(ExArgs a) {
   typedef YTr<T> Tr;
   typedef typename Tr::K K;
   const int lane = threadIdx.x & 31;
