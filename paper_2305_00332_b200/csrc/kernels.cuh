@@ -1804,13 +1804,15 @@ __global__ void k_p2p_merge(const long long* own_buf, const unsigned* own_pad, c
   __syncthreads();
   const long long* rows = own_buf + (int64_t)(epoch & 1) * G * W;
   int64_t off = 0;
-  for (int64_t h = 0; h < g; ++h) off += rows[h * W + 3 * cap];
+  // rows are written by peers over NVLink: read them at L2 (ld.cg), never
+  // from a possibly stale L1 line of this slot's previous use
+  for (int64_t h = 0; h < g; ++h) off += __ldcg(rows + h * W + 3 * cap);
   const long long* row = rows + g * W;
-  const int64_t n = row[3 * cap];
+  const int64_t n = __ldcg(row + 3 * cap);
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    oi[off + i] = row[i];
-    ox[off + i] = __longlong_as_double(row[cap + i]);
-    oy[off + i] = __longlong_as_double(row[2 * cap + i]);
+    oi[off + i] = __ldcg(row + i);
+    ox[off + i] = __longlong_as_double(__ldcg(row + cap + i));
+    oy[off + i] = __longlong_as_double(__ldcg(row + 2 * cap + i));
   }
   if (g == G - 1 && threadIdx.x == 0) om[0] = off + n;
   __syncthreads();
