@@ -142,6 +142,13 @@ int mmlttb_merge_shards(const int64_t *idx, const double *xs, const double *ys, 
                         int64_t G, int64_t cap, int64_t *out_idx, double *out_x, double *out_y,
                         int64_t *out_m, void *stream);
 
+/* Same merge straight from the gathered packed messages: buf is [G][3*cap+1]
+ * int64 rows (idx[cap] | x bits[cap] | y bits[cap] | count), i.e. the
+ * all_gather of what mmlttb_shard_preselect wrote at (buf, buf+cap,
+ * buf+2cap, buf+3cap); no unpacking copies. */
+int mmlttb_merge_packed(const int64_t *buf, int64_t G, int64_t cap, int64_t *out_idx, double *out_x, double *out_y,
+                        int64_t *out_m, void *stream);
+
 /* Device-initiated exchange over peer memory (NVLink stores + epoch flags)
  * in place of the NCCL all_gather: each rank's symmetric buffer is int64
  * [2][G][3*cap+1] (slot = epoch & 1, row = writer rank) with a uint32 signal

@@ -53,6 +53,7 @@ _SIGS = {
     "mmlttb_shard_preselect": (_i32, [_p, _i32, _p, _i32, _i64, _i64, _i64, _i64, _i64, _i64, _i32, _i32,
                                       _p, _p, _p, _p, _p, _i64, _p]),
     "mmlttb_merge_shards": (_i32, [_p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p]),
+    "mmlttb_merge_packed": (_i32, [_p, _i64, _i64, _p, _p, _p, _p, _p]),
     "mmlttb_p2p_publish": (_i32, [_p, _p, _p, _p, _i64, _p, _p, _p, _i64, _i64, ctypes.c_uint32, _p]),
     "mmlttb_p2p_merge": (_i32, [_p, _p, _p, _i64, _i64, _i64, ctypes.c_uint32, _p, _p, _p, _p, _p]),
     "mmlttb_lttb_preselected_workspace_bytes": (_i64, [_i64, _i64, _i64]),

@@ -1058,6 +1058,14 @@ int mmlttb_merge_shards(const int64_t* idx, const double* xs, const double* ys, 
   return check_launch("k_merge_shards");
 }
 
+int mmlttb_merge_packed(const int64_t* buf, int64_t G, int64_t cap, int64_t* out_idx, double* out_x, double* out_y,
+                        int64_t* out_m, void* stream) {
+  if (!buf || !out_idx || !out_x || !out_y || !out_m || G < 1 || cap < 1) return fail(MM_EINVAL, "bad arguments");
+  k_merge_packed<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>((const long long*)buf, G, cap, out_idx, out_x, out_y,
+                                                                out_m);
+  return check_launch("k_merge_packed");
+}
+
 int mmlttb_p2p_publish(const int64_t* idx, const double* xs, const double* ys, const int64_t* count, int64_t cap,
                        const uint64_t* peer_bufs, const uint64_t* peer_pads, const uint32_t* own_pad, int64_t G,
                        int64_t rank, uint32_t epoch, void* stream) {

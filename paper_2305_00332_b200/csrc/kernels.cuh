@@ -1822,6 +1822,23 @@ __global__ void k_p2p_merge(const long long* own_buf, const unsigned* own_pad, c
   }
 }
 
+// Rank-order merge straight from the gathered packed messages ([G][3cap+1]:
+// idx | x bits | y bits | count), so no unpacking copies are needed.
+__global__ void k_merge_packed(const long long* buf, int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy,
+                               int64_t* om) {
+  const int64_t g = blockIdx.x, W = 3 * cap + 1;
+  int64_t off = 0;
+  for (int64_t h = 0; h < g; ++h) off += buf[h * W + 3 * cap];
+  const long long* row = buf + g * W;
+  const int64_t n = row[3 * cap];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    oi[off + i] = row[i];
+    ox[off + i] = __longlong_as_double(row[cap + i]);
+    oy[off + i] = __longlong_as_double(row[2 * cap + i]);
+  }
+  if (g == G - 1 && threadIdx.x == 0) om[0] = off + n;
+}
+
 __global__ void k_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts,
                                int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy, int64_t* om) {
   const int64_t g = blockIdx.x;

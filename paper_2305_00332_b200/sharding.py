@@ -14,8 +14,9 @@ its only parallelism is numba ``prange`` over disjoint buckets
   (``mmlttb_shard_preselect``), the small preselected sets (global index, x,
   y as f64; <= 2*(b1-b0)+2 entries) are packed into one int64 buffer and
   exchanged with ONE ``all_gather`` (NCCL over NVLink), every rank merges
-  them in rank order on the device (``mmlttb_merge_shards``) and runs the
-  LTTB stage on the merged set (``mmlttb_lttb_preselected``).  The exchanged
+  them in rank order on the device (``mmlttb_merge_packed``, straight from
+  the gathered messages) and runs the LTTB stage on the merged set
+  (``mmlttb_lttb_preselected``).  The exchanged
   bytes are O(k), independent of N.
 """
 from __future__ import annotations
@@ -204,14 +205,24 @@ def _peer_exchange(cap: int, device, group) -> PeerExchange:
     return ex
 
 
-def shard_preselect(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out: int, r_ps: int, shard: Shard):
-    """K1 + K2 on this rank's elements -> (idx, x f64, y f64, count) on device."""
+def shard_preselect(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out: int, r_ps: int, shard: Shard,
+                    packed: torch.Tensor | None = None):
+    """K1 + K2 on this rank's elements -> (idx, x f64, y f64, count) on device.
+
+    With ``packed`` (int64 [3*cap+1]) the results are written straight into
+    the exchange message layout of :func:`pack` (views into ``packed``)."""
     dev = y_shard.device
     cap = shard.cap
-    idx = torch.empty(cap, dtype=torch.int64, device=dev)
-    xs = torch.empty(cap, dtype=torch.float64, device=dev)
-    ys = torch.empty(cap, dtype=torch.float64, device=dev)
-    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    if packed is not None:
+        idx = packed[:cap]
+        xs = packed[cap:2 * cap].view(torch.float64)
+        ys = packed[2 * cap:3 * cap].view(torch.float64)
+        cnt = packed[3 * cap:]
+    else:
+        idx = torch.empty(cap, dtype=torch.int64, device=dev)
+        xs = torch.empty(cap, dtype=torch.float64, device=dev)
+        ys = torch.empty(cap, dtype=torch.float64, device=dev)
+        cnt = torch.empty(1, dtype=torch.int64, device=dev)
     L = N.lib()
     with torch.cuda.device(dev):
         wsb = L.mmlttb_shard_workspace_bytes(n, n_out, r_ps, shard.b0, shard.b1)
@@ -222,6 +233,20 @@ def shard_preselect(x_shard: torch.Tensor, y_shard: torch.Tensor, n: int, n_out:
                                          ys.data_ptr(), cnt.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(dev)),
                 "shard_preselect", n)
     return idx, xs, ys, cnt
+
+
+def merge_packed(allbuf: torch.Tensor, world: int, cap: int):
+    """Device rank-order merge of the gathered packed messages (no unpack copies)."""
+    dev = allbuf.device
+    tot = world * cap
+    oi = torch.empty(tot, dtype=torch.int64, device=dev)
+    ox = torch.empty(tot, dtype=torch.float64, device=dev)
+    oy = torch.empty(tot, dtype=torch.float64, device=dev)
+    om = torch.empty(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        N.check(N.lib().mmlttb_merge_packed(allbuf.data_ptr(), world, cap, oi.data_ptr(), ox.data_ptr(),
+                                            oy.data_ptr(), om.data_ptr(), N.stream_ptr(dev)), "merge_packed")
+    return oi, ox, oy, om
 
 
 def lttb_merged(oi, ox, oy, om, n_out: int, r_ps: int) -> torch.Tensor:
@@ -278,12 +303,14 @@ def minmaxlttb_series_sharded(x_shard: torch.Tensor, y_shard: torch.Tensor, n: i
     shard = bucket_ranges(n, n_out, r_ps, world)[rank]
     if y_shard.shape[0] != shard.hi - shard.lo or x_shard.shape[0] != y_shard.shape[0]:
         raise ValueError(f"rank {rank} must hold elements [{shard.lo}, {shard.hi}) of the series")
-    idx, xs, ys, cnt = shard_preselect(x_shard, y_shard, n, n_out, r_ps, shard)
     if exchange_mode == "p2p":
         if not dist.is_initialized():
             raise RuntimeError("exchange_mode='p2p' needs an initialised process group")
+        idx, xs, ys, cnt = shard_preselect(x_shard, y_shard, n, n_out, r_ps, shard)
         return lttb_merged(*_peer_exchange(shard.cap, y_shard.device, group)(idx, xs, ys, cnt), n_out, r_ps)
-    buf = pack(idx, xs, ys, cnt, shard.cap)
+    # K1 + K2 write the exchange message in place (layout of pack()), one
+    # all_gather, then the merge reads the gathered messages directly
+    buf = torch.empty(3 * shard.cap + 1, dtype=torch.int64, device=y_shard.device)
+    shard_preselect(x_shard, y_shard, n, n_out, r_ps, shard, packed=buf)
     allbuf = exchange(buf, world, group) if world > 1 else buf
-    gi, gx, gy, gc = unpack(allbuf, world, shard.cap)
-    return merge_and_lttb(gi, gx, gy, gc, n_out, r_ps)
+    return lttb_merged(*merge_packed(allbuf, world, shard.cap), n_out, r_ps)

@@ -134,3 +134,22 @@ def test_series_sharded_p2p_world1():
     p = subprocess.run([sys.executable, "-c", P2P_WORLD1], cwd=root, env=env, capture_output=True, text=True,
                        timeout=300)
     assert p.returncode == 0 and "P2P_OK" in p.stdout, p.stdout[-2000:] + p.stderr[-4000:]
+
+
+@pytest.mark.parametrize("G,n,n_out,r", [(1, 100_000, 300, 4), (3, 1_000_003, 1000, 4), (8, 3_000_017, 2001, 2)])
+def test_virtual_shards_packed_merge(G, n, n_out, r):
+    """K1 + K2 writing the exchange message in place (shard_preselect(packed=)),
+    the concatenation an all_gather produces, then mmlttb_merge_packed."""
+    rng = np.random.Generator(np.random.PCG64(G * 31 + r))
+    x = np.cumsum(rng.exponential(1.0, n))
+    y = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+    xd, yd = torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV)
+    plan = S.bucket_ranges(n, n_out, r, G)
+    cap = plan[0].cap
+    bufs = []
+    for sh in plan:
+        buf = torch.full((3 * cap + 1,), -9, dtype=torch.int64, device=DEV)
+        S.shard_preselect(xd[sh.lo:sh.hi], yd[sh.lo:sh.hi], n, n_out, r, sh, packed=buf)
+        bufs.append(buf)
+    out = S.lttb_merged(*S.merge_packed(torch.cat(bufs), G, cap), n_out, r).cpu().numpy()
+    assert np.array_equal(out, O.minmaxlttb(x, y.astype(np.float64), n_out, r))
