@@ -1,4 +1,7 @@
-"""Compile libmmlttb.so in-tree for sm_100a (nvcc; no torch extension needed)."""
+"""Compile libmmlttb.so in-tree for sm_100a (nvcc; no torch extension needed).
+
+The launchers are split over several translation units (csrc/*.cu) that
+nvcc compiles in parallel, then one link step produces the shared library."""
 from __future__ import annotations
 
 import os
@@ -8,16 +11,19 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = PKG / "csrc" / "capi.cu"
-DEPS = [SRC, PKG / "csrc" / "kernels.cuh", ROOT / "include" / "mmlttb.h"]
+CSRC = PKG / "csrc"
+SRCS = sorted(CSRC.glob("*.cu"))
+DEPS = [*SRCS, *CSRC.glob("*.cuh"), ROOT / "include" / "mmlttb.h"]
 OUT = PKG / "libmmlttb.so"
+OBJ = PKG / "build"
 
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-fmad=false",  # belt and braces: LTTB already uses explicit __d*_rn ops
-    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-Xcompiler", "-fPIC",
 ]
+LINK_FLAGS = ["-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def nvcc() -> str:
@@ -36,10 +42,18 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     if force or stale():
-        cmd = [nvcc(), *NVCC_FLAGS, "-o", str(OUT), str(SRC)]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+        OBJ.mkdir(exist_ok=True)
+        procs = []
+        for src in SRCS:
+            obj = OBJ / (src.stem + ".o")
+            cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas=-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
+            procs.append((src, obj, subprocess.Popen(cmd)))
+        bad = [str(src) for src, _, p in procs if p.wait() != 0]
+        if bad:
+            raise subprocess.CalledProcessError(1, "nvcc " + " ".join(bad))
+        tmp = OUT.with_suffix(".so.tmp")
+        subprocess.run([nvcc(), *LINK_FLAGS, "-o", str(tmp), *[str(o) for _, o, _ in procs]], check=True)
+        tmp.replace(OUT)
     return OUT
 
 

@@ -3,28 +3,12 @@
 // Each entry validates its O(1) arguments defensively (the Python layer has
 // already raised the reference's exception classes in the reference's order),
 // carves the caller's workspace, and enqueues 1-4 kernels on the caller's
-// stream.  Nothing here synchronises the host.
-#include <cuda_runtime.h>
-#include <stdint.h>
-#include <stdarg.h>
-#include <stdio.h>
-#include <stdlib.h>
-#include <string.h>
-
-#include <algorithm>
-#include <atomic>
-#include <array>
-#include <string>
-#include <vector>
-
-#include "../../include/mmlttb.h"
-#include "kernels.cuh"
-#include "fused.cuh"
+// stream.  Nothing here synchronises the host.  The kernel launchers live in
+// k1_launch.cu / lttb_launch.cu / fused_launch.cu / post_launch.cu (host.cuh).
+#include "host.cuh"
 #include "raster.cuh"
 
-using namespace mm;
-
-namespace {
+namespace mmh {
 
 thread_local std::string g_err;
 
@@ -72,369 +56,6 @@ void stage_mark(cudaStream_t st, int i) {
   if (i == 3) g_timer.calls.push_back(g_timer.cur);
 }
 
-constexpr int64_t ALIGN = 256;
-inline int64_t up(int64_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
-inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
-inline int esize(int dt) { return (dt == MM_F32 || dt == MM_I32) ? 4 : 8; }
-inline bool ydt_ok(int dt) { return dt == MM_F32 || dt == MM_F64; }
-inline bool xdt_ok(int dt) { return dt >= MM_F32 && dt <= MM_I32; }
-
-// workspace bump allocator over the caller's buffer
-struct Carve {
-  char* p;
-  int64_t left;
-  bool ok = true;
-  template <typename T> T* take(int64_t count) {
-    const int64_t bytes = up(count * (int64_t)sizeof(T));
-    if (bytes > left) { ok = false; return nullptr; }
-    T* r = reinterpret_cast<T*>(p);
-    p += bytes;
-    left -= bytes;
-    return r;
-  }
-};
-
-// ---- K1 planning --------------------------------------------------------
-struct ExPlan {
-  int64_t C, chunk, Cmax;
-  int64_t E = 0, Ws = 0, CP = 0;  // flat mode (E > 0): elements/warp, warps/series, partial stride
-};
-
-// Chunks per bucket: enough warps for ~4 waves over 148 SMs x 32 resident
-// warps, never a chunk under MIN_CHUNK elements; buckets of <= 4096 points
-// are one item each (8-lane groups).  Large buckets of closed-form partitions
-// use the flat split (k_extrema_flat): equal element ranges per warp.
-constexpr int64_t SMALL_BUCKET = 4096;  // elements: <= this -> one 8-lane group per bucket
-
-int64_t env_i64(const char* name, int64_t dflt) {
-  const char* e = getenv(name);  // tuning knobs for tools/*.sh only
-  return e ? atoll(e) : dflt;
-}
-
-ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, int64_t B = 0, bool closed_form = false) {
-  // tuned on B200 (tools/plan_sweep.sh): ~4 waves of 148 SMs x 32 resident
-  // warps, chunks of >= 4096 float32 elements
-  static const int64_t want = env_i64("MMLTTB_K1_WANT_WARPS", 148LL * 128);
-  static const int64_t minc32 = env_i64("MMLTTB_K1_MIN_CHUNK", 4096);
-  // flat split: one wave of 148 SMs x 24 resident warps (80 regs), two for
-  // very long series (tools/flat_sweep.sh)
-  static const int64_t flat_env = env_i64("MMLTTB_K1_FLAT_WARPS", -1);
-  const int64_t min_chunk = ydt == MM_F32 ? minc32 : minc32 / 2;
-  ExPlan p;
-  const int64_t nb_ = B > 0 ? buckets_total / B : 0;
-  const int64_t flat_warps = flat_env >= 0 ? flat_env : (nb_ * max_bucket > 400000000LL ? 148LL * 48 : 148LL * 24);
-  if (closed_form && B > 0 && max_bucket > SMALL_BUCKET && flat_warps > 0) {
-    const int64_t nb = nb_;
-    p.Ws = std::max<int64_t>(1, flat_warps / B);
-    p.E = std::max<int64_t>(min_chunk, cdiv(nb * max_bucket, p.Ws));
-    p.Ws = cdiv(nb * max_bucket, p.E);
-    p.CP = cdiv(max_bucket, p.E) + 1;
-    p.C = 1;
-    p.chunk = p.E;
-    p.Cmax = p.CP;
-    return p;
-  }
-  p.Cmax = std::max<int64_t>(1, std::min<int64_t>(256, cdiv(want, std::max<int64_t>(1, buckets_total))));
-  p.C = max_bucket <= SMALL_BUCKET ? 1 : std::max<int64_t>(1, std::min<int64_t>(p.Cmax, cdiv(max_bucket, min_chunk)));
-  p.chunk = cdiv(max_bucket, p.C);
-  return p;
-}
-
-// K1 buffers for nbt = B*nb buckets
-int64_t ex_ws(int64_t nbt, const ExPlan& p) {
-  int64_t b = up(nbt * (int64_t)sizeof(Ext)) + up(nbt);
-  if (p.Cmax > 1) b += up(nbt * p.Cmax * (int64_t)sizeof(Partial)) + up(nbt * 4);
-  return b;
-}
-
-bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
-  a.E = p.E;
-  a.Ws = p.Ws;
-  a.CP = p.CP;
-  a.ext = cv.take<Ext>(nbt);
-  a.cnt8 = cv.take<unsigned char>(nbt);
-  a.part = nullptr;
-  a.arrivals = nullptr;
-  if (p.Cmax > 1) {
-    a.part = cv.take<Partial>(nbt * p.Cmax);
-    a.arrivals = cv.take<unsigned>(nbt);
-  }
-  return cv.ok;
-}
-
-int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
-  if (a.E > 0) {  // flat split
-    if (cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
-      return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
-    const int64_t blocks = cdiv(a.B * a.Ws, 8);
-    static const int64_t fv = env_i64("MMLTTB_K1_FLAT_VARIANT", 0);  // A/B knob (tools/flat_sweep.sh)
-    if (ydt == MM_F32) {
-      switch (fv) {
-        case 1: k_extrema_flat<float, 6, 3, 4><<<(unsigned)blocks, 256, 0, st>>>(a); break;
-        case 2: k_extrema_flat<float, 4, 3, 4><<<(unsigned)blocks, 256, 0, st>>>(a); break;
-        case 3: k_extrema_flat<float, 8, 1, 3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
-        case 4: k_extrema_flat<float, 12, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
-        case 5: k_extrema_flat<float, 16, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
-        default: k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
-      }
-    } else {
-      k_extrema_flat<double, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
-    }
-    return check_launch("k_extrema_flat");
-  }
-  const bool small = a.C == 1 && a.chunk <= SMALL_BUCKET;
-  if (small && a.B * a.nb < 16384) {  // few buckets: a whole warp per bucket fills the GPU better
-    const int64_t blocks = cdiv(a.B * a.nb, 8);
-    if (ydt == MM_F32)
-      k_extrema<float, 8, 3, 1, 32><<<(unsigned)blocks, 256, 0, st>>>(a);
-    else
-      k_extrema<double, 8, 3, 1, 32><<<(unsigned)blocks, 256, 0, st>>>(a);
-    return check_launch("k_extrema(warp/bucket)");
-  }
-  if (small) {
-    const int64_t blocks = cdiv(a.B * a.nb, 8 * 4);
-    if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
-    if (ydt == MM_F32)
-      k_extrema<float, 8, 3, 1, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
-    else
-      k_extrema<double, 8, 3, 1, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
-    return check_launch("k_extrema(small)");
-  }
-  const int64_t warps = a.B * a.nb * a.C;
-  if (a.C > 1 && cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
-    return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
-  const int64_t blocks = cdiv(warps, 8);
-  if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
-  if (a.chunk >= (1LL << 30)) return fail(MM_ERANGE, "bucket chunk too large");
-  static const int variant = [] {
-    const char* e = getenv("MMLTTB_K1_VARIANT");  // tuning knob, default = tuned choice
-    return e ? atoi(e) : 0;
-  }();
-  const unsigned g = (unsigned)blocks;
-#define MM_K1(T, U, L) k_extrema<T, U, L><<<g, 256, 0, st>>>(a)
-#define MM_K1B(T, U, L, MB) k_extrema<T, U, L, MB><<<g, 256, 0, st>>>(a)
-  if (ydt == MM_F32) {
-    switch (variant) {
-      case 1: MM_K1(float, 4, 1); break;
-      case 2: MM_K1(float, 4, 2); break;
-      case 3: MM_K1(float, 4, 3); break;
-      case 4: MM_K1(float, 8, 0); break;
-      case 5: MM_K1(float, 8, 1); break;
-      case 6: MM_K1(float, 8, 3); break;
-      case 7: MM_K1(float, 2, 1); break;
-      case 8: MM_K1B(float, 4, 2, 6); break;
-      case 9: MM_K1B(float, 4, 3, 6); break;
-      case 10: MM_K1B(float, 2, 2, 8); break;
-      case 11: MM_K1B(float, 8, 2, 4); break;
-      case 12: MM_K1(float, 4, 0); break;
-      default: MM_K1(float, 8, 3); break;  // tuned: U=8 vectors in flight, evict-first
-    }
-  } else {
-    switch (variant) {
-      case 1: MM_K1(double, 4, 1); break;
-      case 4: MM_K1(double, 8, 0); break;
-      case 5: MM_K1(double, 8, 1); break;
-      case 12: MM_K1(double, 4, 0); break;
-      default: MM_K1(double, 8, 3); break;
-    }
-  }
-#undef MM_K1
-#undef MM_K1B
-  return check_launch("k_extrema");
-}
-
-bool mul_ok(int64_t a, int64_t b) { return a == 0 || b <= INT64_MAX / a; }
-
-// ---- K3 planning --------------------------------------------------------
-// Buckets of <= 64 points: exact transition tables over all points (K3a).
-// Larger buckets: hull-candidate tables + full verification + repair (K3c).
-constexpr int NBB = 32;   // buckets per k_lttb_tables block
-constexpr int HMAX = 32;  // K3c workspace bound: <= 2 x 16 sampled directions per bucket
-
-int smax_for(int64_t s) {
-  if (s <= 4) return 4;
-  if (s <= 8) return 8;
-  if (s <= 16) return 16;
-  if (s <= 32) return 32;
-  if (s <= 64) return 64;
-  return 0;
-}
-
-constexpr int64_t JUMP_SMEM_MAX = 200 * 1024;
-// buckets per k_lttb_jump shared-memory segment (two byte tables of seg*SMAX)
-int64_t jump_seg(int64_t k3, int smax) {
-  const int64_t cap = (JUMP_SMEM_MAX / (2 * smax)) / 16 * 16;
-  return std::min<int64_t>(cap, (k3 + 15) / 16 * 16);
-}
-
-bool use_tables(int64_t s) { return smax_for(s) > 0; }
-bool use_hull() {
-  static const bool h = env_i64("MMLTTB_K3C_HULL", 0) != 0;  // A/B knob: hull candidates
-  return h;
-}
-bool use_chain() {
-  static const bool c = env_i64("MMLTTB_LTTB_CHAIN", 0) != 0;  // A/B knob: old sequential chain
-  return c;
-}
-
-int64_t tab_ld(int64_t k3, int smax) { return (k3 * smax + 15) / 16 * 16; }
-
-int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s) {
-  const int64_t k3 = n_out - 2;
-  if (use_tables(s)) return up(B * tab_ld(k3, smax_for(s)));
-  if (use_chain()) return up(B * k3 * (int64_t)sizeof(double2));
-  return up(B * k3 * (int64_t)sizeof(double2)) + up(B * k3 * HMAX * 8) + up(B * k3 * 4) + up(B * tab_ld(k3, HMAX)) +
-         up(B * (k3 + 2) * 8) + up(B * k3 * 8) + up(B * k3 * 4) + up(B * k3 * (int64_t)sizeof(double2)) +
-         up(B * k3 * 8) + up(B * k3 * 4) + up(B * 4);
-}
-
-template <int SMAX> int jump_attr() {
-  static bool done = false;
-  if (!done) {
-    if (cudaFuncSetAttribute(k_lttb_jump<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JUMP_SMEM_MAX) != cudaSuccess)
-      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_lttb_jump)");
-    done = true;
-  }
-  return MM_OK;
-}
-
-template <int SMAX>
-int launch_jump(LttbArgs a, cudaStream_t st) {
-  const int64_t k3 = a.n_out - 2;
-  int rc = jump_attr<SMAX>();
-  if (rc) return rc;
-  a.jump_seg = jump_seg(k3, SMAX);
-  k_lttb_jump<SMAX><<<(unsigned)a.B, 1024, (size_t)(2 * a.jump_seg * SMAX), st>>>(a);
-  return check_launch("k_lttb_jump");
-}
-
-template <typename XT, typename YT, int SMAX>
-int launch_tables_jump(LttbArgs a, cudaStream_t st) {
-  const int64_t k3 = a.n_out - 2;
-  a.tab_ld = tab_ld(k3, SMAX);
-  dim3 g((unsigned)cdiv(k3, NBB), (unsigned)a.B);
-  constexpr int NT = NBB * SMAX < 1024 ? NBB * SMAX : 1024;
-  k_lttb_tables<XT, YT, SMAX, NBB><<<g, NT, 0, st>>>(a);
-  int rc = check_launch("k_lttb_tables");
-  if (rc) return rc;
-  if constexpr (SMAX <= 32) {
-    k_lttb_scan<SMAX, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
-    return check_launch("k_lttb_scan");
-  } else {
-    return launch_jump<SMAX>(a, st);
-  }
-}
-
-// K3c: large buckets (see kernels.cuh): means, hull candidates, candidate
-// tables, jump (positions), verification, repair + output
-template <typename XT, typename YT, int H>
-int launch_lttb_large(LttbArgs a, cudaStream_t st) {
-  const int64_t k3 = a.n_out - 2;
-  Carve cv{(char*)a.tables, INT64_MAX / 4};
-  a.means = cv.take<double2>(a.B * k3);
-  a.means_ld = k3;
-  a.cand = cv.take<int64_t>(a.B * k3 * HMAX);
-  a.cand_ld = k3 * H;
-  a.cand_cnt = cv.take<int>(a.B * k3);
-  a.tab_ld = tab_ld(k3, H);
-  unsigned char* tabs = cv.take<unsigned char>(a.B * tab_ld(k3, HMAX));
-  a.pos = cv.take<int64_t>(a.B * (k3 + 2));
-  a.pos_ld = k3 + 2;
-  a.best = cv.take<int64_t>(a.B * k3);
-  a.flag = cv.take<int>(a.B * k3);
-  a.yrange = cv.take<double2>(a.B * k3);
-  a.best2 = cv.take<int64_t>(a.B * k3);
-  a.flist = cv.take<int>(a.B * k3);
-  a.fcount = cv.take<int>(a.B);
-  a.tables = tabs;
-  a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", H);  // test knob: a poor heuristic must still be exact
-  // one warp per bucket, 8 KB of tiles each: every bucket's chain resident at once
-  // loads two tiles ahead (59 vs 64 us on C2); MMLTTB_K3C_MEANS=1: one tile ahead (A/B knob)
-  static const int64_t mv = env_i64("MMLTTB_K3C_MEANS", 0);
-  if (mv == 1) k_lttb_means_staged<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
-  else k_lttb_means_staged2<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
-  int rc = check_launch("k_lttb_means");
-  if (rc) return rc;
-  if (use_hull()) {
-    k_lttb_hull<XT, YT, H><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);
-    if ((rc = check_launch("k_lttb_hull"))) return rc;
-  } else {
-    static const int64_t dnt = env_i64("MMLTTB_K3C_DIRCAND_NT", 64);  // A/B knob (64: 64 vs 68 us at 128 on C2)
-    if (dnt == 32) k_lttb_dircand<XT, YT, H, H / 2, 32><<<dim3((unsigned)k3, (unsigned)a.B), 32, 0, st>>>(a);
-    else if (dnt == 64) k_lttb_dircand<XT, YT, H, H / 2, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
-    else if (dnt == 256) k_lttb_dircand<XT, YT, H, H / 2, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
-    else k_lttb_dircand<XT, YT, H, H / 2, 128><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
-    if ((rc = check_launch("k_lttb_dircand"))) return rc;
-  }
-  k_lttb_ctables<XT, YT, H><<<dim3((unsigned)cdiv(k3, 1024 / H), (unsigned)a.B), 1024, 0, st>>>(a);
-  if ((rc = check_launch("k_lttb_ctables"))) return rc;
-  k_lttb_scan<H, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
-  if ((rc = check_launch("k_lttb_scan"))) return rc;
-  if (cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
-  static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);  // A/B knob (64: 30 vs 37.5 us at 256 on C2)
-  if (vnt == 512) k_lttb_verify<XT, YT, 512><<<dim3((unsigned)k3, (unsigned)a.B), 512, 0, st>>>(a);
-  else if (vnt == 128) k_lttb_verify<XT, YT, 128><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
-  else if (vnt == 64) k_lttb_verify<XT, YT, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
-  else if (vnt == 32) k_lttb_verify<XT, YT, 32><<<dim3((unsigned)k3, (unsigned)a.B), 32, 0, st>>>(a);
-  else k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
-  if ((rc = check_launch("k_lttb_verify"))) return rc;
-  static const int64_t v2 = env_i64("MMLTTB_K3C_VERIFY2_NT", 256);  // A/B knob
-  if (v2 == 64) k_lttb_verify2<XT, YT, 64><<<dim3(148, (unsigned)a.B), 64, 0, st>>>(a);
-  else if (v2 == 128) k_lttb_verify2<XT, YT, 128><<<dim3(148, (unsigned)a.B), 128, 0, st>>>(a);
-  else k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
-  if ((rc = check_launch("k_lttb_verify2"))) return rc;
-  static const int64_t rp = env_i64("MMLTTB_K3C_REPAIR_NT", 512);  // A/B knob (512: 22.1 vs 24.4 us at 1024 on C2)
-  if (rp == 256) k_lttb_repair<XT, YT, 256><<<(unsigned)a.B, 256, 0, st>>>(a);
-  else if (rp == 512) k_lttb_repair<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
-  else k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
-  return check_launch("k_lttb_repair");
-}
-
-template <typename XT, typename YT>
-int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
-  const int64_t k3 = a.n_out - 2;
-  if (a.B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
-  if (use_tables(s)) {
-    switch (smax_for(s)) {
-      case 4: return launch_tables_jump<XT, YT, 4>(a, st);
-      case 8: return launch_tables_jump<XT, YT, 8>(a, st);
-      case 16: return launch_tables_jump<XT, YT, 16>(a, st);
-      case 32: return launch_tables_jump<XT, YT, 32>(a, st);
-      default: return launch_tables_jump<XT, YT, 64>(a, st);
-    }
-  }
-  if (!use_chain()) {
-    static const int64_t h = env_i64("MMLTTB_K3C_HMAX", 16);  // A/B knob: 16 or 32 candidates
-    return h == 32 ? launch_lttb_large<XT, YT, 32>(a, st) : launch_lttb_large<XT, YT, 16>(a, st);
-  }
-  a.means = reinterpret_cast<double2*>(a.tables);
-  a.means_ld = k3;
-  const int64_t n = a.B * k3;
-  k_lttb_means<XT, YT><<<(unsigned)cdiv(n, 128), 128, 0, st>>>(a);
-  int rc = check_launch("k_lttb_means");
-  if (rc) return rc;
-  k_lttb_chain<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
-  return check_launch("k_lttb_chain");
-}
-
-template <typename XT>
-int launch_lttb_x(LttbArgs a, int ydt, int64_t s, cudaStream_t st) {
-  if (ydt == MM_F32) return launch_lttb_t<XT, float>(a, s, st);
-  if (ydt == MM_F64) return launch_lttb_t<XT, double>(a, s, st);
-  return fail(MM_EINVAL, "y dtype");
-}
-
-// a.tables must point at lttb_ws(B, n_out, s) bytes of workspace
-int launch_lttb(LttbArgs a, int xdt, int ydt, int64_t s, cudaStream_t st) {
-  switch (xdt) {
-    case MM_F32: return launch_lttb_x<float>(a, ydt, s, st);
-    case MM_F64: return launch_lttb_x<double>(a, ydt, s, st);
-    case MM_I64: return launch_lttb_x<long long>(a, ydt, s, st);
-    case MM_I32: return launch_lttb_x<int>(a, ydt, s, st);
-  }
-  return fail(MM_EINVAL, "x dtype");
-}
-
 // ---- shared pieces of the fused entries ----------------------------------
 // sizes for minmaxlttb / preselect on B series
 int64_t preselect_ws(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt, bool with_lttb) {
@@ -447,7 +68,6 @@ int64_t preselect_ws(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt,
   return bytes;
 }
 
-constexpr int PAIR_NT = 128, PAIR_ITEMS = 2;
 
 template <typename XT, typename YT>
 void pairs_t(const PairArgs& pa, dim3 g, cudaStream_t st) {
@@ -474,247 +94,12 @@ int launch_pairs(PairArgs pa, int64_t B, cudaStream_t st) {
   return check_launch("k_compact_pairs");
 }
 
-// ---- fused per-series path (batches of medium series) --------------------
-constexpr int64_t FUSED_SMEM_MAX = 110 * 1024;
-constexpr int64_t FUSED_MIN_B = 148;
-
-bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt) {
-  static const bool off = env_i64("MMLTTB_NO_FUSED", 0) != 0;  // A/B knob
-  const int64_t k = (n_out - 2) * (r_ps / 2);
-  return !off && B >= FUSED_MIN_B && r_ps >= 2 && r_ps <= 8 && N < (1LL << 31) &&
-         fused_smem(k, n_out - 2, 8, esize(ydt)) <= FUSED_SMEM_MAX;
-}
-
-template <typename XT, typename YT, int SMAX, int NT, int MINB, int U, int LDV = 3, bool KR = true>
-int launch_fused_v(const FusedArgs& fa, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U, LDV, KR>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_MAX) != cudaSuccess)
-      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_mmlttb_fused)");
-    attr = true;
-  }
-  const int64_t k = (fa.n_out - 2) * (fa.r_ps / 2);
-  const size_t smem = (size_t)fused_smem(k, fa.n_out - 2, SMAX, (int)sizeof(YT));
-  k_mmlttb_fused<XT, YT, SMAX, NT, MINB, U, LDV, KR><<<(unsigned)fa.B, NT, smem, st>>>(fa);
-  return check_launch("k_mmlttb_fused");
-}
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-  }
-  return n;
-}
-
-// TMA-fed persistent fused kernel (fused.cuh): ring of `stages` slots of
-// ~MMLTTB_TMA_TILE bytes (whole sub-buckets per slot).  Returns 1 (not
-// launched) when the rows are not 16-byte aligned or no CTA fits.
-template <typename XT, typename YT, int SMAX, int NT, int MINB, int G>
-int launch_fused_tma_v(FusedArgs fa, cudaStream_t st) {
-  static const int64_t tile_target = env_i64("MMLTTB_TMA_TILE", 65536);
-  static const int64_t stages = std::min<int64_t>(8, std::max<int64_t>(2, env_i64("MMLTTB_TMA_STAGES", 2)));
-  constexpr int64_t ys = sizeof(YT);
-  if (((uintptr_t)fa.y & 15) || (fa.B > 1 && (fa.y_ld * ys) & 15)) return 1;
-  const int64_t k = (fa.n_out - 2) * (fa.r_ps / 2);
-  const int64_t maxlen = cdiv(fa.N - 2, k) + 1;
-  constexpr int64_t R = NT / G;  // tile = whole multiples of R sub-buckets (one per lane group per round)
-  const int64_t tb = std::max<int64_t>(1, std::min<int64_t>(cdiv(k, R), tile_target / (maxlen * ys * R))) * R;
-  fa.tile_buckets = tb;
-  fa.tile_bytes = cdiv(tb * maxlen * ys + 256, 128) * 128;  // + line widening at both ends
-  fa.stages = stages;
-  fa.dbg = env_i64("MMLTTB_TMA_DEBUG", 0);
-  const int64_t p_bytes = cdiv(fused_smem(k, fa.n_out - 2, SMAX, (int)ys), 128) * 128;
-  const int64_t smem = p_bytes + stages * fa.tile_bytes;
-  constexpr int64_t SMEM_CAP = 227 * 1024 - 2048;  // opt-in max minus static shared memory
-  if (smem > SMEM_CAP) return 1;
-  auto kern = k_mmlttb_fused_tma<XT, YT, SMAX, NT, MINB, G>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CAP) != cudaSuccess)
-      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_mmlttb_fused_tma)");
-    attr = true;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, (size_t)smem) != cudaSuccess || per_sm < 1)
-    return 1;
-  const int64_t grid = std::min<int64_t>(fa.B, (int64_t)per_sm * sm_count());
-  kern<<<(unsigned)grid, NT, (size_t)smem, st>>>(fa);
-  return check_launch("k_mmlttb_fused_tma");
-}
-
-template <typename XT, typename YT, int SMAX>
-int launch_fused_t(const FusedArgs& fa, cudaStream_t st) {
-  // opt-in (>= 0): the TMA-fed persistent kernel -- streams at 7.4 TB/s on
-  // its own but its phase-1 math is latency-bound at the 8 warps that fit
-  // beside the ring on C4, so the per-group kernel stays the default
-  static const int64_t tv = env_i64("MMLTTB_TMA_VARIANT", -1);
-  if (tv >= 0) {
-    int rc;
-    switch (tv) {
-      case 1: rc = launch_fused_tma_v<XT, YT, SMAX, 512, 1, 16>(fa, st); break;
-      case 2: rc = launch_fused_tma_v<XT, YT, SMAX, 256, 1, 16>(fa, st); break;
-      case 3: rc = launch_fused_tma_v<XT, YT, SMAX, 256, 1, 32>(fa, st); break;
-      case 4: rc = launch_fused_tma_v<XT, YT, SMAX, 512, 1, 32>(fa, st); break;
-      case 5: rc = launch_fused_tma_v<XT, YT, SMAX, 256, 2, 8>(fa, st); break;
-      default: rc = launch_fused_tma_v<XT, YT, SMAX, 256, 1, 8>(fa, st); break;
-    }
-    if (rc != 1) return rc;
-  }
-  static const int64_t v = env_i64("MMLTTB_FUSED_VARIANT", 0);  // tuning knob (tools/)
-  switch (v) {  // tools/fused_sweep.sh on B200 (variant 0 = default)
-    case 1: return launch_fused_v<XT, YT, SMAX, 512, 2, 4>(fa, st);
-    case 2: return launch_fused_v<XT, YT, SMAX, 384, 3, 4>(fa, st);
-    case 3: return launch_fused_v<XT, YT, SMAX, 256, 4, 4>(fa, st);
-    case 4: return launch_fused_v<XT, YT, SMAX, 512, 3, 2>(fa, st);
-    case 5: return launch_fused_v<XT, YT, SMAX, 512, 2, 8>(fa, st);
-    case 6: return launch_fused_v<XT, YT, SMAX, 512, 3, 4, 2, false>(fa, st);
-    case 7: return launch_fused_v<XT, YT, SMAX, 512, 2, 8, 2, true>(fa, st);
-    case 8: return launch_fused_v<XT, YT, SMAX, 384, 3, 8, 2, false>(fa, st);
-    // measured best on C4: normal-policy loads, winners re-read from L1/L2
-    default: return launch_fused_v<XT, YT, SMAX, 512, 2, 8, 2, false>(fa, st);
-  }
-}
-
-template <typename XT, typename YT>
-int launch_fused_y(const FusedArgs& fa, cudaStream_t st) {
-  return fa.r_ps <= 4 ? launch_fused_t<XT, YT, 4>(fa, st) : launch_fused_t<XT, YT, 8>(fa, st);
-}
-
-template <typename XT>
-int launch_fused_x(const FusedArgs& fa, int ydt, cudaStream_t st) {
-  return ydt == MM_F32 ? launch_fused_y<XT, float>(fa, st) : launch_fused_y<XT, double>(fa, st);
-}
-
-int launch_fused(const FusedArgs& fa, int xdt, int ydt, cudaStream_t st) {
-  switch (xdt) {
-    case MM_F32: return launch_fused_x<float>(fa, ydt, st);
-    case MM_F64: return launch_fused_x<double>(fa, ydt, st);
-    case MM_I64: return launch_fused_x<long long>(fa, ydt, st);
-    default: return launch_fused_x<int>(fa, ydt, st);
-  }
-}
-
 // First 256 bytes of every fused entry's workspace: status word (bit 0 =
 // non-finite y seen), zeroed on the stream at entry.
 int* take_status(Carve& cv, cudaStream_t st) {
   int* p = cv.take<int>(1);
   if (p && cudaMemsetAsync(p, 0, sizeof(int), st) != cudaSuccess) return nullptr;
   return p;
-}
-
-// ---- fused K2+K3 (single / few series) -----------------------------------
-constexpr int64_t POST_SMEM_MAX = 100 * 1024;
-constexpr int64_t POST_SMEM2_MAX = 200 * 1024;
-
-bool post_ok(int64_t k, int64_t n_out, int64_t r_ps) {
-  static const bool off = env_i64("MMLTTB_NO_POST_FUSED", 0) != 0;  // A/B knob
-  // one CTA's latency chains beat two extra launches only for small k
-  // (measured: k = 1996 24 us vs 24 us + a launch; k = 3996 41 us vs 24 us;
-  // with the set staged in shared memory, k_post_smem, C1 takes 14.6 us)
-  return !off && k <= 2048 && smax_for(r_ps) > 0 && smax_for(r_ps) <= 8 &&
-         post_smem(n_out - 2, smax_for(r_ps)) <= POST_SMEM_MAX;
-}
-
-template <typename XT, typename YT, int SMAX>
-int launch_post_t(const PostArgs& pa, int64_t B, cudaStream_t st) {
-  static const bool global_staging = env_i64("MMLTTB_POST_GLOBAL", 0) != 0;  // A/B knob
-  const int64_t sm2 = post_smem2(pa.n_out - 2, SMAX, pa.cap);
-  if (!global_staging && sm2 <= POST_SMEM2_MAX) {  // preselected set staged in shared memory
-    static bool attr2 = false;
-    if (!attr2) {
-      if (cudaFuncSetAttribute(k_post_smem<XT, YT, SMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)POST_SMEM2_MAX) != cudaSuccess)
-        return fail(MM_ECUDA, "cudaFuncSetAttribute(k_post_smem)");
-      attr2 = true;
-    }
-    k_post_smem<XT, YT, SMAX, 1024><<<(unsigned)B, 1024, (size_t)sm2, st>>>(pa);
-    return check_launch("k_post_smem");
-  }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_post_fused<XT, YT, SMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)POST_SMEM_MAX) != cudaSuccess)
-      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_post_fused)");
-    attr = true;
-  }
-  k_post_fused<XT, YT, SMAX, 1024><<<(unsigned)B, 1024, (size_t)post_smem(pa.n_out - 2, SMAX), st>>>(pa);
-  return check_launch("k_post_fused");
-}
-
-template <typename XT, typename YT>
-int launch_post_y(const PostArgs& pa, int64_t B, int smax, cudaStream_t st) {
-  return smax <= 4 ? launch_post_t<XT, YT, 4>(pa, B, st) : launch_post_t<XT, YT, 8>(pa, B, st);
-}
-
-int launch_post(const PostArgs& pa, int64_t B, int xdt, int ydt, int smax, cudaStream_t st) {
-  const bool y32 = ydt == MM_F32;
-  switch (xdt) {
-    case MM_F32: return y32 ? launch_post_y<float, float>(pa, B, smax, st) : launch_post_y<float, double>(pa, B, smax, st);
-    case MM_F64: return y32 ? launch_post_y<double, float>(pa, B, smax, st) : launch_post_y<double, double>(pa, B, smax, st);
-    case MM_I64:
-      return y32 ? launch_post_y<long long, float>(pa, B, smax, st) : launch_post_y<long long, double>(pa, B, smax, st);
-    default: return y32 ? launch_post_y<int, float>(pa, B, smax, st) : launch_post_y<int, double>(pa, B, smax, st);
-  }
-}
-
-// ---- cooperative K2+K3a ----------------------------------------------------
-template <typename XT, typename YT, int SMAX>
-int launch_coop_t(PairArgs pa, LttbArgs la, int64_t B, cudaStream_t st, bool* launched) {
-  constexpr int NT = PAIR_NT, IT = PAIR_ITEMS;
-  auto fn = k_post_coop<XT, YT, SMAX, NT, IT>;
-  static int cap = -1;
-  if (cap < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, NT, 0);
-    cap = sms * per;
-  }
-  int64_t ntiles = std::max<int64_t>(1, cdiv(pa.nb, NT * IT));
-  if (ntiles * B > cap || B > 65535) { *launched = false; return MM_OK; }
-  *launched = true;
-  la.tab_ld = tab_ld(la.n_out - 2, SMAX);
-  void* args[] = {(void*)&pa, (void*)&la, (void*)&ntiles};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)ntiles, (unsigned)B), dim3(NT),
-                                                    args, 0, st);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (e != cudaSuccess) return fail(MM_ECUDA, "k_post_coop: %s", cudaGetErrorString(e));
-  return MM_OK;
-}
-
-template <typename XT, typename YT>
-int launch_coop_y(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched) {
-  return smax <= 4 ? launch_coop_t<XT, YT, 4>(pa, la, B, st, launched)
-                   : launch_coop_t<XT, YT, 8>(pa, la, B, st, launched);
-}
-
-// Try the cooperative K2+K3a; *launched = false when it does not apply.
-int launch_coop(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched) {
-  // opt-in (MMLTTB_COOP=1): measured neutral-to-slower than the separate
-  // launches on B200 (c3_1e9 28 vs 26 us, c3 1e8 27 vs 24 us) -- the fixed
-  // cost is the phases' dependent memory round trips, not the launches
-  static const bool on = env_i64("MMLTTB_COOP", 0) != 0;
-  *launched = false;
-  if (!on || smax <= 0 || smax > 8) return MM_OK;
-  const bool y32 = pa.ydt == MM_F32;
-  switch (pa.xdt) {
-    case MM_F32:
-      return y32 ? launch_coop_y<float, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<float, double>(pa, la, B, smax, st, launched);
-    case MM_F64:
-      return y32 ? launch_coop_y<double, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<double, double>(pa, la, B, smax, st, launched);
-    case MM_I64:
-      return y32 ? launch_coop_y<long long, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<long long, double>(pa, la, B, smax, st, launched);
-    default:
-      return y32 ? launch_coop_y<int, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<int, double>(pa, la, B, smax, st, launched);
-  }
 }
 
 int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
@@ -725,7 +110,8 @@ int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
   return MM_OK;
 }
 
-}  // namespace
+}  // namespace mmh
+
 
 extern "C" {
 
@@ -734,9 +120,7 @@ int mmlttb_version(void) { return 1; }
 int64_t mmlttb_launch_count(void) { return g_launches.load(); }
 
 int64_t mmlttb_repair_scans(void) {
-  unsigned long long v = 0;
-  if (cudaMemcpyFromSymbol(&v, g_repair_scans, sizeof v) != cudaSuccess) return -1;
-  return (int64_t)v;
+  return repair_scans_read();
 }
 
 int mmlttb_stage_timer(int enable) {

@@ -1,0 +1,164 @@
+// host.cuh -- host-side helpers shared by the translation units behind
+// include/mmlttb.h (capi.cu: the extern "C" entries; k1_launch.cu,
+// lttb_launch.cu, fused_launch.cu, post_launch.cu: the kernel launchers,
+// compiled in parallel).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <array>
+#include <string>
+#include <vector>
+
+#include "../../include/mmlttb.h"
+#include "kernels.cuh"
+#include "fused.cuh"
+
+using namespace mm;
+
+namespace mmh {
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+extern std::atomic<int64_t> g_launches;
+int check_launch(const char* what);
+void stage_mark(cudaStream_t st, int i);
+
+constexpr int64_t ALIGN = 256;
+inline int64_t up(int64_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int esize(int dt) { return (dt == MM_F32 || dt == MM_I32) ? 4 : 8; }
+inline bool ydt_ok(int dt) { return dt == MM_F32 || dt == MM_F64; }
+inline bool xdt_ok(int dt) { return dt >= MM_F32 && dt <= MM_I32; }
+
+// workspace bump allocator over the caller's buffer
+struct Carve {
+  char* p;
+  int64_t left;
+  bool ok = true;
+  template <typename T> T* take(int64_t count) {
+    const int64_t bytes = up(count * (int64_t)sizeof(T));
+    if (bytes > left) { ok = false; return nullptr; }
+    T* r = reinterpret_cast<T*>(p);
+    p += bytes;
+    left -= bytes;
+    return r;
+  }
+};
+
+// ---- K1 planning --------------------------------------------------------
+struct ExPlan {
+  int64_t C, chunk, Cmax;
+  int64_t E = 0, Ws = 0, CP = 0;  // flat mode (E > 0): elements/warp, warps/series, partial stride
+};
+
+// Chunks per bucket: enough warps for ~4 waves over 148 SMs x 32 resident
+// warps, never a chunk under MIN_CHUNK elements; buckets of <= 4096 points
+// are one item each (8-lane groups).  Large buckets of closed-form partitions
+// use the flat split (k_extrema_flat): equal element ranges per warp.
+constexpr int64_t SMALL_BUCKET = 4096;  // elements: <= this -> one 8-lane group per bucket
+
+inline int64_t env_i64(const char* name, int64_t dflt) {
+  const char* e = getenv(name);  // tuning knobs for tools/*.sh only
+  return e ? atoll(e) : dflt;
+}
+
+inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, int64_t B = 0, bool closed_form = false) {
+  // tuned on B200 (tools/plan_sweep.sh): ~4 waves of 148 SMs x 32 resident
+  // warps, chunks of >= 4096 float32 elements
+  static const int64_t want = env_i64("MMLTTB_K1_WANT_WARPS", 148LL * 128);
+  static const int64_t minc32 = env_i64("MMLTTB_K1_MIN_CHUNK", 4096);
+  // flat split: one wave of 148 SMs x 24 resident warps (80 regs), two for
+  // very long series (tools/flat_sweep.sh)
+  static const int64_t flat_env = env_i64("MMLTTB_K1_FLAT_WARPS", -1);
+  const int64_t min_chunk = ydt == MM_F32 ? minc32 : minc32 / 2;
+  ExPlan p;
+  const int64_t nb_ = B > 0 ? buckets_total / B : 0;
+  const int64_t flat_warps = flat_env >= 0 ? flat_env : (nb_ * max_bucket > 400000000LL ? 148LL * 48 : 148LL * 24);
+  if (closed_form && B > 0 && max_bucket > SMALL_BUCKET && flat_warps > 0) {
+    const int64_t nb = nb_;
+    p.Ws = std::max<int64_t>(1, flat_warps / B);
+    p.E = std::max<int64_t>(min_chunk, cdiv(nb * max_bucket, p.Ws));
+    p.Ws = cdiv(nb * max_bucket, p.E);
+    p.CP = cdiv(max_bucket, p.E) + 1;
+    p.C = 1;
+    p.chunk = p.E;
+    p.Cmax = p.CP;
+    return p;
+  }
+  p.Cmax = std::max<int64_t>(1, std::min<int64_t>(256, cdiv(want, std::max<int64_t>(1, buckets_total))));
+  p.C = max_bucket <= SMALL_BUCKET ? 1 : std::max<int64_t>(1, std::min<int64_t>(p.Cmax, cdiv(max_bucket, min_chunk)));
+  p.chunk = cdiv(max_bucket, p.C);
+  return p;
+}
+
+// K1 buffers for nbt = B*nb buckets
+inline int64_t ex_ws(int64_t nbt, const ExPlan& p) {
+  int64_t b = up(nbt * (int64_t)sizeof(Ext)) + up(nbt);
+  if (p.Cmax > 1) b += up(nbt * p.Cmax * (int64_t)sizeof(Partial)) + up(nbt * 4);
+  return b;
+}
+
+inline bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
+  a.E = p.E;
+  a.Ws = p.Ws;
+  a.CP = p.CP;
+  a.ext = cv.take<Ext>(nbt);
+  a.cnt8 = cv.take<unsigned char>(nbt);
+  a.part = nullptr;
+  a.arrivals = nullptr;
+  if (p.Cmax > 1) {
+    a.part = cv.take<Partial>(nbt * p.Cmax);
+    a.arrivals = cv.take<unsigned>(nbt);
+  }
+  return cv.ok;
+}
+
+
+inline bool mul_ok(int64_t a, int64_t b) { return a == 0 || b <= INT64_MAX / a; }
+
+// ---- K1 (k1_launch.cu) ----
+int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st);
+
+// ---- K3 (lttb_launch.cu) ----
+// Buckets of <= 64 points: exact transition tables over all points (K3a).
+// Larger buckets: candidate tables + full verification + repair (K3c).
+constexpr int NBB = 32;   // buckets per k_lttb_tables block
+constexpr int HMAX = 32;  // K3c workspace bound: <= 2 x 16 sampled directions per bucket
+inline int smax_for(int64_t s) {
+  if (s <= 4) return 4;
+  if (s <= 8) return 8;
+  if (s <= 16) return 16;
+  if (s <= 32) return 32;
+  if (s <= 64) return 64;
+  return 0;
+}
+inline bool use_tables(int64_t s) { return smax_for(s) > 0; }
+inline int64_t tab_ld(int64_t k3, int smax) { return (k3 * smax + 15) / 16 * 16; }
+// K3c flat passes (B == 1): one wave of warps, partial slots per bucket
+constexpr int64_t K3C_FLAT_WARPS = 148 * 24;
+constexpr int64_t K3C_FLAT_PART = 256;  // bytes per (bucket, warp) partial, >= every pass's partial
+inline int64_t flat_cp_max(int64_t k3) { return (K3C_FLAT_WARPS * 65 / 64 + k3 - 1) / k3 + 3; }
+int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s);
+int launch_lttb(LttbArgs a, int xdt, int ydt, int64_t s, cudaStream_t st);
+int64_t repair_scans_read();
+
+// ---- fused batch kernel (fused_launch.cu) ----
+bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt);
+int launch_fused(const FusedArgs& fa, int xdt, int ydt, cudaStream_t st);
+int sm_count();
+
+// ---- K2 + K3 single-CTA / cooperative (post_launch.cu) ----
+constexpr int PAIR_NT = 128, PAIR_ITEMS = 2;
+bool post_ok(int64_t k, int64_t n_out, int64_t r_ps);
+int launch_post(const PostArgs& pa, int64_t B, int xdt, int ydt, int smax, cudaStream_t st);
+int launch_coop(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched);
+
+}  // namespace mmh
+
+using namespace mmh;

@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(NT) k_compact(CompactArgs a) {
 }
 
 // extrema-only finalize for the _extrema_by_bucket entry point
-__global__ void k_finalize_extrema(const Ext* ext, int64_t k, int64_t* out_min, int64_t* out_max) {
+static __global__ void k_finalize_extrema(const Ext* ext, int64_t k, int64_t* out_min, int64_t* out_max) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= k) return;
   out_min[b] = ext[b].imin;
@@ -656,6 +656,32 @@ __global__ void __launch_bounds__(NT) k_compact_pairs(PairArgs a) {
 // -------------------------------------------------------------- LTTB -----
 // Points of series s: x/y typed (XT/YT), count m (device per series or
 // fixed), optional map position -> output index (the preselected indices).
+// K3c: a bucket whose x values a closed formula reproduces bit-exactly (an
+// arange, or evenly spaced timestamps): later passes compute x_j instead of
+// loading it (half the bytes per point)
+struct XAff {
+  double x0, d;         // float x: x_j = fl(x0 + fl((j - lo) * d))
+  long long x0i, di;    // integer x: x_j = (double)(x0i + (j - lo) * di), two's complement
+  int ok, pad;
+};
+
+template <typename XT> struct XForm {
+  static constexpr bool integral = false;
+  __device__ __forceinline__ static double at(const XAff& f, int64_t t) { return __dadd_rn(f.x0, __dmul_rn((double)t, f.d)); }
+};
+template <> struct XForm<long long> {
+  static constexpr bool integral = true;
+  __device__ __forceinline__ static double at(const XAff& f, int64_t t) {
+    return __ll2double_rn((long long)((unsigned long long)f.x0i + (unsigned long long)t * (unsigned long long)f.di));
+  }
+};
+template <> struct XForm<int> {
+  static constexpr bool integral = true;
+  __device__ __forceinline__ static double at(const XAff& f, int64_t t) {
+    return __ll2double_rn((long long)((unsigned long long)f.x0i + (unsigned long long)t * (unsigned long long)f.di));
+  }
+};
+
 struct LttbArgs {
   const void* x; int64_t x_ld;
   const void* y; int64_t y_ld;
@@ -677,12 +703,68 @@ struct LttbArgs {
   int* flist; int* fcount;                // [B][k3] flagged buckets (unordered), [B] their count (zeroed)
   int cand_cap;                           // <= HMAX (tests lower it to force repairs)
   double2* yrange;                        // [B][k3] per-bucket (ymin, ymax) (K3c candidates)
+  double2* merr;                          // [B][k3] K3c: |exact - approx| bound of means[b] ((0,0): exact), or null
+  int cert_force;                         // test knob: treat every non-exact certification as failed
+  XAff* xaff;                             // [B][k3] K3c affine-x buckets, or null
+  double2* xrange;                        // [B][k3] K3c flat passes: per-bucket (xmin, xmax)
 };
 
 __device__ __forceinline__ double lttb_area(double ax, double ay, double cx, double cy, double xj, double yj) {
   // _kernels.py:114: abs((ax - cx) * (ys[j] - ay) - (ax - xs[j]) * (cy - ay)), every op rounded
   return fabs(__dsub_rn(__dmul_rn(__dsub_rn(ax, cx), __dsub_rn(yj, ay)),
                         __dmul_rn(__dsub_rn(ax, xj), __dsub_rn(cy, ay))));
+}
+
+// XU-free element arithmetic for the flat passes.  On B200 the fp64 compares
+// (DSETP, behind fmin/fmax and `>` on doubles) and the int64 -> f64 / f64 ->
+// f32 conversions issue on the narrow XU pipe, which ncu showed saturated
+// (109 %) in a first version of these passes while the fp64 pipe idled.
+// Maxima are taken on integer keys instead, and conversions use ALU bit tricks.
+// order-preserving int64 key of a double (IEEE total order; the map is an involution)
+__device__ __forceinline__ long long dkey(double v) {
+  const long long b = __double_as_longlong(v);
+  return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
+}
+__device__ __forceinline__ double dkey_inv(long long k) { return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffLL)); }
+// exact int64 -> f64 for |x| < 2^51: 1.5 * 2^52 + x has x in its low mantissa bits
+__device__ __forceinline__ double i2d_magic(long long x) {
+  return __dsub_rn(__longlong_as_double(x + 0x4338000000000000LL), 6755399441055744.0);
+}
+__device__ __forceinline__ bool i2d_magic_ok(long long x) { return (unsigned long long)(x + (1LL << 51)) < (1ULL << 52); }
+// element -> f64 exactly as to_f64 (numpy's conversion)
+template <typename T> __device__ __forceinline__ double elem_f64(T v) { return (double)v; }
+template <> __device__ __forceinline__ double elem_f64<long long>(long long v) {
+  return i2d_magic_ok(v) ? i2d_magic(v) : __ll2double_rn(v);
+}
+template <> __device__ __forceinline__ double elem_f64<int>(int v) { return i2d_magic((long long)v); }
+// f64 -> f32 by truncation (candidate heuristic only): sign, rebased exponent,
+// top 23 mantissa bits; underflow -> +-0, overflow -> +-FLT_MAX
+__device__ __forceinline__ float d2f_trunc(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(b >> 32);
+  const int e = (int)((hi >> 20) & 0x7ff) - 1023 + 127;
+  const unsigned sg = hi & 0x80000000u;
+  unsigned r = sg | ((unsigned)e << 23) | (unsigned)((b >> 29) & 0x7fffff);
+  r = e <= 0 ? sg : r;
+  r = e >= 255 ? (sg | 0x7f7fffffu) : r;
+  return __uint_as_float(r);
+}
+// |T| as a non-negative key; NaN -> -1 (never wins, like the reference's `>`)
+__device__ __forceinline__ long long area_key(double t, int& bad) {
+  long long k = __double_as_longlong(t) & 0x7fffffffffffffffLL;
+  if (k >= 0x7ff0000000000000LL) bad = 1;  // inf or NaN: no certification
+  return k > 0x7ff0000000000000LL ? -1LL : k;
+}
+
+struct VPart { long long k1, k2, i1; int bad, pad; };
+
+__device__ __forceinline__ void vpart_merge(long long& k1, long long& i1, long long& k2, int& bad, long long o1,
+                                            long long oi, long long o2, int ob) {
+  const bool take = o1 > k1 || (o1 == k1 && oi < i1);
+  const long long lose = take ? k1 : o1;
+  k2 = max(max(k2, o2), lose);
+  if (take) { k1 = o1; i1 = oi; }
+  bad |= ob;
 }
 
 __device__ __forceinline__ int64_t lbound(const LttbArgs& a, int64_t m, int64_t b) {
@@ -1425,20 +1507,31 @@ __global__ void __launch_bounds__(NT) k_lttb_dircand(LttbArgs a) {
   int imax[D], imin[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) { vmax[k] = -INFINITY; vmin[k] = INFINITY; imax[k] = INT_MAX; imin[k] = INT_MAX; }
+  // affine-x bucket: X = x_j - x_lo from the index alone (y is the only stream).
+  // Conversions avoid the XU pipe (float counter, d2f_trunc): a heuristic, any
+  // consistent X, Y works (verify/repair make the result exact)
+  const bool aff = a.xaff && a.xaff[s * k3 + b].ok;
+  const float fxf = aff ? (float)(XForm<XT>::integral ? (double)a.xaff[s * k3 + b].di : a.xaff[s * k3 + b].d) : 0.f;
+  const double xrd = elem_f64(xr);
+  const float yrf = (float)yr;
   constexpr int UN = K3C_UN_DIR;
-  for (int64_t j0 = blo + threadIdx.x; j0 < bhi; j0 += NT * UN) {
+  float of = (float)threadIdx.x;  // running offset from blo (exact below 2^24)
+  for (int64_t j0 = blo + threadIdx.x; j0 < bhi; j0 += NT * UN, of += (float)(NT * UN)) {
     XT rx[UN];
     YT ry[UN];
 #pragma unroll
     for (int u = 0; u < UN; ++u) {  // UN points' loads in flight before any use
       const int64_t j = j0 + NT * u < bhi ? j0 + NT * u : blo;
-      rx[u] = xs[j];
+      if (!aff) rx[u] = xs[j];
       ry[u] = ys[j];
     }
 #pragma unroll
     for (int u = 0; u < UN; ++u) {
       if (j0 + NT * u < bhi) {
-        const float X = (float)(rx[u] - xr), Y = (float)((double)ry[u] - yr);
+        const float X = aff ? (of + (float)(NT * u)) * fxf : d2f_trunc(__dsub_rn(elem_f64(rx[u]), xrd));
+        float Y;
+        if constexpr (sizeof(YT) == 4) Y = __fsub_rn((float)ry[u], yrf);
+        else Y = d2f_trunc(__dsub_rn((double)ry[u], yr));
         const int o = (int)(j0 + NT * u - blo);
 #pragma unroll
         for (int k = 0; k < D; ++k) {
@@ -1542,45 +1635,56 @@ __global__ void __launch_bounds__(1024) k_lttb_ctables(LttbArgs a) {
 // block argmax of the exact area over [lo, hi) given anchor (ax, ay) and mean c
 template <typename XT, typename YT, int NT>
 __device__ __forceinline__ int64_t block_bucket_argmax(const XT* xs, const YT* ys, int64_t lo, int64_t hi, double ax,
-                                                       double ay, double2 c, double* s_a, long long* s_i) {
+                                                       double ay, double2 c, double* s_a, long long* s_i,
+                                                       const XAff* xa = nullptr) {
+  // argmax on integer keys of |area| (NaN -> -1, never wins): no fp64
+  // compares, which issue on B200's narrow XU pipe
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double bestv = -1.0;
+  long long bk = -1;
   long long bi = LLONG_MAX;
   constexpr int UN = K3C_UN_VER;
+  const bool aff = xa && xa->ok;
+  XAff f;
+  if (aff) f = *xa;
+  const double P = __dsub_rn(ax, c.x), S = __dsub_rn(c.y, ay);
   for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += (int64_t)NT * UN) {
     XT rx[UN];
     YT ry[UN];
 #pragma unroll
     for (int u = 0; u < UN; ++u) {  // loads in flight before the area math
       const int64_t j = j0 + (int64_t)NT * u < hi ? j0 + (int64_t)NT * u : lo;
-      rx[u] = xs[j];
+      if (!aff) rx[u] = xs[j];
       ry[u] = ys[j];
     }
 #pragma unroll
     for (int u = 0; u < UN; ++u) {
       const int64_t j = j0 + (int64_t)NT * u;
       if (j < hi) {
-        const double ar = lttb_area(ax, ay, c.x, c.y, (double)rx[u], (double)ry[u]);
-        if (ar > bestv) { bestv = ar; bi = j; }
+        const double xj = aff ? XForm<XT>::at(f, j - lo) : elem_f64(rx[u]);
+        // lttb_area: abs((ax - cx) * (y_j - ay) - (ax - x_j) * (cy - ay)), same op order
+        const double t = __dsub_rn(__dmul_rn(P, __dsub_rn(elem_f64(ry[u]), ay)), __dmul_rn(__dsub_rn(ax, xj), S));
+        long long k = __double_as_longlong(t) & 0x7fffffffffffffffLL;
+        k = k > 0x7ff0000000000000LL ? -1LL : k;
+        if (k > bk) { bk = k; bi = j; }
       }
     }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    const double oa = __shfl_xor_sync(FULL, bestv, o);
+    const long long ok = __shfl_xor_sync(FULL, bk, o);
     const long long oi = __shfl_xor_sync(FULL, bi, o);
-    if (oa > bestv || (oa == bestv && oi < bi)) { bestv = oa; bi = oi; }
+    if (ok > bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
   }
-  if (lane == 0) { s_a[wid] = bestv; s_i[wid] = bi; }
+  if (lane == 0) { s_a[wid] = __longlong_as_double(bk); s_i[wid] = bi; }
   __syncthreads();
   if (wid == 0) {
-    bestv = lane < NT / 32 ? s_a[lane] : -1.0;
+    bk = lane < NT / 32 ? __double_as_longlong(s_a[lane]) : -1LL;
     bi = lane < NT / 32 ? s_i[lane] : LLONG_MAX;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      const double oa = __shfl_xor_sync(FULL, bestv, o);
+      const long long ok = __shfl_xor_sync(FULL, bk, o);
       const long long oi = __shfl_xor_sync(FULL, bi, o);
-      if (oa > bestv || (oa == bestv && oi < bi)) { bestv = oa; bi = oi; }
+      if (ok > bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
     }
     if (lane == 0) s_i[0] = bi == LLONG_MAX ? lo : bi;  // all-NaN bucket keeps bounds[b] (:110)
   }
@@ -1588,6 +1692,830 @@ __device__ __forceinline__ int64_t block_bucket_argmax(const XT* xs, const YT* y
   const int64_t r = s_i[0];
   __syncthreads();
   return r;
+}
+
+// ---- K3c certified means -------------------------------------------------
+// The reference's bucket means are in-order fp64 sums (_kernels.py:98-104): a
+// dependent chain of ~5,000 DADDs per bucket.  Instead, K3c takes any-order
+// (parallel) sums plus a rigorous bound on their distance to the in-order
+// result, and every exact argmax (verify / verify2 / repair) CERTIFIES its
+// pick against that bound: the runner-up area must trail the winner by more
+// than twice the worst-case area error the mean error can cause.  A bucket
+// that fails (near-tie, non-finite area) gets its in-order mean computed
+// exactly on the spot and is re-scanned, so the output is the reference's
+// whatever the data.  A mean is EXACT (bound 0, no certification needed)
+// when every partial sum in any order is representable: all values are
+// multiples of 2^L (L = lowest set bit over the bucket) and sum|v| < 2^(53+L)
+// -- integer x (arange) and float32-origin y usually are.
+constexpr double K3C_U = 1.1102230246251565e-16;  // unit roundoff 2^-53
+
+// exponent of the lowest set bit of |v| (zero: +large, it constrains nothing);
+// subnormals come out one low, which only makes the exactness test stricter
+__device__ __forceinline__ int lsb_exp(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const int e = (int)((b >> 52) & 0x7ff);
+  const long long mnt = (long long)((b & 0xfffffffffffffull) | (1ull << 52));
+  return v == 0.0 ? 4096 : e - 1075 + (__ffsll(mnt) - 1);
+}
+
+// |in-order fp64 mean - fl(S/n)| bound for a bucket of n values with any-order
+// sum S, any-order sum of magnitudes A and lowest-bit exponent L; 0 = exact.
+__device__ __forceinline__ double mean_err_bound(double S, double A, int L, double n) {
+  const double lim = L + 53 > 1100 ? INFINITY : ldexp(1.0, L + 53);
+  if (A < lim) return 0.0;  // every partial sum representable: both sums exact
+  const double g = n * K3C_U / (1.0 - n * K3C_U);  // gamma_n: |sum_fl - sum| <= gamma_n * sum|v|, any order
+  const double c = S / n;
+  // |ref - S| <= 2 gamma A; the two divisions add u|c| + u|c'|
+  return (2.0 * g * A / n * (1.0 + 4.0 * g) + 2.0 * K3C_U * fabs(c)) * (1.0 + 1e-12) + 1e-300;
+}
+
+// Per-bucket stats in one coalesced pass, one CTA per bucket q: (ymin, ymax)
+// of bucket q (direction candidates) and, for q >= 1, the approximate mean of
+// bucket q with its error bound -> means[q-1], merr[q-1] (the mean bucket q-1
+// anchors on).  Bandwidth-bound: no dependent add chain.
+template <typename XT, typename YT, int NT, int UN>
+__global__ void __launch_bounds__(NT) k_lttb_means_approx(LttbArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ double s_d[6][NW];
+  __shared__ int s_l[2][NW];
+  const int64_t s = blockIdx.y, q = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t lo = lbound(a, m, q), hi = lbound(a, m, q + 1);
+  double sx = 0.0, sy = 0.0, ax = 0.0, ay = 0.0, ymn = INFINITY, ymx = -INFINITY;
+  int lx = XForm<XT>::integral ? 0 : 4096, ly = 4096;
+  // affine-x candidate from the bucket's first two points (XAff)
+  XAff f;
+  {
+    const XT x0r = xs[lo], x1r = hi - lo > 1 ? xs[lo + 1] : xs[lo];
+    f.x0 = (double)x0r;
+    f.d = __dsub_rn((double)x1r, (double)x0r);
+    f.x0i = (long long)x0r;
+    f.di = (long long)((unsigned long long)(long long)x1r - (unsigned long long)(long long)x0r);
+  }
+  bool aff = true;
+  for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += (int64_t)NT * UN) {
+    XT rx[UN];
+    YT ry[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {  // all loads in flight before any use
+      const int64_t j = j0 + (int64_t)NT * u < hi ? j0 + (int64_t)NT * u : lo;
+      rx[u] = __ldcs(xs + j);  // x streams (evict-first): y stays L2-resident for the later passes
+      ry[u] = ys[j];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      if (j0 + (int64_t)NT * u < hi) {
+        const double vx = (double)rx[u], vy = (double)ry[u];
+        sx += vx;
+        sy += vy;
+        ax += fabs(vx);
+        ay += fabs(vy);
+        ymn = fmin(ymn, vy);
+        ymx = fmax(ymx, vy);
+        if constexpr (!XForm<XT>::integral) lx = min(lx, lsb_exp(vx));  // integers: lsb >= 2^0
+        ly = min(ly, lsb_exp(vy));
+        const int64_t t = j0 + (int64_t)NT * u - lo;
+        if constexpr (XForm<XT>::integral) aff &= (long long)rx[u] == (long long)((unsigned long long)f.x0i + (unsigned long long)t * (unsigned long long)f.di);
+        else aff &= __double_as_longlong(vx) == __double_as_longlong(XForm<XT>::at(f, t));
+      }
+    }
+  }
+  aff = __syncthreads_and(aff);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sx += __shfl_xor_sync(FULL, sx, o);
+    sy += __shfl_xor_sync(FULL, sy, o);
+    ax += __shfl_xor_sync(FULL, ax, o);
+    ay += __shfl_xor_sync(FULL, ay, o);
+    ymn = fmin(ymn, __shfl_xor_sync(FULL, ymn, o));
+    ymx = fmax(ymx, __shfl_xor_sync(FULL, ymx, o));
+    lx = min(lx, __shfl_xor_sync(FULL, lx, o));
+    ly = min(ly, __shfl_xor_sync(FULL, ly, o));
+  }
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (NW > 1) {
+    if (lane == 0) {
+      s_d[0][wid] = sx; s_d[1][wid] = sy; s_d[2][wid] = ax; s_d[3][wid] = ay; s_d[4][wid] = ymn; s_d[5][wid] = ymx;
+      s_l[0][wid] = lx; s_l[1][wid] = ly;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < NW; ++w) {
+      sx += s_d[0][w]; sy += s_d[1][w]; ax += s_d[2][w]; ay += s_d[3][w];
+      ymn = fmin(ymn, s_d[4][w]); ymx = fmax(ymx, s_d[5][w]);
+      lx = min(lx, s_l[0][w]); ly = min(ly, s_l[1][w]);
+    }
+  } else if (lane != 0) {
+    return;
+  }
+  a.yrange[s * k3 + q] = make_double2(ymn, ymx);
+  if (a.xaff) {
+    f.ok = aff;
+    f.pad = 0;
+    a.xaff[s * k3 + q] = f;
+  }
+  if (q >= 1) {
+    const double n = (double)(hi - lo);
+    a.means[s * a.means_ld + q - 1] = make_double2(__ddiv_rn(sx, n), __ddiv_rn(sy, n));
+    a.merr[s * k3 + q - 1] = make_double2(mean_err_bound(sx, ax, lx, n), mean_err_bound(sy, ay, ly, n));
+  }
+  if (q == 0) {  // the last bucket anchors on point m-1 itself (_kernels.py:105-107): exact
+    a.means[s * a.means_ld + k3 - 1] = make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
+    a.merr[s * k3 + k3 - 1] = make_double2(0.0, 0.0);
+  }
+}
+
+// In-order (reference) mean of bucket b+1, by a whole CTA: tiles staged in
+// shared memory, threads 0/1 carry the x/y add chains.  The rare path of a
+// failed certification.
+template <typename XT, typename YT, int NT>
+__device__ double2 block_exact_mean(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b) {
+  constexpr int TILE = 512;
+  __shared__ double s_t[2][TILE];
+  __shared__ double s_c[2];
+  const int64_t k3 = a.n_out - 2;
+  if (b + 1 >= k3) return make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
+  const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
+  double acc = 0.0;
+  for (int64_t t0 = nlo; t0 < nhi; t0 += TILE) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < TILE; i += NT) {
+      const int64_t j = t0 + i;
+      if (j < nhi) { s_t[0][i] = to_f64(xs, j); s_t[1][i] = to_f64(ys, j); }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      const int n = (int)(nhi - t0 < TILE ? nhi - t0 : (int64_t)TILE);
+      const double* src = s_t[threadIdx.x];
+      for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, src[i]);  // sx += xs[j] in index order
+    }
+  }
+  const double cnt = (double)(nhi - nlo);
+  if (threadIdx.x < 2) s_c[threadIdx.x] = __ddiv_rn(acc, cnt);
+  __syncthreads();
+  const double2 c = make_double2(s_c[0], s_c[1]);
+  __syncthreads();
+  return c;
+}
+
+// Exact argmax of bucket b given anchor `prev` when means[b] is approximate:
+// scan with the approximate mean tracking the winner, the runner-up and the
+// magnitudes that bound the area error; certify, else compute the exact mean
+// (stored back: merr[b] = 0) and re-scan.
+template <typename XT, typename YT, int NT>
+__device__ int64_t block_bucket_argmax_cert(const LttbArgs& a, int64_t s, int64_t m, const XT* xs, const YT* ys,
+                                            int64_t b, int64_t prev, double* s_a, long long* s_i) {
+  const int64_t k3 = a.n_out - 2;
+  const int64_t lo = lbound(a, m, b), hi = lbound(a, m, b + 1);
+  const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
+  double2* mp = a.means + s * a.means_ld + b;
+  double2* ep = a.merr + s * k3 + b;
+  const double2 c = *mp;
+  const double2 ce = *ep;
+  const XAff* xa = a.xaff ? a.xaff + s * k3 + b : nullptr;
+  if (ce.x == 0.0 && ce.y == 0.0)  // exact mean: the plain scan IS the reference's
+    return block_bucket_argmax<XT, YT, NT>(xs, ys, lo, hi, ax, ay, c, s_a, s_i, xa);
+  __shared__ double s_v2[NT / 32], s_q[NT / 32], s_r[NT / 32];
+  __shared__ int s_bad[NT / 32];
+  __shared__ int s_ok;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double P = __dsub_rn(ax, c.x), S = __dsub_rn(c.y, ay);
+  // keys (bit patterns of non-negative doubles order like the values): no fp64 compares
+  long long k1 = -1, k2 = -1, kq = 0, kr = 0;
+  long long i1 = LLONG_MAX;
+  int bad = 0;
+  constexpr int UN = K3C_UN_VER;
+  const bool aff = xa && xa->ok;
+  XAff f;
+  if (aff) f = *xa;
+  for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += (int64_t)NT * UN) {
+    XT rx[UN];
+    YT ry[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int64_t j = j0 + (int64_t)NT * u < hi ? j0 + (int64_t)NT * u : lo;
+      if (!aff) rx[u] = xs[j];
+      ry[u] = ys[j];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int64_t j = j0 + (int64_t)NT * u;
+      if (j < hi) {
+        const double xj = aff ? XForm<XT>::at(f, j - lo) : elem_f64(rx[u]);
+        const double R = __dsub_rn(ax, xj), Q = __dsub_rn(elem_f64(ry[u]), ay);
+        const double t = __dsub_rn(__dmul_rn(P, Q), __dmul_rn(R, S));  // lttb_area, same op order
+        long long k = __double_as_longlong(t) & 0x7fffffffffffffffLL;
+        bad |= (int)(k >> 32) >= 0x7ff00000;  // inf or NaN: no certification
+        k = k > 0x7ff0000000000000LL ? -1LL : k;
+        kq = max(kq, __double_as_longlong(Q) & 0x7fffffffffffffffLL);
+        kr = max(kr, __double_as_longlong(R) & 0x7fffffffffffffffLL);
+        if (k > k2) {
+          if (k > k1) { k2 = k1; k1 = k; i1 = j; }
+          else k2 = k;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    vpart_merge(k1, i1, k2, bad, __shfl_xor_sync(FULL, k1, o), __shfl_xor_sync(FULL, i1, o),
+                __shfl_xor_sync(FULL, k2, o), __shfl_xor_sync(FULL, bad, o));
+    kq = max(kq, __shfl_xor_sync(FULL, kq, o));
+    kr = max(kr, __shfl_xor_sync(FULL, kr, o));
+  }
+  if (lane == 0) {
+    s_a[wid] = __longlong_as_double(k1); s_i[wid] = i1; s_v2[wid] = __longlong_as_double(k2);
+    s_q[wid] = __longlong_as_double(kq); s_r[wid] = __longlong_as_double(kr); s_bad[wid] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < NT / 32; ++w) {
+      vpart_merge(k1, i1, k2, bad, __double_as_longlong(s_a[w]), s_i[w], __double_as_longlong(s_v2[w]), s_bad[w]);
+      kq = max(kq, __double_as_longlong(s_q[w]));
+      kr = max(kr, __double_as_longlong(s_r[w]));
+    }
+    const double v1 = k1 < 0 ? -1.0 : __longlong_as_double(k1), v2 = k2 < 0 ? -1.0 : __longlong_as_double(k2);
+    const double qm = __longlong_as_double(kq), rm = __longlong_as_double(kr);
+    // area error bound over the bucket (certified means):
+    // |P-P'| <= dP, |S-S'| <= dS; |T1-T1'| <= qm (dP + u(2|P'| + dP)), same for T2;
+    // |A-A'| <= (dT1 + dT2)(1+u) + 2u max A'
+    const double u = K3C_U;
+    const double dP = ce.x == 0.0 ? 0.0 : ce.x + u * (2.0 * fabs(P) * (1.0 + 2.0 * u) + ce.x);
+    const double dS = ce.y == 0.0 ? 0.0 : ce.y + u * (2.0 * fabs(S) * (1.0 + 2.0 * u) + ce.y);
+    const double dT = (dP == 0.0 ? 0.0 : qm * (dP + u * (2.0 * fabs(P) + dP))) +
+                      (dS == 0.0 ? 0.0 : rm * (dS + u * (2.0 * fabs(S) + dS)));
+    const double E = (dT * (1.0 + 2.0 * u) + 2.0 * u * fmax(v1, 0.0) * (1.0 + 2.0 * u)) * (1.0 + 1e-9) + 1e-300;
+    const bool ok = hi - lo == 1 || (!bad && !a.cert_force && __dsub_rn(v1, v2) > 2.0 * E * (1.0 + 1e-9));
+    s_ok = ok;
+    s_i[0] = i1 == LLONG_MAX ? lo : i1;
+  }
+  __syncthreads();
+  const int ok = s_ok;
+  const int64_t r = s_i[0];
+  __syncthreads();
+  if (ok) return r;
+  // failed: the reference's own in-order mean, kept for later scans of bucket b
+  const double2 ce2 = block_exact_mean<XT, YT, NT>(a, xs, ys, m, b);
+  if (threadIdx.x == 0) { *mp = ce2; *ep = make_double2(0.0, 0.0); }
+  return block_bucket_argmax<XT, YT, NT>(xs, ys, lo, hi, ax, ay, ce2, s_a, s_i, xa);
+}
+
+template <typename XT, typename YT, int NT>
+__device__ __forceinline__ int64_t k3c_argmax(const LttbArgs& a, int64_t s, int64_t m, const XT* xs, const YT* ys,
+                                              int64_t b, int64_t prev, double* s_a, long long* s_i) {
+  if (a.merr) return block_bucket_argmax_cert<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
+  return block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
+                                         to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+}
+
+// ---- K3c flat passes --------------------------------------------------------
+// The per-bucket passes above give each bucket one CTA; with ~2,000 buckets of
+// ~5,000 points that is 1-2 waves of CTAs each walking its bucket in ~10
+// dependent load rounds, so the GPU idles on latency.  The flat passes split
+// the series' elements [1, m-1) into equal contiguous ranges, one per warp
+// (a single wave), each warp walking the 1-2 bucket segments its range
+// intersects; per-(bucket, warp) partials are combined by the bucket's
+// last-arriving warp (threadfence reduction), which finalises the bucket.
+#ifndef K3C_FLAT_MINB
+#define K3C_FLAT_MINB 3  // 3 x 256 threads per SM = 24 warps (host: flat_plan); candidates 2 x 256
+#endif
+struct FlatArgs {
+  int64_t E;                 // elements per warp
+  int64_t W;                 // warps per series
+  int64_t CP;                // partial slots per bucket (>= warps touching one bucket)
+  unsigned* cnt;             // [B][k3] arrival counters (zeroed per call)
+  void* part;                // [B][k3][CP] partials
+  int* ulist; int* ucount;   // verify: [B][k3] buckets whose certification failed, [B] count (zeroed)
+};
+
+// largest b with lbound(b) = 1 + floor(b (m-2) / k3) <= j, for j in [1, m-1)
+__device__ __forceinline__ int64_t lttb_bucket_of(int64_t j, int64_t m, int64_t k3) { return (j * k3 - 1) / (m - 2); }
+
+// lane 0: publish this warp's partial, return true if it was the bucket's last
+__device__ __forceinline__ bool flat_arrive(unsigned* c, unsigned n) {
+  __threadfence();
+  const unsigned old = atomicAdd(c, 1u);
+  if (old + 1 != n) return false;
+  __threadfence();
+  return true;
+}
+
+// |T_j - T'_j| bound for every j of a bucket (see block_bucket_argmax_cert):
+// from the mean error ce and the bucket's |y - ay| / |ax - x| extremes
+__device__ __forceinline__ double k3c_area_err(double2 ce, double P, double S, double qmax, double rmax, double v1) {
+  const double u = K3C_U;
+  const double dP = ce.x == 0.0 ? 0.0 : ce.x + u * (2.0 * fabs(P) * (1.0 + 2.0 * u) + ce.x);
+  const double dS = ce.y == 0.0 ? 0.0 : ce.y + u * (2.0 * fabs(S) * (1.0 + 2.0 * u) + ce.y);
+  const double dT = (dP == 0.0 ? 0.0 : qmax * (dP + u * (2.0 * fabs(P) + dP))) +
+                    (dS == 0.0 ? 0.0 : rmax * (dS + u * (2.0 * fabs(S) + dS)));
+  return (dT * (1.0 + 2.0 * u) + 2.0 * u * fmax(v1, 0.0) * (1.0 + 2.0 * u)) * (1.0 + 1e-9) + 1e-300;
+}
+
+// One warp's pass over a verification segment [0, n) (offsets from the
+// segment start): keys of |T_j| (T_j exactly as lttb_area), top-2 and the
+// first index of the top key.  MODE 0: affine integer x from a running f64
+// (exact: integers < 2^50); 1: affine x by formula; 2: x loaded.
+template <int MODE, typename XT, typename YT, int UN>
+__device__ __forceinline__ void verify_scan(const XT* __restrict__ xb, const YT* __restrict__ yb, int n, int lane,
+                                            double ax, double ay, double P, double S, double x0d, double dx1,
+                                            double dstep, const XAff& f, int64_t t0, long long& k1, long long& k2,
+                                            int& i1, int& bad) {
+  double xl = MODE == 0 ? __dadd_rn(x0d, __dmul_rn((double)lane, dx1)) : 0.0;  // exact: integer-valued
+  for (int i = lane; i < n; i += 32 * UN) {
+    XT rx[UN];
+    YT ry[UN];
+    const bool full = i + 32 * (UN - 1) < n;
+    if (full) {  // constant offsets from one pointer: no per-load address arithmetic
+      const XT* xp = xb + i;
+      const YT* yp = yb + i;
+#pragma unroll
+      for (int q = 0; q < UN; ++q) {
+        if (MODE == 2) rx[q] = xp[32 * q];
+        ry[q] = yp[32 * q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < UN; ++q) {
+        const int ii = i + 32 * q < n ? i + 32 * q : i;
+        if (MODE == 2) rx[q] = xb[ii];
+        ry[q] = yb[ii];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UN; ++q) {
+      double xj;
+      if (MODE == 0) xj = xl;
+      else if (MODE == 1) xj = XForm<XT>::at(f, t0 + i + 32 * q);
+      else xj = elem_f64(rx[q]);
+      if (MODE == 0) xl = __dadd_rn(xl, dstep);
+      if (full || i + 32 * q < n) {
+        const double R = __dsub_rn(ax, xj), Q = __dsub_rn(elem_f64(ry[q]), ay);
+        const double t = __dsub_rn(__dmul_rn(P, Q), __dmul_rn(R, S));  // lttb_area, same op order
+        const long long k = __double_as_longlong(t) & 0x7fffffffffffffffLL;
+        bad |= (int)(k >> 32) >= 0x7ff00000;  // inf / NaN: the bucket takes the exact fallback
+        if (k > k2) {  // rare after the first few points
+          if (k > k1) { k2 = k1; k1 = k; i1 = i + 32 * q; }
+          else k2 = k;
+        }
+      }
+    }
+  }
+}
+
+// Flat verification: every bucket's exact argmax given the candidate chain's
+// previous pick, certified against merr (see block_bucket_argmax_cert); a
+// bucket that fails certification goes on ulist for k_lttb_verify_fix.
+template <typename XT, typename YT, int UN>
+__global__ void __launch_bounds__(256, K3C_FLAT_MINB) k_lttb_verify_flat(LttbArgs a, FlatArgs fl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t s = blockIdx.y;
+  const int64_t k3 = a.n_out - 2, m = a.n;
+  const int64_t e0 = 1 + gw * fl.E, e1 = min(m - 1, e0 + fl.E);
+  if (gw >= fl.W || e0 >= e1) return;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t* pos = a.pos + s * a.pos_ld;
+  VPart* part = (VPart*)fl.part + s * k3 * fl.CP;
+  const double u = K3C_U;
+  int64_t b = lttb_bucket_of(e0, m, k3);
+  for (int64_t j = e0; j < e1; ++b) {
+    const int64_t lo = lbound(a, m, b), hi = lbound(a, m, b + 1);
+    const int64_t s1 = min(e1, hi);
+    const int n = (int)(s1 - j);  // segment [j, s1), 32-bit offsets
+    const int64_t prev = pos[b];
+    const double2 c = a.means[s * a.means_ld + b];
+    const double2 ce = a.merr ? a.merr[s * k3 + b] : make_double2(0.0, 0.0);
+    const double2 yr = a.yrange[s * k3 + b], xr = a.xrange[s * k3 + b];
+    const bool aff = a.xaff && a.xaff[s * k3 + b].ok;
+    XAff f;
+    if (aff) f = a.xaff[s * k3 + b];
+    // affine integer x inside the magic range: x_j = i2d_magic(x0 + t d) and
+    // consecutive lanes' x step by exact f64 adds (every value an integer < 2^51)
+    const bool afi = aff && XForm<XT>::integral && fmax(fabs(xr.x), fabs(xr.y)) < 1125899906842624.0;
+    const double dstep = afi ? i2d_magic(32 * f.di) : 0.0;
+    const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
+    const double P = __dsub_rn(ax, c.x), S = __dsub_rn(c.y, ay);
+    long long k1 = -1, k2 = -1;
+    int i1 = INT_MAX, bad = 0;
+    const int64_t t0 = j - lo;
+    if (afi) {
+      const double x0d = i2d_magic((long long)((unsigned long long)f.x0i + (unsigned long long)t0 * (unsigned long long)f.di));
+      const double dx1 = i2d_magic(f.di);
+      verify_scan<0, XT, YT, UN>(xs + j, ys + j, n, lane, ax, ay, P, S, x0d, dx1, dstep, f, t0, k1, k2, i1, bad);
+    } else if (aff) {
+      verify_scan<1, XT, YT, UN>(xs + j, ys + j, n, lane, ax, ay, P, S, 0.0, 0.0, 0.0, f, t0, k1, k2, i1, bad);
+    } else {
+      verify_scan<2, XT, YT, UN>(xs + j, ys + j, n, lane, ax, ay, P, S, 0.0, 0.0, 0.0, f, t0, k1, k2, i1, bad);
+    }
+    long long i1g = i1 == INT_MAX ? LLONG_MAX : j + i1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+      vpart_merge(k1, i1g, k2, bad, __shfl_xor_sync(FULL, k1, o), __shfl_xor_sync(FULL, i1g, o),
+                  __shfl_xor_sync(FULL, k2, o), __shfl_xor_sync(FULL, bad, o));
+    const int64_t w0 = (lo - 1) / fl.E;
+    const unsigned ns = (unsigned)((hi - 2) / fl.E - w0 + 1);
+    bool last = false;
+    if (lane == 0) {
+      VPart p;
+      p.k1 = k1; p.k2 = k2; p.i1 = i1g; p.bad = bad; p.pad = 0;
+      part[b * fl.CP + (gw - w0)] = p;
+      last = flat_arrive(fl.cnt + s * k3 + b, ns);
+    }
+    if (__shfl_sync(FULL, (int)last, 0)) {
+      k1 = -1; k2 = -1; i1g = LLONG_MAX; bad = 0;
+      for (unsigned q = lane; q < ns; q += 32) {
+        const VPart* pp = part + b * fl.CP + q;
+        vpart_merge(k1, i1g, k2, bad, __ldcg(&pp->k1), __ldcg(&pp->i1), __ldcg(&pp->k2), __ldcg(&pp->bad));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+        vpart_merge(k1, i1g, k2, bad, __shfl_xor_sync(FULL, k1, o), __shfl_xor_sync(FULL, i1g, o),
+                    __shfl_xor_sync(FULL, k2, o), __shfl_xor_sync(FULL, bad, o));
+      if (lane == 0) {
+        const bool exact = ce.x == 0.0 && ce.y == 0.0;
+        // inf/NaN areas: keys were not remapped in the scan, so the exact block scan decides
+        bool ok = !bad && (exact || hi - lo == 1);
+        if (!ok && !bad && !a.cert_force) {
+          // |Q_j| <= (1+u) max|y - ay| over the bucket's y extremes (likewise R)
+          const double qmax = fmax(fabs(__dsub_rn(yr.y, ay)), fabs(__dsub_rn(yr.x, ay))) * (1.0 + 4.0 * u);
+          const double rmax = fmax(fabs(__dsub_rn(ax, xr.x)), fabs(__dsub_rn(ax, xr.y))) * (1.0 + 4.0 * u);
+          const double v1 = k1 < 0 ? -1.0 : __longlong_as_double(k1), v2 = k2 < 0 ? -1.0 : __longlong_as_double(k2);
+          const double E = k3c_area_err(ce, P, S, qmax, rmax, v1);
+          ok = __dsub_rn(v1, v2) > 2.0 * E * (1.0 + 1e-9);  // NaN bounds fail
+        }
+        if (ok) {
+          const int64_t r = i1g == LLONG_MAX ? lo : i1g;  // all-NaN bucket keeps bounds[b] (:110)
+          a.best[s * k3 + b] = r;
+          const bool fg = r != pos[b + 1];
+          a.flag[s * k3 + b] = fg;
+          if (fg) a.flist[s * k3 + atomicAdd(&a.fcount[s], 1)] = (int)b;
+        } else {
+          fl.ulist[s * k3 + atomicAdd(&fl.ucount[s], 1)] = (int)b;
+        }
+      }
+    }
+    j = s1;
+  }
+}
+
+// Buckets whose flat certification failed: exact in-order mean, exact re-scan.
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_verify_fix(LttbArgs a, FlatArgs fl) {
+  __shared__ double s_a[NT / 32];
+  __shared__ long long s_i[NT / 32];
+  const int64_t s = blockIdx.y;
+  const int64_t k3 = a.n_out - 2;
+  const int nu = fl.ucount[s];
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  const int64_t* pos = a.pos + s * a.pos_ld;
+  for (int q = blockIdx.x; q < nu; q += gridDim.x) {
+    const int64_t b = fl.ulist[s * k3 + q];
+    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, pos[b], s_a, s_i);
+    if (threadIdx.x == 0) {
+      a.best[s * k3 + b] = r;
+      const bool fg = r != pos[b + 1];
+      a.flag[s * k3 + b] = fg;
+      if (fg) a.flist[s * k3 + atomicAdd(&a.fcount[s], 1)] = (int)b;
+    }
+  }
+}
+
+// Flat means pass: per-bucket any-order sums, magnitudes, lowest set bits,
+// x / y extremes (integer keys) and the affine-x test, from equal element
+// ranges per warp (partials combined by the bucket's last-arriving warp).
+struct MPart { double sx, sy, ax, ay; long long kxmn, kxmx, kymn, kymx; int lx, ly, aff, pad; };
+
+__device__ __forceinline__ void mpart_merge(MPart& p, const MPart& o) {
+  p.sx += o.sx; p.sy += o.sy; p.ax += o.ax; p.ay += o.ay;
+  p.kxmn = min(p.kxmn, o.kxmn); p.kxmx = max(p.kxmx, o.kxmx);
+  p.kymn = min(p.kymn, o.kymn); p.kymx = max(p.kymx, o.kymx);
+  p.lx = min(p.lx, o.lx); p.ly = min(p.ly, o.ly); p.aff &= o.aff;
+}
+__device__ __forceinline__ void mpart_shfl(MPart& p, int o) {
+  MPart q;
+  q.sx = __shfl_xor_sync(FULL, p.sx, o); q.sy = __shfl_xor_sync(FULL, p.sy, o);
+  q.ax = __shfl_xor_sync(FULL, p.ax, o); q.ay = __shfl_xor_sync(FULL, p.ay, o);
+  q.kxmn = __shfl_xor_sync(FULL, p.kxmn, o); q.kxmx = __shfl_xor_sync(FULL, p.kxmx, o);
+  q.kymn = __shfl_xor_sync(FULL, p.kymn, o); q.kymx = __shfl_xor_sync(FULL, p.kymx, o);
+  q.lx = __shfl_xor_sync(FULL, p.lx, o); q.ly = __shfl_xor_sync(FULL, p.ly, o);
+  q.aff = __shfl_xor_sync(FULL, p.aff, o);
+  mpart_merge(p, q);
+}
+__device__ __forceinline__ void mpart_init(MPart& p, bool integral) {
+  p.sx = p.sy = p.ax = p.ay = 0.0;
+  p.kxmn = p.kymn = LLONG_MAX; p.kxmx = p.kymx = LLONG_MIN;
+  p.lx = integral ? 0 : 4096; p.ly = 4096; p.aff = 1; p.pad = 0;
+}
+
+// exponent of |v| (unbiased), for the exactness pre-check
+__device__ __forceinline__ int exp_of(double v) { return (int)((__double_as_longlong(v) >> 52) & 0x7ff) - 1023; }
+
+// One warp's pass over a means segment [0, n): any-order sums, magnitudes,
+// y extremes (keys), x extremes, lowest set bits (TRYY: y's; float x: x's when
+// try_x) and the affine-x test against the bucket's formula.
+template <bool TRYY, typename XT, typename YT, int UN>
+__device__ __forceinline__ void means_scan(const XT* __restrict__ xb, const YT* __restrict__ yb, int n, int lane,
+                                           const XAff& f, int64_t t0, MPart& p, long long& xmn, long long& xmx,
+                                           bool try_x) {
+  const long long dstep = (long long)((unsigned long long)f.di * 32ull);
+  long long xe = (long long)((unsigned long long)f.x0i + (unsigned long long)(t0 + lane) * (unsigned long long)f.di);
+  for (int i = lane; i < n; i += 32 * UN) {
+    XT rx[UN];
+    YT ry[UN];
+    const bool full = i + 32 * (UN - 1) < n;
+    if (full) {
+      const XT* xp = xb + i;
+      const YT* yp = yb + i;
+#pragma unroll
+      for (int q = 0; q < UN; ++q) {
+        rx[q] = __ldcs(xp + 32 * q);  // x streams (evict-first): y stays L2-resident for the later passes
+        ry[q] = yp[32 * q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < UN; ++q) {
+        const int ii = i + 32 * q < n ? i + 32 * q : i;
+        rx[q] = __ldcs(xb + ii);
+        ry[q] = yb[ii];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UN; ++q) {
+      if (full || i + 32 * q < n) {
+        const double vx = elem_f64(rx[q]), vy = elem_f64(ry[q]);
+        p.sx = __dadd_rn(p.sx, vx); p.sy = __dadd_rn(p.sy, vy);
+        p.ax = __dadd_rn(p.ax, fabs(vx)); p.ay = __dadd_rn(p.ay, fabs(vy));
+        const long long ky = dkey(vy);
+        if (ky < p.kymn) p.kymn = ky;
+        if (ky > p.kymx) p.kymx = ky;
+        if (TRYY) p.ly = min(p.ly, lsb_exp(vy));
+        if constexpr (XForm<XT>::integral) {
+          const long long xi = (long long)rx[q];
+          if (xi < xmn) xmn = xi;
+          if (xi > xmx) xmx = xi;
+          p.aff &= xi == xe;
+        } else {
+          const long long kx = dkey(vx);
+          if (kx < p.kxmn) p.kxmn = kx;
+          if (kx > p.kxmx) p.kxmx = kx;
+          if (try_x) p.lx = min(p.lx, lsb_exp(vx));
+          p.aff &= __double_as_longlong(vx) == __double_as_longlong(XForm<XT>::at(f, t0 + i + 32 * q));
+        }
+      }
+      xe = (long long)((unsigned long long)xe + (unsigned long long)dstep);
+    }
+  }
+}
+
+template <typename XT, typename YT, int UN>
+__global__ void __launch_bounds__(256, K3C_FLAT_MINB) k_lttb_means_flat(LttbArgs a, FlatArgs fl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t s = blockIdx.y;
+  const int64_t k3 = a.n_out - 2, m = a.n;
+  const int64_t e0 = 1 + gw * fl.E, e1 = min(m - 1, e0 + fl.E);
+  if (gw >= fl.W || e0 >= e1) return;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  MPart* part = (MPart*)fl.part + s * k3 * fl.CP;
+  int64_t b = lttb_bucket_of(e0, m, k3);
+  for (int64_t j = e0; j < e1; ++b) {
+    const int64_t lo = lbound(a, m, b), hi = lbound(a, m, b + 1);
+    const int64_t s1 = min(e1, hi);
+    const int n = (int)(s1 - j);
+    XAff f;  // affine-x candidate from the bucket's first two points
+    {
+      const XT x0r = xs[lo], x1r = hi - lo > 1 ? xs[lo + 1] : xs[lo];
+      f.x0 = (double)x0r;
+      f.d = __dsub_rn((double)x1r, (double)x0r);
+      f.x0i = (long long)x0r;
+      f.di = (long long)((unsigned long long)(long long)x1r - (unsigned long long)(long long)x0r);
+    }
+    // exactness is only worth tracking (lowest set bits) when it is plausible:
+    // full-mantissa values can never have every partial sum representable, and
+    // declaring a mean inexact is always safe (it is then certified)
+    const double nb = (double)(hi - lo);
+    const double y0 = elem_f64(ys[j]), x0 = elem_f64(xs[j]);
+    const bool try_y = y0 == 0.0 || (double)lsb_exp(y0) + 55.0 > (double)exp_of(y0) + log2(nb);
+    const bool try_x = !XForm<XT>::integral && (x0 == 0.0 || (double)lsb_exp(x0) + 55.0 > (double)exp_of(x0) + log2(nb));
+    const XT* xb = xs + j;
+    const YT* yb = ys + j;
+    MPart p;
+    mpart_init(p, XForm<XT>::integral);
+    if (!try_y) p.ly = -4096;
+    if (!XForm<XT>::integral && !try_x) p.lx = -4096;
+    long long xmn = LLONG_MAX, xmx = LLONG_MIN;  // integer x: extremes on the values themselves
+    if (try_y) means_scan<true, XT, YT, UN>(xb, yb, n, lane, f, j - lo, p, xmn, xmx, try_x);
+    else means_scan<false, XT, YT, UN>(xb, yb, n, lane, f, j - lo, p, xmn, xmx, try_x);
+    if constexpr (XForm<XT>::integral) {  // keys of the (exactly or nearest-) converted extremes
+      if (xmn <= xmx) {
+        p.kxmn = dkey(elem_f64((XT)xmn));
+        p.kxmx = dkey(elem_f64((XT)xmx));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mpart_shfl(p, o);
+    const int64_t w0 = (lo - 1) / fl.E;
+    const unsigned ns = (unsigned)((hi - 2) / fl.E - w0 + 1);
+    bool last = false;
+    if (lane == 0) {
+      part[b * fl.CP + (gw - w0)] = p;
+      last = flat_arrive(fl.cnt + s * k3 + b, ns);
+    }
+    if (__shfl_sync(FULL, (int)last, 0)) {
+      mpart_init(p, true);
+      p.lx = 4096;
+      for (unsigned q = lane; q < ns; q += 32) {
+        const MPart* pp = part + b * fl.CP + q;
+        MPart o;
+        o.sx = __ldcg(&pp->sx); o.sy = __ldcg(&pp->sy); o.ax = __ldcg(&pp->ax); o.ay = __ldcg(&pp->ay);
+        o.kxmn = __ldcg(&pp->kxmn); o.kxmx = __ldcg(&pp->kxmx); o.kymn = __ldcg(&pp->kymn); o.kymx = __ldcg(&pp->kymx);
+        o.lx = __ldcg(&pp->lx); o.ly = __ldcg(&pp->ly); o.aff = __ldcg(&pp->aff);
+        mpart_merge(p, o);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mpart_shfl(p, o);
+      if (lane == 0) {
+        a.yrange[s * k3 + b] = make_double2(dkey_inv(p.kymn), dkey_inv(p.kymx));
+        a.xrange[s * k3 + b] = make_double2(dkey_inv(p.kxmn), dkey_inv(p.kxmx));
+        if (a.xaff) {
+          f.ok = p.aff;
+          f.pad = 0;
+          a.xaff[s * k3 + b] = f;
+        }
+        if (b >= 1) {
+          a.means[s * a.means_ld + b - 1] = make_double2(__ddiv_rn(p.sx, nb), __ddiv_rn(p.sy, nb));
+          a.merr[s * k3 + b - 1] = make_double2(mean_err_bound(p.sx, p.ax, p.lx, nb), mean_err_bound(p.sy, p.ay, p.ly, nb));
+        } else {  // the last bucket anchors on point m-1 itself (_kernels.py:105-107): exact
+          a.means[s * a.means_ld + k3 - 1] = make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
+          a.merr[s * k3 + k3 - 1] = make_double2(0.0, 0.0);
+        }
+      }
+    }
+    j = s1;
+  }
+}
+
+// Flat direction-sampled candidates (k_lttb_dircand's heuristic): per warp
+// segment the D directions' argmax/argmin, merged by the last-arriving warp,
+// which sorts, dedups and writes the bucket's candidate list.  Points enter
+// as float32 offsets from (x_lo, c_y), converted without the XU pipe.
+template <int D> struct CPart { float v[2 * D]; int i[2 * D]; };
+
+template <typename XT, typename YT, int HMAX, int D, int UN>
+__global__ void __launch_bounds__(256, K3C_FLAT_MINB - 1) k_lttb_dircand_flat(LttbArgs a, FlatArgs fl) {
+  static_assert(2 * D <= HMAX && 2 * D <= 32, "candidates must fit");
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t s = blockIdx.y;
+  const int64_t k3 = a.n_out - 2, m = a.n;
+  const int64_t e0 = 1 + gw * fl.E, e1 = min(m - 1, e0 + fl.E);
+  if (gw >= fl.W || e0 >= e1) return;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  CPart<D>* part = (CPart<D>*)fl.part + s * k3 * fl.CP;
+  int64_t b = lttb_bucket_of(e0, m, k3);
+  for (int64_t j = e0; j < e1; ++b) {
+    const int64_t blo = lbound(a, m, b), bhi = lbound(a, m, b + 1);
+    const int64_t s1 = min(e1, bhi);
+    const double2 c = a.means[s * a.means_ld + b];
+    double ax0, ax1, ay0, ay1;  // anchor box of bucket b-1 (or the fixed first point)
+    if (b == 0) {
+      ax0 = ax1 = to_f64(xs, 0);
+      ay0 = ay1 = to_f64(ys, 0);
+    } else {
+      const double2 rx = a.xrange[s * k3 + b - 1], ry = a.yrange[s * k3 + b - 1];
+      ax0 = rx.x; ax1 = rx.y; ay0 = ry.x; ay1 = ry.y;
+    }
+    float th_lo = 1e30f, th_hi = -1e30f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double dxv = c.y - ((q & 1) ? ay1 : ay0);
+      const double dyv = ((q & 2) ? ax1 : ax0) - c.x;
+      float th = atan2f((float)dyv, (float)dxv);
+      if (th > 3.0f) th -= 6.2831853f;  // keep the (x <= c.x) half-plane contiguous
+      th_lo = fminf(th_lo, th);
+      th_hi = fmaxf(th_hi, th);
+    }
+    float cs[D], sn[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float th = D > 1 ? th_lo + (th_hi - th_lo) * (float)k / (float)(D - 1) : th_lo;
+      sincosf(th, &sn[k], &cs[k]);
+    }
+    const double xrd = to_f64(xs, blo);
+    const double yr = c.y;
+    const float yrf = (float)yr;
+    const bool aff = a.xaff && a.xaff[s * k3 + b].ok;
+    const float fxf = aff ? (float)(XForm<XT>::integral ? (double)a.xaff[s * k3 + b].di : a.xaff[s * k3 + b].d) : 0.f;
+    const int n = (int)(s1 - j), ob = (int)(j - blo);  // segment [j, s1), offsets from the bucket start
+    const XT* xb = xs + j;
+    const YT* yb = ys + j;
+    float vmax[D], vmin[D];
+    int imax[D], imin[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) { vmax[k] = -INFINITY; vmin[k] = INFINITY; imax[k] = INT_MAX; imin[k] = INT_MAX; }
+    float of = (float)(ob + lane);  // running offset (exact below 2^24)
+    for (int i = lane; i < n; i += 32 * UN, of += (float)(32 * UN)) {
+      XT rx[UN];
+      YT ry[UN];
+      const bool full = i + 32 * (UN - 1) < n;
+#pragma unroll
+      for (int q = 0; q < UN; ++q) {
+        const int ii = full || i + 32 * q < n ? i + 32 * q : i;
+        if (!aff) rx[q] = xb[ii];
+        ry[q] = yb[ii];
+      }
+#pragma unroll
+      for (int q = 0; q < UN; ++q) {
+        if (full || i + 32 * q < n) {
+          const int o = ob + i + 32 * q;
+          const float X = aff ? (of + (float)(32 * q)) * fxf : d2f_trunc(__dsub_rn(elem_f64(rx[q]), xrd));
+          float Y;
+          if constexpr (sizeof(YT) == 4) Y = __fsub_rn((float)ry[q], yrf);
+          else Y = d2f_trunc(__dsub_rn((double)ry[q], yr));
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const float v = fmaf(cs[k], X, sn[k] * Y);
+            if (v > vmax[k]) { vmax[k] = v; imax[k] = o; }
+            if (v < vmin[k]) { vmin[k] = v; imin[k] = o; }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const float ov = __shfl_xor_sync(FULL, vmax[k], off);
+        const int oi = __shfl_xor_sync(FULL, imax[k], off);
+        if (ov > vmax[k] || (ov == vmax[k] && oi < imax[k])) { vmax[k] = ov; imax[k] = oi; }
+        const float ow = __shfl_xor_sync(FULL, vmin[k], off);
+        const int oj = __shfl_xor_sync(FULL, imin[k], off);
+        if (ow < vmin[k] || (ow == vmin[k] && oj < imin[k])) { vmin[k] = ow; imin[k] = oj; }
+      }
+    }
+    const int64_t w0 = (blo - 1) / fl.E;
+    const unsigned ns = (unsigned)((bhi - 2) / fl.E - w0 + 1);
+    CPart<D>* mine = part + b * fl.CP + (gw - w0);
+    if (lane < 2 * D) {  // lane 2k: max of direction k; lane 2k+1: min (stored negated: both as "max")
+      float v = 0.f;
+      int ix = 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        if (lane == 2 * k) { v = vmax[k]; ix = imax[k]; }
+        if (lane == 2 * k + 1) { v = -vmin[k]; ix = imin[k]; }
+      }
+      mine->v[lane] = v;
+      mine->i[lane] = ix;
+      __threadfence();
+    }
+    __syncwarp();
+    bool last = false;
+    if (lane == 0) last = flat_arrive(fl.cnt + s * k3 + b, ns);
+    if (__shfl_sync(FULL, (int)last, 0)) {
+      int ci = INT_MAX;
+      if (lane < 2 * D) {
+        float bv = -INFINITY;
+        for (unsigned q = 0; q < ns; ++q) {
+          const CPart<D>* pp = part + b * fl.CP + q;
+          const float v = __ldcg(&pp->v[lane]);
+          const int i = __ldcg(&pp->i[lane]);
+          if (v > bv || (v == bv && i < ci)) { bv = v; ci = i; }
+        }
+      }
+      // sort the <= 32 candidate offsets across the warp (bitonic), then dedup
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+          const int o = __shfl_xor_sync(FULL, ci, jj);
+          const bool up = ((lane & k) == 0);
+          const bool lower = (lane & jj) == 0;
+          ci = (lower == up) ? min(ci, o) : max(ci, o);
+        }
+      }
+      const int prv = __shfl_up_sync(FULL, ci, 1);
+      const bool keep = ci != INT_MAX && (lane == 0 || prv != ci);
+      const unsigned km = __ballot_sync(FULL, keep);
+      const int rank = __popc(km & ((1u << lane) - 1));
+      const int cap = a.cand_cap > 0 && a.cand_cap < HMAX ? a.cand_cap : HMAX;
+      int64_t* cand = a.cand + s * a.cand_ld + b * HMAX;
+      if (keep && rank < cap) cand[rank] = blo + ci;
+      if (lane == 0) {
+        const int w = min(__popc(km), cap);
+        if (w == 0) cand[0] = blo;
+        a.cand_cnt[s * k3 + b] = w ? w : 1;
+      }
+    }
+    j = s1;
+  }
 }
 
 template <typename XT, typename YT, int NT>
@@ -1602,9 +2530,7 @@ __global__ void __launch_bounds__(NT) k_lttb_verify(LttbArgs a) {
   const YT* ys = (const YT*)a.y + s * a.y_ld;
   const int64_t* pos = a.pos + s * a.pos_ld;
   const int64_t prev = pos[b];
-  const double2 c = a.means[s * a.means_ld + b];
-  const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
-                                                    to_f64(ys, prev), c, s_a, s_i);
+  const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
   if (threadIdx.x == 0) {
     a.best[s * k3 + b] = r;
     const bool f = r != pos[b + 1];
@@ -1630,13 +2556,12 @@ __global__ void __launch_bounds__(NT) k_lttb_verify2(LttbArgs a) {
     const int64_t b = (int64_t)a.flist[s * k3 + q] + 1;
     if (b >= k3) continue;
     const int64_t prev = a.best[s * k3 + b - 1];
-    const int64_t r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
-                                                      to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
     if (threadIdx.x == 0) a.best2[s * k3 + b] = r;
   }
 }
 
-__device__ unsigned long long g_repair_scans;  // exact bucket scans done by k_lttb_repair (stats)
+static __device__ unsigned long long g_repair_scans;  // exact bucket scans done by k_lttb_repair (stats)
 
 template <typename XT, typename YT, int NT>
 __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
@@ -1695,8 +2620,7 @@ __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
       if (flag[b - 1] && prev == best[b - 1]) {
         r = a.best2[s * k3 + b];  // precomputed by k_lttb_verify2
       } else {
-        r = block_bucket_argmax<XT, YT, NT>(xs, ys, lbound(a, m, b), lbound(a, m, b + 1), to_f64(xs, prev),
-                                            to_f64(ys, prev), a.means[s * a.means_ld + b], s_a, s_i);
+        r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
         if (threadIdx.x == 0) atomicAdd(&g_repair_scans, 1ull);
       }
       const int64_t was = pos[b + 1];
@@ -1716,13 +2640,97 @@ __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
   }
 }
 
+// Same walk with the chain state staged in shared memory (k3 <= ~7,000): the
+// positions, verified picks, speculative picks and a next-flagged-bucket
+// index (suffix minimum over the flags) live on chip, so each walk step
+// costs shared-memory reads instead of dependent global round trips, and no
+// flagged-list sort is needed.
+__host__ __device__ inline int64_t repair_smem_bytes(int64_t k3) { return 8 * (k3 + 2) + 16 * k3 + 4 * (k3 + 1); }
+
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ double s_a[NT / 32];
+  __shared__ long long s_i[NT / 32];
+  __shared__ int s_cm[NT];
+  const int64_t s = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  long long* P = (long long*)dsm;  // chain positions [k3 + 2]
+  long long* Bv = P + (k3 + 2);    // verified pick given P[b] [k3]
+  long long* B2 = Bv + k3;         // pick given Bv[b-1] (valid where b-1 is flagged) [k3]
+  int* Nx = (int*)(B2 + k3);       // smallest flagged bucket >= i, or INT_MAX [k3 + 1]
+  const int64_t* pos = a.pos + s * a.pos_ld;
+  const int* flag = a.flag + s * k3;
+  for (int64_t i = threadIdx.x; i < k3 + 2; i += NT) P[i] = pos[i];
+  for (int64_t i = threadIdx.x; i < k3; i += NT) {
+    Bv[i] = a.best[s * k3 + i];
+    B2[i] = a.best2[s * k3 + i];
+  }
+  // next-flagged index: per-thread chunk suffix, then a suffix minimum over chunks
+  const int64_t C = (k3 + NT - 1) / NT;
+  const int64_t c0 = threadIdx.x * C, c1 = min(k3, c0 + C);
+  int nxt = INT_MAX;
+  for (int64_t i = c1 - 1; i >= c0; --i) {
+    if (flag[i]) nxt = (int)i;
+    Nx[i] = nxt;
+  }
+  s_cm[threadIdx.x] = nxt;
+  __syncthreads();
+  for (int o = 1; o < NT; o <<= 1) {  // Hillis-Steele suffix minimum
+    const int v = threadIdx.x + o < NT ? s_cm[threadIdx.x + o] : INT_MAX;
+    __syncthreads();
+    s_cm[threadIdx.x] = min(s_cm[threadIdx.x], v);
+    __syncthreads();
+  }
+  const int carry = threadIdx.x + 1 < NT ? s_cm[threadIdx.x + 1] : INT_MAX;
+  for (int64_t i = c0; i < c1; ++i)
+    if (Nx[i] == INT_MAX) Nx[i] = carry;
+  if (threadIdx.x == 0) Nx[k3] = INT_MAX;
+  __syncthreads();
+  int64_t b = 0;
+  while (b < k3) {
+    const int64_t nb = Nx[b];  // next verified mismatch at or after b (synced up to b)
+    if (nb >= k3) break;
+    b = nb;
+    if (threadIdx.x == 0) P[b + 1] = Bv[b];  // exact: P[b] is on the true chain
+    __syncthreads();
+    ++b;
+    while (b < k3) {  // walk exactly until the chain re-joins the verified candidate chain
+      const int64_t prev = P[b];
+      int64_t r;
+      if (Nx[b - 1] == b - 1 && prev == Bv[b - 1]) {
+        r = B2[b];  // precomputed by k_lttb_verify2
+      } else {
+        r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
+        if (threadIdx.x == 0) atomicAdd(&g_repair_scans, 1ull);
+      }
+      const int64_t was = P[b + 1];
+      __syncthreads();
+      if (threadIdx.x == 0) P[b + 1] = r;
+      __syncthreads();
+      ++b;
+      if (r == was) break;
+    }
+  }
+  __syncthreads();
+  int64_t* out = a.out + s * a.n_out;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  for (int64_t i = threadIdx.x; i < k3 + 2; i += NT) {
+    const int64_t p = P[i];
+    out[i] = map ? map[p] : p;
+  }
+}
+
 // ----------------------------------------------------------- misc -------
-__global__ void k_fill(int64_t* p, int64_t n, int64_t v) {
+static __global__ void k_fill(int64_t* p, int64_t n, int64_t v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
 
-__global__ void k_every_nth(int64_t n, int64_t n_out, int64_t* out) {
+static __global__ void k_every_nth(int64_t n, int64_t n_out, int64_t* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n_out) out[i] = (i * n) / n_out;  // downsamplers.py:44-47
 }
@@ -1741,7 +2749,7 @@ __global__ void k_validate(const XT* x, const YT* y, int64_t n, int* flags) {
 
 // TSB1 ingest (seriesio.py:75-95): interleaved little-endian f64 (x, y)
 // pairs -> separate x and y arrays on the device.
-__global__ void k_deinterleave_f64(const double2* __restrict__ in, double* __restrict__ x, double* __restrict__ y,
+static __global__ void k_deinterleave_f64(const double2* __restrict__ in, double* __restrict__ x, double* __restrict__ y,
                                    int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double2 v = __ldcs(in + i);
@@ -1770,7 +2778,7 @@ __device__ __forceinline__ void spin_until_ge(const unsigned* p, unsigned want) 
 
 // CTA g: store this rank's preselected set into peer g's buffer, then raise
 // the peer's data flag.  Waits first for peer g's ack of epoch-2 (same slot).
-__global__ void k_p2p_publish(const int64_t* idx, const double* xs, const double* ys, const int64_t* count, int64_t cap,
+static __global__ void k_p2p_publish(const int64_t* idx, const double* xs, const double* ys, const int64_t* count, int64_t cap,
                               const unsigned long long* peer_bufs, const unsigned long long* peer_pads,
                               const unsigned* own_pad, int64_t G, int64_t rank, unsigned epoch) {
   const int64_t g = blockIdx.x;
@@ -1794,7 +2802,7 @@ __global__ void k_p2p_publish(const int64_t* idx, const double* xs, const double
 
 // CTA g: wait for every row of this epoch, append row g at its offset (rank
 // order), then ack rank g.
-__global__ void k_p2p_merge(const long long* own_buf, const unsigned* own_pad, const unsigned long long* peer_pads,
+static __global__ void k_p2p_merge(const long long* own_buf, const unsigned* own_pad, const unsigned long long* peer_pads,
                             int64_t G, int64_t rank, int64_t cap, unsigned epoch, int64_t* oi, double* ox, double* oy,
                             int64_t* om) {
   const int64_t g = blockIdx.x;
@@ -1824,7 +2832,7 @@ __global__ void k_p2p_merge(const long long* own_buf, const unsigned* own_pad, c
 
 // Rank-order merge straight from the gathered packed messages ([G][3cap+1]:
 // idx | x bits | y bits | count), so no unpacking copies are needed.
-__global__ void k_merge_packed(const long long* buf, int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy,
+static __global__ void k_merge_packed(const long long* buf, int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy,
                                int64_t* om) {
   const int64_t g = blockIdx.x, W = 3 * cap + 1;
   int64_t off = 0;
@@ -1839,7 +2847,7 @@ __global__ void k_merge_packed(const long long* buf, int64_t G, int64_t cap, int
   if (g == G - 1 && threadIdx.x == 0) om[0] = off + n;
 }
 
-__global__ void k_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts,
+static __global__ void k_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts,
                                int64_t G, int64_t cap, int64_t* oi, double* ox, double* oy, int64_t* om) {
   const int64_t g = blockIdx.x;
   int64_t off = 0;

@@ -1,0 +1,228 @@
+// lttb_impl.cuh -- K3 (LTTB) launch templates, instantiated per x dtype in
+// lttb_x_{f32,f64,i64,i32}.cu (parallel compilation); dispatch in lttb_launch.cu.
+#pragma once
+#include "host.cuh"
+
+namespace mmh {
+
+constexpr int64_t JUMP_SMEM_MAX = 200 * 1024;
+// buckets per k_lttb_jump shared-memory segment (two byte tables of seg*SMAX)
+inline int64_t jump_seg(int64_t k3, int smax) {
+  const int64_t cap = (JUMP_SMEM_MAX / (2 * smax)) / 16 * 16;
+  return std::min<int64_t>(cap, (k3 + 15) / 16 * 16);
+}
+
+inline bool use_hull() {
+  static const bool h = env_i64("MMLTTB_K3C_HULL", 0) != 0;  // A/B knob: hull candidates
+  return h;
+}
+inline bool use_chain() {
+  static const bool c = env_i64("MMLTTB_LTTB_CHAIN", 0) != 0;  // A/B knob: old sequential chain
+  return c;
+}
+
+
+template <int SMAX> int jump_attr() {
+  static bool done = false;
+  if (!done) {
+    if (cudaFuncSetAttribute(k_lttb_jump<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JUMP_SMEM_MAX) != cudaSuccess)
+      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_lttb_jump)");
+    done = true;
+  }
+  return MM_OK;
+}
+
+template <int SMAX>
+int launch_jump(LttbArgs a, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  int rc = jump_attr<SMAX>();
+  if (rc) return rc;
+  a.jump_seg = jump_seg(k3, SMAX);
+  k_lttb_jump<SMAX><<<(unsigned)a.B, 1024, (size_t)(2 * a.jump_seg * SMAX), st>>>(a);
+  return check_launch("k_lttb_jump");
+}
+
+template <typename XT, typename YT, int SMAX>
+int launch_tables_jump(LttbArgs a, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  a.tab_ld = tab_ld(k3, SMAX);
+  dim3 g((unsigned)cdiv(k3, NBB), (unsigned)a.B);
+  constexpr int NT = NBB * SMAX < 1024 ? NBB * SMAX : 1024;
+  k_lttb_tables<XT, YT, SMAX, NBB><<<g, NT, 0, st>>>(a);
+  int rc = check_launch("k_lttb_tables");
+  if (rc) return rc;
+  if constexpr (SMAX <= 32) {
+    k_lttb_scan<SMAX, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
+    return check_launch("k_lttb_scan");
+  } else {
+    return launch_jump<SMAX>(a, st);
+  }
+}
+
+// K3c: large buckets (see kernels.cuh): means, hull candidates, candidate
+// tables, jump (positions), verification, repair + output
+template <typename XT, typename YT, int H>
+int launch_lttb_large(LttbArgs a, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  Carve cv{(char*)a.tables, INT64_MAX / 4};
+  a.means = cv.take<double2>(a.B * k3);
+  a.means_ld = k3;
+  a.cand = cv.take<int64_t>(a.B * k3 * HMAX);
+  a.cand_ld = k3 * H;
+  a.cand_cnt = cv.take<int>(a.B * k3);
+  a.tab_ld = tab_ld(k3, H);
+  unsigned char* tabs = cv.take<unsigned char>(a.B * tab_ld(k3, HMAX));
+  a.pos = cv.take<int64_t>(a.B * (k3 + 2));
+  a.pos_ld = k3 + 2;
+  a.best = cv.take<int64_t>(a.B * k3);
+  a.flag = cv.take<int>(a.B * k3);
+  a.yrange = cv.take<double2>(a.B * k3);
+  a.best2 = cv.take<int64_t>(a.B * k3);
+  a.flist = cv.take<int>(a.B * k3);
+  a.fcount = cv.take<int>(a.B);
+  a.merr = cv.take<double2>(a.B * k3);
+  // affine-x detection in the means pass (A/B knob MMLTTB_K3C_XAFF=0: always load x)
+  static const bool xaff_on = env_i64("MMLTTB_K3C_XAFF", 1) != 0;
+  a.xaff = cv.take<XAff>(a.B * k3);
+  if (!xaff_on) a.xaff = nullptr;
+  a.tables = tabs;
+  a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", H);  // test knob: a poor heuristic must still be exact
+  // flat passes (one series with closed-form buckets; A/B knob MMLTTB_K3C_FLAT=0: per-bucket CTAs)
+  static const bool flat_on = env_i64("MMLTTB_K3C_FLAT", 1) != 0;
+  static const int64_t mv = env_i64("MMLTTB_K3C_MEANS", 0);
+  const bool flat = flat_on && mv == 0 && a.B == 1 && !a.bounds && !a.m_dev;
+  a.xrange = cv.take<double2>(a.B * k3);
+  FlatArgs fl{}, fl_c{};  // fl_c: the candidate pass (16 resident warps per SM instead of 24)
+  unsigned* fcnt = nullptr;
+  if (flat) {
+    const int64_t L = a.n - 2;
+    auto plan = [&](FlatArgs& f, int64_t warps) {
+      f.W = std::max<int64_t>(1, std::min<int64_t>(warps, cdiv(L, 256)));
+      f.E = cdiv(L, f.W);
+      f.W = cdiv(L, f.E);
+      f.CP = cdiv(cdiv(L, k3), f.E) + 1;
+      return f.CP <= flat_cp_max(k3);
+    };
+    if (!plan(fl, K3C_FLAT_WARPS) || !plan(fl_c, K3C_FLAT_WARPS * 2 / 3)) return fail(MM_ERANGE, "K3c flat partial slots");
+    fcnt = cv.take<unsigned>(3 * k3 + 1);  // arrival counters of the three passes + the failed-certification count
+    fl.ucount = (int*)(fcnt + 3 * k3);
+    fl.part = cv.take<unsigned char>(k3 * flat_cp_max(k3) * K3C_FLAT_PART);
+    fl.ulist = cv.take<int>(k3);
+    fl_c.part = fl.part;
+    if (cudaMemsetAsync(fcnt, 0, (size_t)(3 * k3 + 1) * sizeof(unsigned), st) != cudaSuccess)
+      return fail(MM_ECUDA, "memset");
+  }
+  const unsigned flat_grid = (unsigned)cdiv(fl.W, 8);
+  // default: any-order means + error bounds (one bandwidth-bound pass; the
+  // exact argmaxes certify against the bounds).  A/B knob MMLTTB_K3C_MEANS:
+  // 1 / 2 = the exact in-order chains (one warp per bucket, one / two tiles ahead)
+  static const int cforce = (int)env_i64("MMLTTB_K3C_CERT_FORCE", 0);  // test knob: every certification fails
+  a.cert_force = cforce;
+  if (mv == 1 || mv == 2) {
+    a.merr = nullptr;
+    a.xaff = nullptr;
+    if (mv == 1) k_lttb_means_staged<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
+    else k_lttb_means_staged2<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
+  } else if (flat) {
+    fl.cnt = fcnt;
+    k_lttb_means_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+  } else {
+    static const int64_t mnt = env_i64("MMLTTB_K3C_MEANS_NT", 256);
+    const dim3 g((unsigned)k3, (unsigned)a.B);
+    if (mnt == 128) k_lttb_means_approx<XT, YT, 128, 8><<<g, 128, 0, st>>>(a);
+    else k_lttb_means_approx<XT, YT, 256, 4><<<g, 256, 0, st>>>(a);
+  }
+  int rc = check_launch("k_lttb_means");
+  if (rc) return rc;
+  if (use_hull()) {
+    k_lttb_hull<XT, YT, H><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);
+    if ((rc = check_launch("k_lttb_hull"))) return rc;
+  } else {
+    static const int64_t dnt = env_i64("MMLTTB_K3C_DIRCAND_NT", 64);  // A/B knob (64: 64 vs 68 us at 128 on C2)
+    static const bool dflat = env_i64("MMLTTB_K3C_DIRCAND_FLAT", 0) != 0;  // A/B knob: flat candidate pass
+    if (flat && dflat) {
+      fl_c.cnt = fcnt + k3;
+      static_assert(sizeof(CPart<H / 2>) <= K3C_FLAT_PART, "flat partial buffer");
+      k_lttb_dircand_flat<XT, YT, H, H / 2, 4><<<dim3((unsigned)cdiv(fl_c.W, 8), 1), 256, 0, st>>>(a, fl_c);
+    } else if (dnt == 128) k_lttb_dircand<XT, YT, H, H / 2, 128><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
+    else k_lttb_dircand<XT, YT, H, H / 2, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
+    if ((rc = check_launch("k_lttb_dircand"))) return rc;
+  }
+  k_lttb_ctables<XT, YT, H><<<dim3((unsigned)cdiv(k3, 1024 / H), (unsigned)a.B), 1024, 0, st>>>(a);
+  if ((rc = check_launch("k_lttb_ctables"))) return rc;
+  k_lttb_scan<H, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
+  if ((rc = check_launch("k_lttb_scan"))) return rc;
+  if (cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
+  static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);  // A/B knob (64: 30 vs 37.5 us at 256 on C2)
+  if (flat) {
+    fl.cnt = fcnt + 2 * k3;
+    k_lttb_verify_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+    if ((rc = check_launch("k_lttb_verify_flat"))) return rc;
+    k_lttb_verify_fix<XT, YT, 256><<<dim3(148, 1), 256, 0, st>>>(a, fl);
+    if ((rc = check_launch("k_lttb_verify_fix"))) return rc;
+  } else {
+    if (vnt == 256) k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
+    else k_lttb_verify<XT, YT, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
+    if ((rc = check_launch("k_lttb_verify"))) return rc;
+  }
+  static const int64_t v2 = env_i64("MMLTTB_K3C_VERIFY2_NT", 256);  // A/B knob
+  if (v2 == 128) k_lttb_verify2<XT, YT, 128><<<dim3(148, (unsigned)a.B), 128, 0, st>>>(a);
+  else k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
+  if ((rc = check_launch("k_lttb_verify2"))) return rc;
+  static const int64_t rp = env_i64("MMLTTB_K3C_REPAIR_NT", 512);  // A/B knob (512: 22.1 vs 24.4 us at 1024 on C2)
+  // chain state staged in shared memory when it fits (A/B knob MMLTTB_K3C_REPAIR_SMEM=0: global)
+  static const bool rsm = env_i64("MMLTTB_K3C_REPAIR_SMEM", 1) != 0;
+  constexpr int64_t RSMEM_MAX = 200 * 1024;
+  const int64_t rbytes = repair_smem_bytes(k3);
+  if (rsm && rbytes <= RSMEM_MAX) {
+    auto kern = k_lttb_repair_smem<XT, YT, 512>;
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RSMEM_MAX) != cudaSuccess)
+        return fail(MM_ECUDA, "cudaFuncSetAttribute(k_lttb_repair_smem)");
+      attr = true;
+    }
+    kern<<<(unsigned)a.B, 512, (size_t)rbytes, st>>>(a);
+    return check_launch("k_lttb_repair_smem");
+  }
+  if (rp == 1024) k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
+  else k_lttb_repair<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
+  return check_launch("k_lttb_repair");
+}
+
+template <typename XT, typename YT>
+int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  if (a.B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
+  if (use_tables(s)) {
+    switch (smax_for(s)) {
+      case 4: return launch_tables_jump<XT, YT, 4>(a, st);
+      case 8: return launch_tables_jump<XT, YT, 8>(a, st);
+      case 16: return launch_tables_jump<XT, YT, 16>(a, st);
+      case 32: return launch_tables_jump<XT, YT, 32>(a, st);
+      default: return launch_tables_jump<XT, YT, 64>(a, st);
+    }
+  }
+  if (!use_chain()) {
+    static const int64_t h = env_i64("MMLTTB_K3C_HMAX", 16);  // A/B knob: 16 or 32 candidates
+    if (h == 8) return launch_lttb_large<XT, YT, 8>(a, st);  // 4 directions
+    return h == 32 ? launch_lttb_large<XT, YT, 32>(a, st) : launch_lttb_large<XT, YT, 16>(a, st);
+  }
+  a.means = reinterpret_cast<double2*>(a.tables);
+  a.means_ld = k3;
+  const int64_t n = a.B * k3;
+  k_lttb_means<XT, YT><<<(unsigned)cdiv(n, 128), 128, 0, st>>>(a);
+  int rc = check_launch("k_lttb_means");
+  if (rc) return rc;
+  k_lttb_chain<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
+  return check_launch("k_lttb_chain");
+}
+
+template <typename XT>
+int launch_lttb_x(LttbArgs a, int ydt, int64_t s, cudaStream_t st) {
+  if (ydt == MM_F32) return launch_lttb_t<XT, float>(a, s, st);
+  if (ydt == MM_F64) return launch_lttb_t<XT, double>(a, s, st);
+  return fail(MM_EINVAL, "y dtype");
+}
+
+}  // namespace mmh

@@ -1,0 +1,15 @@
+// lttb_x_f32.cu -- K3 launchers for x = float (see lttb_impl.cuh)
+#include "lttb_impl.cuh"
+
+namespace mmh {
+
+int launch_lttb_f32(LttbArgs a, int ydt, int64_t s, cudaStream_t st) { return launch_lttb_x<float>(a, ydt, s, st); }
+
+// k_lttb_repair's counter is a per-translation-unit device variable
+int64_t repair_scans_f32() {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_repair_scans, sizeof v) != cudaSuccess) return -1;
+  return (int64_t)v;
+}
+
+}  // namespace mmh

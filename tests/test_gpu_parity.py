@@ -314,6 +314,24 @@ def test_lttb_large_bucket_repair_path():
         assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+def test_lttb_large_bucket_certification_ties():
+    """K3c means are any-order sums certified against an error bound; duplicated
+    points tie in every bucket, so every certification fails and each bucket
+    falls back to the reference's in-order mean (exact re-scan)."""
+    rng = np.random.Generator(np.random.PCG64(11))
+    n = 200_000
+    x = np.repeat(np.arange(n // 2, dtype=np.float64) * 0.37, 2)
+    y = np.repeat(np.cumsum(rng.standard_normal(n // 2)), 2)
+    for n_out in (100, 1001):
+        got = mm.lttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out).cpu().numpy()
+        assert np.array_equal(got, O.lttb(x, y, n_out))
+    # integer-valued data: the means are exact (no certification needed)
+    xi = np.arange(n, dtype=np.int64)
+    yi = np.cumsum(rng.integers(-5, 6, n)).astype(np.float64)
+    got = mm.lttb(torch.from_numpy(xi).to(DEV), torch.from_numpy(yi).to(DEV), 150).cpu().numpy()
+    assert np.array_equal(got, O.lttb(xi, yi, 150))
+
+
 def test_lttb_large_bucket_degenerate():
     """Ties everywhere (constant / collinear / duplicated points) through K3c."""
     n = 100_000
