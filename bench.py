@@ -265,14 +265,23 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------- GPU leg ------
+def _pinned_copy(t):
+    """Device tensor -> pinned host copy, without a pageable intermediate (8 ranks x 12 GB of
+    inputs must fit the host's memory once, not twice)."""
+    import torch
+
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    torch.cuda.synchronize()
+    return h
+
+
 def _e2e(step, x, y, e2e_steps, n_out, r_ps, batch, op, ws, dist):
     """Public API with pinned HOST buffers: H2D of y (+ zero-copy x gather)
     and the D2H of the indices are inside every timed step."""
     import torch
 
-    yh = y.cpu().pin_memory()
-    xh = x.cpu().pin_memory()
-    torch.cuda.synchronize()
+    yh, xh = _pinned_copy(y), _pinned_copy(x)
     res = step(xh, yh)  # warm the host path once
     if ws > 1:
         dist.barrier()
@@ -300,8 +309,7 @@ def _e2e_sharded(x, y, e2e_steps, n, n_out, r_ps, ws, dist, dev):
 
     from paper_2305_00332_b200 import sharding
 
-    yh = y.cpu().pin_memory()
-    xh = x.cpu().pin_memory()
+    yh, xh = _pinned_copy(y), _pinned_copy(x)
 
     def host_step():
         yd = yh.to(dev, non_blocking=True)

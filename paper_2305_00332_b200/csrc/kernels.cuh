@@ -2727,29 +2727,50 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
     if (Nx[i] == INT_MAX) Nx[i] = carry;
   if (threadIdx.x == 0) Nx[k3] = INT_MAX;
   __syncthreads();
-  int64_t b = 0;
-  while (b < k3) {
-    const int64_t nb = Nx[b];  // next verified mismatch at or after b (synced up to b)
-    if (nb >= k3) break;
-    b = nb;
-    if (threadIdx.x == 0) P[b + 1] = Bv[b];  // exact: P[b] is on the true chain
-    __syncthreads();
-    ++b;
-    while (b < k3) {  // walk exactly until the chain re-joins the verified candidate chain
-      const int64_t prev = P[b];
-      int64_t r;
-      if (Nx[b - 1] == b - 1 && prev == Bv[b - 1]) {
-        r = B2[b];  // precomputed by k_lttb_verify2
-      } else {
-        r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
-        if (threadIdx.x == 0) atomicAdd(&g_repair_scans, 1ull);
+  // Thread 0 walks the chain alone (shared-memory state only, no barrier per
+  // step) and hands a bucket to the whole CTA only when it needs an exact scan.
+  __shared__ long long s_rb, s_rp;  // scan request: bucket, previous pick (-1: walk finished)
+  int64_t b = 0;                    // thread 0: chain synced up to b
+  bool walking = false;             // thread 0: inside a deviation
+  int64_t scanned = -1;             // thread 0: result of the last requested scan
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_rb = -1;
+      while (true) {
+        if (!walking) {
+          const int64_t nb = b < k3 ? Nx[b] : INT_MAX;  // next verified mismatch at or after b
+          if (nb >= k3) break;
+          b = nb;
+          P[b + 1] = Bv[b];  // exact: P[b] is on the true chain
+          ++b;
+          walking = true;
+        }
+        if (b >= k3) break;
+        const int64_t prev = P[b];
+        int64_t r;
+        if (scanned >= 0) {
+          r = scanned;
+          scanned = -1;
+        } else if (Nx[b - 1] == b - 1 && prev == Bv[b - 1]) {
+          r = B2[b];  // precomputed by k_lttb_verify2
+        } else {
+          s_rb = b;
+          s_rp = prev;
+          break;
+        }
+        const int64_t was = P[b + 1];
+        P[b + 1] = r;
+        ++b;
+        if (r == was) walking = false;  // re-joined the verified candidate chain
       }
-      const int64_t was = P[b + 1];
-      __syncthreads();
-      if (threadIdx.x == 0) P[b + 1] = r;
-      __syncthreads();
-      ++b;
-      if (r == was) break;
+    }
+    __syncthreads();
+    const int64_t rb = s_rb;
+    if (rb < 0) break;
+    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, rb, s_rp, s_a, s_i);
+    if (threadIdx.x == 0) {
+      scanned = r;
+      atomicAdd(&g_repair_scans, 1ull);
     }
   }
   __syncthreads();
