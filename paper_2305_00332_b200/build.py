@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         procs = []
         for src in SRCS:
             obj = OBJ / (src.stem + ".o")
-            cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas=-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
+            extra = os.environ.get("MMLTTB_NVCC_EXTRA", "").split()  # A/B builds (tools/): e.g. -DK3C_UN_DIR=4
+            cmd = [nvcc(), *NVCC_FLAGS, *extra, *(["-Xptxas=-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
             procs.append((src, obj, subprocess.Popen(cmd)))
         bad = [str(src) for src, _, p in procs if p.wait() != 0]
         if bad:

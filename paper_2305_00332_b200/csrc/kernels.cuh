@@ -1995,6 +1995,9 @@ __device__ int64_t block_bucket_argmax_cert(const LttbArgs& a, int64_t s, int64_
   __syncthreads();
   if (ok) return r;
   // failed: the reference's own in-order mean, kept for later scans of bucket b
+#ifdef MM_REPAIR_TRACE
+  if (threadIdx.x == 0) printf("exact-mean fallback: bucket %lld\n", (long long)b);
+#endif
   const double2 ce2 = block_exact_mean<XT, YT, NT>(a, xs, ys, m, b);
   if (threadIdx.x == 0) { *mp = ce2; *ep = make_double2(0.0, 0.0); }
   return block_bucket_argmax<XT, YT, NT>(xs, ys, lo, hi, ax, ay, ce2, s_a, s_i, xa);
@@ -2702,16 +2705,18 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
   const int64_t* pos = a.pos + s * a.pos_ld;
   const int* flag = a.flag + s * k3;
   for (int64_t i = threadIdx.x; i < k3 + 2; i += NT) P[i] = pos[i];
-  for (int64_t i = threadIdx.x; i < k3; i += NT) {
+  for (int64_t i = threadIdx.x; i < k3; i += NT) {  // coalesced staging (flags into Nx first)
     Bv[i] = a.best[s * k3 + i];
     B2[i] = a.best2[s * k3 + i];
+    Nx[i] = flag[i];
   }
-  // next-flagged index: per-thread chunk suffix, then a suffix minimum over chunks
+  __syncthreads();
+  // next-flagged index: per-thread chunk suffix (shared memory), then a suffix minimum over chunks
   const int64_t C = (k3 + NT - 1) / NT;
   const int64_t c0 = threadIdx.x * C, c1 = min(k3, c0 + C);
   int nxt = INT_MAX;
   for (int64_t i = c1 - 1; i >= c0; --i) {
-    if (flag[i]) nxt = (int)i;
+    if (Nx[i]) nxt = (int)i;
     Nx[i] = nxt;
   }
   s_cm[threadIdx.x] = nxt;
@@ -2729,6 +2734,11 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
   __syncthreads();
   // Thread 0 walks the chain alone (shared-memory state only, no barrier per
   // step) and hands a bucket to the whole CTA only when it needs an exact scan.
+#ifdef MM_REPAIR_TRACE
+  const long long t_walk0 = clock64();
+  long long t_scan = 0;
+  int n_scan = 0;
+#endif
   __shared__ long long s_rb, s_rp;  // scan request: bucket, previous pick (-1: walk finished)
   int64_t b = 0;                    // thread 0: chain synced up to b
   bool walking = false;             // thread 0: inside a deviation
@@ -2767,12 +2777,26 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
     __syncthreads();
     const int64_t rb = s_rb;
     if (rb < 0) break;
+#ifdef MM_REPAIR_TRACE
+    const long long t0s = clock64();
+#endif
     const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, rb, s_rp, s_a, s_i);
     if (threadIdx.x == 0) {
       scanned = r;
       atomicAdd(&g_repair_scans, 1ull);
+#ifdef MM_REPAIR_TRACE
+      t_scan += clock64() - t0s;
+      ++n_scan;
+#endif
     }
   }
+#ifdef MM_REPAIR_TRACE
+  if (threadIdx.x == 0) {
+    int nflag = 0;
+    for (int64_t i = 0; i < k3; i = Nx[i] + 1) { if (Nx[i] >= k3) break; ++nflag; }
+    printf("repair: walk+scans %lld cycles, %d scans %lld cycles, %d flagged\n", clock64() - t_walk0, n_scan, t_scan, nflag);
+  }
+#endif
   __syncthreads();
   int64_t* out = a.out + s * a.n_out;
   const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
