@@ -10,9 +10,14 @@
 //     k_lttb_jump      T_b[p] = argmax_j area(P_p, P_j, C_{b+1}) built in
 //                      parallel, the bucket chain resolved by pointer
 //                      jumping in shared memory: _kernels.py:81-119
-// K3b k_lttb_means +   LTTB over large buckets: parallel in-order means,
-//     k_lttb_chain     then one CTA walks the chain, threads evaluating the
-//                      bucket's triangle areas: _kernels.py:81-119
+// K3c k_lttb_means_flat LTTB over large buckets (> 64 points, e.g. full
+//     -> dircand ->    `lttb`): certified any-order means, direction-sampled
+//     ctables -> scan  candidates, candidate tables + scan, every bucket
+//     -> verify_flat   re-scanned exactly (verify), speculative next-bucket
+//     -> verify2 ->    picks (verify2) and a repair walk: exact whatever the
+//     repair_smem      heuristic (_kernels.py:81-119)
+// K3b k_lttb_means +   (A/B knob only) in-order means, then one CTA walks
+//     k_lttb_chain     the chain evaluating each bucket's areas
 //
 // Arithmetic parity: extrema compare IEEE total-order
 // integer keys (-0.0 < +0.0; f32 keys order exactly like the f64 keys the
