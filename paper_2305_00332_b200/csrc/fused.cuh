@@ -125,9 +125,9 @@ __device__ __forceinline__ void fused_phase23(const FusedArgs& a, int64_t s, uns
     if (valid) {
       const double ax = px(ap), ay = (double)s_py[ap];
       const double2 c = s_mean[b];
-      double best = -1.0;
+      long long best = -1;
       for (int64_t j = blo; j < bhi; ++j) {
-        const double ar = lttb_area(ax, ay, c.x, c.y, px(j), (double)s_py[j]);
+        const long long ar = lttb_area_key(ax, ay, c.x, c.y, px(j), (double)s_py[j]);
         if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
       }
     }
@@ -560,9 +560,9 @@ __global__ void __launch_bounds__(NT) k_post_fused(PostArgs a) {
     if (valid) {
       const double ax = X(ap), ay = Y(ap);
       const double2 c = s_mean[b];
-      double best = -1.0;
+      long long best = -1;
       for (int64_t j = blo; j < bhi; ++j) {
-        const double ar = lttb_area(ax, ay, c.x, c.y, X(j), Y(j));
+        const long long ar = lttb_area_key(ax, ay, c.x, c.y, X(j), Y(j));
         if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
       }
     }
@@ -667,9 +667,9 @@ __global__ void __launch_bounds__(NT) k_post_smem(PostArgs a) {
     if (valid) {
       const double ax = s_px[ap], ay = s_py[ap];
       const double2 c = s_mean[b];
-      double best = -1.0;
+      long long best = -1;
       for (int64_t j = blo; j < bhi; ++j) {
-        const double ar = lttb_area(ax, ay, c.x, c.y, s_px[j], s_py[j]);
+        const long long ar = lttb_area_key(ax, ay, c.x, c.y, s_px[j], s_py[j]);
         if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
       }
     }
@@ -736,9 +736,9 @@ __global__ void __launch_bounds__(NT) k_post_coop(PairArgs pa, LttbArgs la, int6
         cy = __ldcg(py + m - 1);
       }
       const double ax = __ldcg(px + ap), ay = __ldcg(py + ap);
-      double best = -1.0;
+      long long best = -1;
       for (int64_t j = blo; j < bhi; ++j) {
-        const double ar = lttb_area(ax, ay, cx, cy, __ldcg(px + j), __ldcg(py + j));
+        const long long ar = lttb_area_key(ax, ay, cx, cy, __ldcg(px + j), __ldcg(py + j));
         if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
       }
     }

@@ -720,6 +720,17 @@ __device__ __forceinline__ double lttb_area(double ax, double ay, double cx, dou
                         __dmul_rn(__dsub_rn(ax, xj), __dsub_rn(cy, ay))));
 }
 
+// lttb_area as an ordering key: the bit pattern of |area| (non-negative doubles
+// order like their values), NaN -> -1 so it never wins -- the reference's
+// `area > best_area` from -1.0 without fp64 compares (DSETP issues on B200's
+// narrow XU pipe)
+__device__ __forceinline__ long long lttb_area_key(double ax, double ay, double cx, double cy, double xj, double yj) {
+  const long long k = __double_as_longlong(__dsub_rn(__dmul_rn(__dsub_rn(ax, cx), __dsub_rn(yj, ay)),
+                                                     __dmul_rn(__dsub_rn(ax, xj), __dsub_rn(cy, ay)))) &
+                      0x7fffffffffffffffLL;
+  return k > 0x7ff0000000000000LL ? -1LL : k;
+}
+
 // XU-free element arithmetic for the flat passes.  On B200 the fp64 compares
 // (DSETP, behind fmin/fmax and `>` on doubles) and the int64 -> f64 / f64 ->
 // f32 conversions issue on the narrow XU pipe, which ncu showed saturated
@@ -832,9 +843,9 @@ __global__ void __launch_bounds__(NBB * SMAX < 1024 ? NBB * SMAX : 1024) k_lttb_
     if (valid) {
       const double ax = to_f64(xs, ap), ay = to_f64(ys, ap);
       const double2 c = s_mean[bi];
-      double best = -1.0;
+      long long best = -1;
       for (int64_t j = blo; j < bhi; ++j) {
-        const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+        const long long ar = lttb_area_key(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
         if (ar > best) { best = ar; r = (unsigned char)(j - blo); }  // strict '>' (:115)
       }
     }
@@ -1287,7 +1298,7 @@ __global__ void __launch_bounds__(32) k_lttb_means_staged2(LttbArgs a) {
 // K3b, part 2: one CTA per series carries the bucket-to-bucket dependency.
 template <typename XT, typename YT, int NT>
 __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
-  __shared__ double s_area[NT / 32];
+  __shared__ long long s_area[NT / 32];
   __shared__ long long s_idx[NT / 32];
   __shared__ long long s_prev;
   const int64_t s = blockIdx.x;
@@ -1305,26 +1316,26 @@ __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
     const int64_t bhi = lbound(a, m, b + 1);
     const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
     const double2 c = means[b];
-    double best = -1.0;
+    long long best = -1;
     long long bi = INT64_MAX;
     for (int64_t j = blo + threadIdx.x; j < bhi; j += NT) {
-      const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+      const long long ar = lttb_area_key(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
       if (ar > best) { best = ar; bi = j; }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      const double oa = __shfl_xor_sync(FULL, best, o);
+      const long long oa = __shfl_xor_sync(FULL, best, o);
       const long long oi = __shfl_xor_sync(FULL, bi, o);
       if (oa > best || (oa == best && oi < bi)) { best = oa; bi = oi; }
     }
     if (lane == 0) { s_area[wid] = best; s_idx[wid] = bi; }
     __syncthreads();
     if (wid == 0) {
-      best = lane < NT / 32 ? s_area[lane] : -1.0;
+      best = lane < NT / 32 ? s_area[lane] : -1LL;
       bi = lane < NT / 32 ? s_idx[lane] : INT64_MAX;
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
-        const double oa = __shfl_xor_sync(FULL, best, o);
+        const long long oa = __shfl_xor_sync(FULL, best, o);
         const long long oi = __shfl_xor_sync(FULL, bi, o);
         if (oa > best || (oa == best && oi < bi)) { best = oa; bi = oi; }
       }
@@ -1664,10 +1675,10 @@ __global__ void __launch_bounds__(1024) k_lttb_ctables(LttbArgs a) {
     const double ax = to_f64(xs, ap), ay = to_f64(ys, ap);
     const double2 c = a.means[s * a.means_ld + b];
     const int nc = cnt[b];
-    double bestv = -1.0;
+    long long bestv = -1;
     for (int q = 0; q < nc; ++q) {
       const int64_t j = cand[b * HMAX + q];
-      const double ar = lttb_area(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+      const long long ar = lttb_area_key(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
       if (ar > bestv) { bestv = ar; r = (unsigned char)q; }
     }
   }
