@@ -332,6 +332,30 @@ def test_lttb_large_bucket_certification_ties():
     assert np.array_equal(got, O.lttb(xi, yi, 150))
 
 
+@pytest.mark.parametrize("xkind", ["f64_even", "f32_even", "i64_irregular", "i32_arange", "f64_large"])
+def test_lttb_large_bucket_x_kinds(xkind):
+    """K3c flat passes across x layouts: evenly spaced float timestamps (affine by
+    formula), irregular integers (x loaded), int32 and large-magnitude float x
+    (inexact x means, so x certification matters too)."""
+    rng = np.random.Generator(np.random.PCG64(hash(xkind) % 2**32))
+    n = 400_003
+    if xkind == "f64_even":
+        x = 1.7e9 + 0.25 * np.arange(n, dtype=np.float64)
+    elif xkind == "f32_even":
+        x = (np.arange(n, dtype=np.float64) * 0.5).astype(np.float32)
+    elif xkind == "i64_irregular":
+        x = np.cumsum(rng.integers(1, 5, n)).astype(np.int64)
+    elif xkind == "i32_arange":
+        x = np.arange(n, dtype=np.int32) * 3
+    else:
+        x = np.cumsum(rng.exponential(1.0, n)) * 1e12
+    for ydt in (np.float64, np.float32):
+        y = (np.cumsum(rng.standard_normal(n)) * 1e3).astype(ydt)
+        for n_out in (300, 1234):
+            got = mm.lttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out).cpu().numpy()
+            assert np.array_equal(got, O.lttb(x, y, n_out)), (xkind, ydt, n_out)
+
+
 def test_lttb_large_bucket_degenerate():
     """Ties everywhere (constant / collinear / duplicated points) through K3c."""
     n = 100_000
