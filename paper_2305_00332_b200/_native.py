@@ -137,6 +137,41 @@ def check(rc: int, what: str, n: int | None = None) -> None:
     raise errors.CudaError(f"{what} failed ({rc}): {msg}")
 
 
+_wsb_cache: dict = {}
+
+
+def workspace_bytes(op: int, B: int, n: int, n_out: int, r_ps: int, ydt: int) -> int:
+    """mmlttb_workspace_bytes, memoised (a pure function of its arguments)."""
+    key = (op, B, n, n_out, r_ps, ydt)
+    v = _wsb_cache.get(key)
+    if v is None:
+        v = _wsb_cache[key] = int(lib().mmlttb_workspace_bytes(op, B, n, n_out, r_ps, ydt))
+    return v
+
+
+_ws_local = threading.local()
+WS_CACHE_MAX = 64 << 20  # larger workspaces are allocated per call
+
+
+def stream_workspace(nbytes: int, device: torch.device, stream: int, n: int | None = None) -> torch.Tensor:
+    """Workspace reused across calls on the same (thread, device, stream).
+
+    Calls on one stream are ordered, so a later call's kernels only start after
+    the earlier call's are done with the buffer; the cache is thread-local so two
+    host threads sharing a stream never interleave their use of one buffer.
+    """
+    if nbytes > WS_CACHE_MAX:
+        return workspace(nbytes, device, n)
+    d = getattr(_ws_local, "d", None)
+    if d is None:
+        d = _ws_local.d = {}
+    key = (device.index, stream)
+    t = d.get(key)
+    if t is None or t.numel() < nbytes:
+        t = d[key] = workspace(max(int(nbytes), 1 << 20), device, n)
+    return t
+
+
 def workspace(nbytes: int, device: torch.device, n: int | None = None) -> torch.Tensor:
     try:
         return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)

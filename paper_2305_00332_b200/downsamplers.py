@@ -287,10 +287,11 @@ def lttb(series, n_out, *args, **kw):
     if x is not None and not x.is_cuda:
         x = x.to(b.device)  # full LTTB reads every x
     with _ctx(b):
-        wsb = N.lib().mmlttb_workspace_bytes(N.OP_LTTB, b.B, b.n, n_out, 0, ydt)
-        ws = N.workspace(wsb, b.device, b.n)
+        st = N.stream_ptr(b.device)
+        wsb = N.workspace_bytes(N.OP_LTTB, b.B, b.n, n_out, 0, ydt)
+        ws = N.stream_workspace(wsb, b.device, st, b.n)
         N.check(N.lib().mmlttb_lttb(x.data_ptr(), xdt, b.x_ld, b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out,
-                                    out.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(b.device)), "lttb", b.n)
+                                    out.data_ptr(), ws.data_ptr(), wsb, st), "lttb", b.n)
     return b.ret(out)
 
 
@@ -324,10 +325,11 @@ def _minmaxlttb_batch(b, n_out: int, r_ps: int):
     xdt, ydt = _codes(b)
     out = torch.empty((b.B, n_out), dtype=torch.int64, device=b.device)
     with _ctx(b):
-        wsb = N.lib().mmlttb_workspace_bytes(N.OP_MINMAXLTTB, b.B, b.n, n_out, r_ps, ydt)
-        ws = N.workspace(wsb, b.device, b.n)
+        st = N.stream_ptr(b.device)
+        wsb = N.workspace_bytes(N.OP_MINMAXLTTB, b.B, b.n, n_out, r_ps, ydt)
+        ws = N.stream_workspace(wsb, b.device, st, b.n)
         N.check(N.lib().mmlttb_minmaxlttb(N.ptr(b.x), xdt, b.x_ld, b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out,
-                                          r_ps, out.data_ptr(), None, ws.data_ptr(), wsb, N.stream_ptr(b.device)),
+                                          r_ps, out.data_ptr(), None, ws.data_ptr(), wsb, st),
                 "minmaxlttb", b.n)
     b.post_check(ws)
     return b.ret(out)
