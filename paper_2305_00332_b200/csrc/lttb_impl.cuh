@@ -12,6 +12,12 @@ inline int64_t jump_seg(int64_t k3, int smax) {
   return std::min<int64_t>(cap, (k3 + 15) / 16 * 16);
 }
 
+// A/B knobs: points in flight per lane in the flat verification (default 8: 26 vs 29 us on
+// C2) and means (default 4: 43 vs 45 us) passes
+inline int64_t flat_un(bool verify) {
+  static const int64_t uv = env_i64("MMLTTB_K3C_VERIFY_UN", 8), um = env_i64("MMLTTB_K3C_MEANS_UN", 4);
+  return verify ? uv : um;
+}
 inline bool use_hull() {
   static const bool h = env_i64("MMLTTB_K3C_HULL", 0) != 0;  // A/B knob: hull candidates
   return h;
@@ -125,7 +131,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
     else k_lttb_means_staged2<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
   } else if (flat) {
     fl.cnt = fcnt;
-    k_lttb_means_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+    if (flat_un(false) == 8) k_lttb_means_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+    else k_lttb_means_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
   } else {
     static const int64_t mnt = env_i64("MMLTTB_K3C_MEANS_NT", 256);
     const dim3 g((unsigned)k3, (unsigned)a.B);
@@ -156,7 +163,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);  // A/B knob (64: 30 vs 37.5 us at 256 on C2)
   if (flat) {
     fl.cnt = fcnt + 2 * k3;
-    k_lttb_verify_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+    if (flat_un(true) == 4) k_lttb_verify_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+    else k_lttb_verify_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
     if ((rc = check_launch("k_lttb_verify_flat"))) return rc;
     k_lttb_verify_fix<XT, YT, 256><<<dim3(148, 1), 256, 0, st>>>(a, fl);
     if ((rc = check_launch("k_lttb_verify_fix"))) return rc;
