@@ -1109,6 +1109,80 @@ __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
   }
 }
 
+// Segmented chain resolution (k3 <= 64 * LTTB_SEG): two short kernels
+// instead of one CTA scanning every map.  Kernel 1: one warp per segment of
+// LTTB_SEG buckets stages the segment's transition maps in shared memory and
+// lane p walks them from entry p, overwriting each map row in place with the
+// path: row b becomes (T_b o ... o T_first)(p) for every entry p.  The
+// segment's last row is then its composed map M_s.  Kernel 2: each segment
+// composes M_0 .. M_{s-1} from entry 0 (the fixed first point) to get its
+// entry e_s, and every bucket's pick is row_b[e_s].
+constexpr int LTTB_SEG = 64;
+
+template <int W>
+__global__ void __launch_bounds__(32) k_lttb_seg_paths(LttbArgs a) {
+  __shared__ unsigned char t[LTTB_SEG][W];
+  const int64_t s = blockIdx.y, seg = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t b0 = seg * LTTB_SEG;
+  const int n = (int)min((int64_t)LTTB_SEG, k3 - b0);
+  unsigned char* tab = a.tables + s * a.tab_ld + b0 * W;
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n * W; i += 32) t[i / W][i % W] = tab[i];
+  __syncwarp();
+  if (lane < W) {
+    int st = lane;
+    for (int i = 0; i < n; ++i) {
+      st = t[i][st];
+      tab[i * W + lane] = (unsigned char)st;  // path row (reads come from the staged copy)
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(64) k_lttb_seg_emit(LttbArgs a) {
+  __shared__ int s_e;
+  const int64_t s = blockIdx.y, seg = blockIdx.x;
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const unsigned char* tab = a.tables + s * a.tab_ld;
+  int64_t* out = a.out + s * a.n_out;
+  int64_t* pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
+  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
+  const int64_t* cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
+  // entry of this segment: the earlier segments' composed maps (their last path rows),
+  // staged in shared memory in parallel, then applied in order from entry 0
+  __shared__ unsigned char mrow[64][W];
+  for (int i = threadIdx.x; i < seg * W; i += blockDim.x)
+    mrow[i / W][i % W] = tab[((int64_t)(i / W) * LTTB_SEG + LTTB_SEG - 1) * W + i % W];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int e = 0;
+    for (int64_t t = 0; t < seg; ++t) e = mrow[t][e];
+    s_e = e;
+  }
+  __syncthreads();
+  const int e = s_e;
+  const int64_t b0 = seg * LTTB_SEG;
+  const int n = (int)min((int64_t)LTTB_SEG, k3 - b0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t b = b0 + i;
+    const int sel = tab[b * W + e];
+    const int64_t p = cand ? cand[b * W + sel] : lbound(a, m, b) + sel;
+    if (pos) pos[b + 1] = p;
+    else out[b + 1] = map ? map[p] : p;
+  }
+  if (seg == 0 && threadIdx.x == 0) {
+    if (pos) {
+      pos[0] = 0;
+      pos[k3 + 1] = m - 1;
+    } else {
+      out[0] = map ? map[0] : 0;
+      out[k3 + 1] = map ? map[m - 1] : m - 1;
+    }
+  }
+}
+
 // K3b, part 1: next-bucket means for every (series, bucket), one thread each.
 template <typename XT, typename YT>
 __global__ void k_lttb_means(LttbArgs a) {

@@ -28,6 +28,27 @@ inline bool use_chain() {
 }
 
 
+// chain resolution over transition maps of width W: the one-CTA scan (default), or
+// the segmented two-kernel version (A/B knob MMLTTB_LTTB_SEGSCAN=1, k3 <= 64 segments;
+// measured: C3 r=4 96.9 vs 92.7 us, r=32 114.2 vs 116.7, C2 189.3 vs 187.2 -- the
+// second launch costs what the parallel walk saves)
+template <int W>
+int launch_chain_scan(LttbArgs a, cudaStream_t st) {
+  const int64_t k3 = a.n_out - 2;
+  static const bool seg_on = env_i64("MMLTTB_LTTB_SEGSCAN", 0) != 0;
+  const int64_t S = cdiv(k3, LTTB_SEG);
+  if (seg_on && S <= 64) {
+    const dim3 g((unsigned)S, (unsigned)a.B);
+    k_lttb_seg_paths<W><<<g, 32, 0, st>>>(a);
+    int rc = check_launch("k_lttb_seg_paths");
+    if (rc) return rc;
+    k_lttb_seg_emit<W><<<g, 64, 0, st>>>(a);
+    return check_launch("k_lttb_seg_emit");
+  }
+  k_lttb_scan<W, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
+  return check_launch("k_lttb_scan");
+}
+
 template <int SMAX> int jump_attr() {
   static bool done = false;
   if (!done) {
@@ -58,8 +79,7 @@ int launch_tables_jump(LttbArgs a, cudaStream_t st) {
   int rc = check_launch("k_lttb_tables");
   if (rc) return rc;
   if constexpr (SMAX <= 32) {
-    k_lttb_scan<SMAX, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
-    return check_launch("k_lttb_scan");
+    return launch_chain_scan<SMAX>(a, st);
   } else {
     return launch_jump<SMAX>(a, st);
   }
@@ -157,8 +177,7 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   }
   k_lttb_ctables<XT, YT, H><<<dim3((unsigned)cdiv(k3, 1024 / H), (unsigned)a.B), 1024, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_ctables"))) return rc;
-  k_lttb_scan<H, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
-  if ((rc = check_launch("k_lttb_scan"))) return rc;
+  if ((rc = launch_chain_scan<H>(a, st))) return rc;
   if (cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
   static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);  // A/B knob (64: 30 vs 37.5 us at 256 on C2)
   if (flat) {
