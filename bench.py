@@ -207,7 +207,9 @@ def build_sample(name, max_points=100_000_000, threads=0):
         if ydt == "f32":
             y = y.astype(np.float32).astype(np.float64)
     x = np.cumsum(rng.exponential(1.0, m)) if xdt == "f64" else i
-    threads = threads or O.max_threads()
+    # all host cores this process may run on (torchrun sets OMP_NUM_THREADS=1 for its
+    # workers, which must not shrink the reference arm to one thread)
+    threads = threads or len(os.sched_getaffinity(0))
     n_out_s = n_out if m == n else max(3, int(round((n_out - 2) * m / n)) + 2)
     if op == "lttb":
         fn = lambda: O.lttb(x, y, n_out_s)  # noqa: E731  (sequential by contract)
