@@ -437,16 +437,16 @@ int mmlttb_shard_preselect(const void* x_shard, int x_dtype, const void* y_shard
 int mmlttb_merge_shards(const int64_t* idx, const double* xs, const double* ys, const int64_t* counts, int64_t G,
                         int64_t cap, int64_t* out_idx, double* out_x, double* out_y, int64_t* out_m, void* stream) {
   if (G < 1 || cap < 1) return fail(MM_EINVAL, "bad arguments");
-  k_merge_shards<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>(idx, xs, ys, counts, G, cap, out_idx, out_x, out_y,
-                                                                 out_m);
+  const dim3 grid((unsigned)cdiv(cap, MERGE_TILE), (unsigned)G);
+  k_merge_shards<<<grid, 256, 0, (cudaStream_t)stream>>>(idx, xs, ys, counts, G, cap, out_idx, out_x, out_y, out_m);
   return check_launch("k_merge_shards");
 }
 
 int mmlttb_merge_packed(const int64_t* buf, int64_t G, int64_t cap, int64_t* out_idx, double* out_x, double* out_y,
                         int64_t* out_m, void* stream) {
   if (!buf || !out_idx || !out_x || !out_y || !out_m || G < 1 || cap < 1) return fail(MM_EINVAL, "bad arguments");
-  k_merge_packed<<<(unsigned)G, 256, 0, (cudaStream_t)stream>>>((const long long*)buf, G, cap, out_idx, out_x, out_y,
-                                                                out_m);
+  const dim3 grid((unsigned)cdiv(cap, MERGE_TILE), (unsigned)G);
+  k_merge_packed<<<grid, 256, 0, (cudaStream_t)stream>>>((const long long*)buf, G, cap, out_idx, out_x, out_y, out_m);
   return check_launch("k_merge_packed");
 }
 
