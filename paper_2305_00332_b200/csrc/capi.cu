@@ -553,8 +553,13 @@ int mmlttb_validate(const void* x, int x_dtype, const void* y, int y_dtype, int6
   if (!x || !y || !flags || N < 1 || !xdt_ok(x_dtype) || !ydt_ok(y_dtype)) return fail(MM_EINVAL, "bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(flags, 0, sizeof(int32_t), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(N, 256), 148 * 16);
-#define MM_V(XT, YT) k_validate<XT, YT><<<blocks, 256, 0, st>>>((const XT*)x, (const YT*)y, N, (int*)flags)
+  const bool al = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);  // 16-byte loads of 4 elements
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(al ? cdiv(N, 4) : N, 256), 148 * 8);
+#define MM_V(XT, YT)                                                                                 \
+  do {                                                                                               \
+    if (al) k_validate<XT, YT><<<blocks, 256, 0, st>>>((const XT*)x, (const YT*)y, N, (int*)flags);  \
+    else k_validate_scalar<XT, YT><<<blocks, 256, 0, st>>>((const XT*)x, (const YT*)y, N, (int*)flags); \
+  } while (0)
   if (y_dtype == MM_F32) {
     switch (x_dtype) {
       case MM_F32: MM_V(float, float); break;

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <limits.h>
+#include <string.h>
 
 namespace mm {
 
@@ -2907,13 +2908,94 @@ static __global__ void k_every_nth(int64_t n, int64_t n_out, int64_t* out) {
   if (i < n_out) out[i] = (i * n) / n_out;  // downsamplers.py:44-47
 }
 
+// TimeSeries invariants on device (core.py:80-94): bit 0 = a non-finite x or
+// y, bit 1 = x decreasing somewhere (np.diff(xs) < 0, i.e. x[i+1] < x[i] in
+// value: -0.0 == +0.0).  Integer-domain checks only (finiteness from the
+// exponent bits, order on integers or +-0-merged total-order keys): no fp64
+// compares or int64 conversions, which issue on B200's narrow XU pipe.  Four
+// coalesced elements in flight per thread.
+template <typename T> __device__ __forceinline__ bool v_nonfinite(T v) { return false; }
+template <> __device__ __forceinline__ bool v_nonfinite<float>(float v) {
+  return (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+}
+template <> __device__ __forceinline__ bool v_nonfinite<double>(double v) {
+  return ((unsigned)(__double_as_longlong(v) >> 32) & 0x7ff00000u) == 0x7ff00000u;
+}
+template <typename T> __device__ __forceinline__ long long v_order(T v) { return (long long)v; }  // int32: exact
+// int64: the reference compares the float64 conversions (equal beyond 2^53 when
+// the integers differ by less than the rounding step), so order the conversions
+template <> __device__ __forceinline__ long long v_order<long long>(long long v) { return dkey(elem_f64(v)); }
+template <> __device__ __forceinline__ long long v_order<float>(float v) {
+  const int b = __float_as_int(v) == (int)0x80000000 ? 0 : __float_as_int(v);  // -0.0 -> +0.0
+  return (long long)(b ^ ((b >> 31) & 0x7fffffff));
+}
+template <> __device__ __forceinline__ long long v_order<double>(double v) {
+  long long b = __double_as_longlong(v);
+  b = b == (long long)0x8000000000000000ULL ? 0 : b;
+  return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
+}
+
+template <typename T> struct V4 {  // 4 consecutive elements from 16-byte loads
+  T v[4];
+  __device__ __forceinline__ void load(const T* p) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint4 w[sizeof(T) / 4];
+#pragma unroll
+    for (int k = 0; k < (int)sizeof(T) / 4; ++k) w[k] = __ldg(q + k);
+    memcpy(v, w, 4 * sizeof(T));
+  }
+};
+
 template <typename XT, typename YT>
-__global__ void k_validate(const XT* x, const YT* y, int64_t n, int* flags) {
+__global__ void __launch_bounds__(256) k_validate(const XT* __restrict__ x, const YT* __restrict__ y, int64_t n,
+                                                 int* flags) {
+  // thread t checks elements [4t, 4t+4) per round (16-byte loads; the host
+  // guarantees 16-byte aligned x and y), plus the pair (4t+3, 4t+4)
+  int f = 0;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c * 4 < n; c += T) {
+    const int64_t i0 = c * 4;
+    XT xv[5];
+    YT yv[4];
+    if (i0 + 4 <= n) {
+      V4<XT> a;
+      V4<YT> b;
+      a.load(x + i0);
+      b.load(y + i0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { xv[q] = a.v[q]; yv[q] = b.v[q]; }
+      xv[4] = i0 + 4 < n ? x[i0 + 4] : xv[3];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i = i0 + q < n ? i0 + q : n - 1;
+        xv[q] = x[i];
+        yv[q] = y[i];
+      }
+      xv[4] = xv[3];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i0 + q < n) {
+        if (v_nonfinite(xv[q]) || v_nonfinite(yv[q])) f |= 1;  // core.py:89-90
+        const XT nx = i0 + q + 1 < n ? xv[q + 1] : xv[q];
+        if (v_order(nx) < v_order(xv[q])) f |= 2;               // core.py:91-92
+      }
+    }
+  }
+  f = __reduce_or_sync(FULL, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+// unaligned inputs (views): one element per thread per round
+template <typename XT, typename YT>
+__global__ void __launch_bounds__(256) k_validate_scalar(const XT* __restrict__ x, const YT* __restrict__ y,
+                                                        int64_t n, int* flags) {
   int f = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double xv = to_f64(x, i), yv = to_f64(y, i);
-    if (!isfinite(xv) || !isfinite(yv)) f |= 1;  // core.py:89-90
-    if (i + 1 < n && to_f64(x, i + 1) < xv) f |= 2;  // core.py:91-92
+    const XT xv = x[i];
+    if (v_nonfinite(xv) || v_nonfinite(y[i])) f |= 1;
+    if (i + 1 < n && v_order(x[i + 1]) < v_order(xv)) f |= 2;
   }
   f = __reduce_or_sync(FULL, f);
   if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);

@@ -260,6 +260,60 @@ def test_device_validation():
         mm.TimeSeries(x2, y)
 
 
+@pytest.mark.parametrize("case", ["ok", "neg_zero_after_pos_zero", "i64_equal_after_rounding", "i64_decreasing",
+                                  "last_pair", "first_pair", "nan_x", "inf_y32", "inf_y64", "f32x_decreasing"])
+def test_device_validation_cases(case):
+    """Device TimeSeries validation against the reference's own rules (core.py:89-92:
+    np.isfinite on the float64 conversions, then np.diff(xs) < 0), across dtypes,
+    +-0.0, int64 beyond 2^53 and grid-stride boundaries."""
+    n = 3_000_003
+    rng = np.random.Generator(np.random.PCG64(5))
+    x = np.arange(n, dtype=np.int64)
+    y = rng.standard_normal(n).astype(np.float32)
+    if case == "neg_zero_after_pos_zero":
+        x = np.arange(n, dtype=np.float64) - 1000.0
+        x[1000] = 0.0
+        x[1001] = -0.0
+        x[1002] = 1.0
+    elif case == "i64_equal_after_rounding":
+        x = np.arange(n, dtype=np.int64) * 4096 + (1 << 60)
+        x[777], x[778] = (1 << 60) + 777 * 4096 + 1, (1 << 60) + 777 * 4096  # equal as float64
+    elif case == "i64_decreasing":
+        x[2_500_000] = x[2_499_999] - 1
+    elif case == "last_pair":
+        x[-1] = x[-2] - 1
+    elif case == "first_pair":
+        x[0] = 5
+    elif case == "nan_x":
+        x = np.arange(n, dtype=np.float64)
+        x[123_456] = np.nan
+    elif case == "inf_y32":
+        y[n - 1] = np.inf
+    elif case == "inf_y64":
+        y = y.astype(np.float64)
+        y[17] = -np.inf
+    elif case == "f32x_decreasing":
+        x = np.arange(n, dtype=np.float32)
+        x[2_999_000] = 1.0
+    xf, yf = x.astype(np.float64), y.astype(np.float64)
+    if not (np.isfinite(xf).all() and np.isfinite(yf).all()):
+        want = errors.NonFiniteValue
+    elif np.any(np.diff(xf) < 0):
+        want = errors.NonMonotonicX
+    else:
+        want = None
+    xd, yd = torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV)
+    for off in (0, 1):  # aligned (16-byte vector path) and an unaligned view (scalar path)
+        if off and case in ("first_pair",):
+            continue
+        xo, yo = xd[off:], yd[off:]
+        if want is None:
+            mm.TimeSeries(xo, yo)
+        else:
+            with pytest.raises(want):
+                mm.TimeSeries(xo, yo)
+
+
 def test_large_properties_1e9():
     """Size-independent properties at the headline size (C3 recipe, N=1e9)."""
     n = 1_000_000_000
