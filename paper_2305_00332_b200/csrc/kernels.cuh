@@ -3041,10 +3041,19 @@ static __global__ void k_p2p_publish(const int64_t* idx, const double* xs, const
   __syncthreads();
   long long* dst = reinterpret_cast<long long*>(peer_bufs[g]) + ((int64_t)(epoch & 1) * G + rank) * W;
   const int64_t n = min(*count, cap);
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    dst[i] = idx[i];
-    dst[cap + i] = __double_as_longlong(xs[i]);
-    dst[2 * cap + i] = __double_as_longlong(ys[i]);
+  constexpr int PER = 4;  // loads in flight per thread before the remote stores
+  for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)blockDim.x * PER) {
+    long long vi[PER], vx[PER], vy[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t i = i0 + (int64_t)q * blockDim.x;
+      if (i < n) { vi[q] = idx[i]; vx[q] = __double_as_longlong(xs[i]); vy[q] = __double_as_longlong(ys[i]); }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t i = i0 + (int64_t)q * blockDim.x;
+      if (i < n) { dst[i] = vi[q]; dst[cap + i] = vx[q]; dst[2 * cap + i] = vy[q]; }
+    }
   }
   if (threadIdx.x == 0) dst[3 * cap] = n;
   __syncthreads();
@@ -3071,10 +3080,19 @@ static __global__ void k_p2p_merge(const long long* own_buf, const unsigned* own
   for (int64_t h = 0; h < g; ++h) off += __ldcg(rows + h * W + 3 * cap);
   const long long* row = rows + g * W;
   const int64_t n = __ldcg(row + 3 * cap);
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    oi[off + i] = __ldcg(row + i);
-    ox[off + i] = __longlong_as_double(__ldcg(row + cap + i));
-    oy[off + i] = __longlong_as_double(__ldcg(row + 2 * cap + i));
+  constexpr int PER = 4;  // loads in flight per thread
+  for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)blockDim.x * PER) {
+    long long vi[PER], vx[PER], vy[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t i = i0 + (int64_t)q * blockDim.x;
+      if (i < n) { vi[q] = __ldcg(row + i); vx[q] = __ldcg(row + cap + i); vy[q] = __ldcg(row + 2 * cap + i); }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t i = i0 + (int64_t)q * blockDim.x;
+      if (i < n) { oi[off + i] = vi[q]; ox[off + i] = __longlong_as_double(vx[q]); oy[off + i] = __longlong_as_double(vy[q]); }
+    }
   }
   if (g == G - 1 && threadIdx.x == 0) om[0] = off + n;
   __syncthreads();
