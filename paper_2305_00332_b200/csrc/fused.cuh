@@ -600,31 +600,45 @@ __global__ void __launch_bounds__(NT) k_post_smem(PostArgs a) {
   long long* s_pre = reinterpret_cast<long long*>(s_py + a.cap);
   const int ydt = sizeof(YT) == 4 ? 0 : 1;
   // ---- compaction: [0] + (lo, hi)... + [N-1]  (downsamplers.py:60-69, 157-160)
-  int64_t carry = 1;
-  for (int64_t c0 = 0; c0 < k; c0 += NT) {
-    const int64_t b = c0 + threadIdx.x;
-    int n = 0;
-    int64_t lo = 0, hi = 0;
-    long long klo = 0, khi = 0;
-    double xl = 0.0, xh = 0.0;
+  // k <= 2 * NT on this path (post_ok): both rounds' Ext loads, then both rounds'
+  // x gathers, are issued before any is consumed (two memory round trips in all)
+  static_assert(NT >= 1024, "post_ok bounds k by 2048");
+  int n[2];
+  int64_t lo[2], hi[2];
+  long long klo[2], khi[2];
+  double xl[2], xh[2];
+  Ext e[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int64_t b = (int64_t)r * NT + threadIdx.x;
+    if (b < k) e[r] = ext[b];
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int64_t b = (int64_t)r * NT + threadIdx.x;
+    n[r] = 0; lo[r] = hi[r] = 0; klo[r] = khi[r] = 0; xl[r] = xh[r] = 0.0;
     if (b < k) {
-      const Ext e = ext[b];
-      if (a.status && keys_nonfinite(e.kmin, e.kmax, ydt)) atomicOr(a.status, 1);
-      const bool mfirst = e.imin <= e.imax;
-      lo = mfirst ? e.imin : e.imax;
-      hi = mfirst ? e.imax : e.imin;
-      klo = mfirst ? e.kmin : e.kmax;
-      khi = mfirst ? e.kmax : e.kmin;
-      n = hi != lo ? 2 : 1;
-      xl = to_f64(xs, lo);  // both gathers in flight across the scan
-      if (n == 2) xh = to_f64(xs, hi);
+      if (a.status && keys_nonfinite(e[r].kmin, e[r].kmax, ydt)) atomicOr(a.status, 1);
+      const bool mfirst = e[r].imin <= e[r].imax;
+      lo[r] = mfirst ? e[r].imin : e[r].imax;
+      hi[r] = mfirst ? e[r].imax : e[r].imin;
+      klo[r] = mfirst ? e[r].kmin : e[r].kmax;
+      khi[r] = mfirst ? e[r].kmax : e[r].kmin;
+      n[r] = hi[r] != lo[r] ? 2 : 1;
+      xl[r] = to_f64(xs, lo[r]);  // gathers in flight across the scans
+      if (n[r] == 2) xh[r] = to_f64(xs, hi[r]);
     }
+  }
+  int64_t carry = 1;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if ((int64_t)r * NT >= k) break;  // uniform
     int tot;
-    const int ex = block_excl_scan<NT>(n, tot, sh);
-    if (b < k) {
+    const int ex = block_excl_scan<NT>(n[r], tot, sh);
+    if ((int64_t)r * NT + threadIdx.x < k) {
       const int64_t p = carry + ex;
-      s_pre[p] = lo; s_px[p] = xl; s_py[p] = key_value<YT>(klo);
-      if (n == 2) { s_pre[p + 1] = hi; s_px[p + 1] = xh; s_py[p + 1] = key_value<YT>(khi); }
+      s_pre[p] = lo[r]; s_px[p] = xl[r]; s_py[p] = key_value<YT>(klo[r]);
+      if (n[r] == 2) { s_pre[p + 1] = hi[r]; s_px[p + 1] = xh[r]; s_py[p + 1] = key_value<YT>(khi[r]); }
     }
     carry += tot;
   }
