@@ -1454,6 +1454,9 @@ __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
 #ifndef K3C_UN_VER
 #define K3C_UN_VER 8
 #endif
+#ifndef K3C_QUAD
+#define K3C_QUAD 8  // points per min/max group in the direction-candidate scan
+#endif
 
 __device__ __forceinline__ double hcross(double ox, double oy, double ax, double ay, double bx, double by) {
   return (ax - ox) * (by - oy) - (ay - oy) * (bx - ox);
@@ -1611,35 +1614,40 @@ __global__ void __launch_bounds__(NT) k_lttb_dircand(LttbArgs a) {
   // max / min come from 3 + 3 min/max instructions and only they are compared against the
   // running extremes, which record the quad's first offset; the winning quads are resolved
   // to their element after the CTA reduction.  (5 instead of 8 ALU/FMA ops per point and direction)
-  static_assert(UN % 4 == 0, "quads");
+  static_assert(UN % K3C_QUAD == 0, "groups");
+  constexpr int QG = K3C_QUAD;  // points per group (4: quads, 8: octets)
   for (int64_t j0 = blo + threadIdx.x; j0 < bhi; j0 += NT * UN, of += (float)(NT * UN)) {
     XT rx[UN];
     YT ry[UN];
 #pragma unroll
     for (int u = 0; u < UN; ++u) {  // UN points' loads in flight before any use
-      const int64_t j = j0 + NT * u < bhi ? j0 + NT * u : j0;  // out of range: repeat the quad's first point
+      const int64_t j = j0 + NT * u < bhi ? j0 + NT * u : j0;  // out of range: repeat the group's first point
       if (!aff) rx[u] = xs[j];
       ry[u] = ys[j];
     }
 #pragma unroll
-    for (int g = 0; g < UN / 4; ++g) {
-      if (j0 + NT * 4 * g < bhi) {
-        float X[4], Y[4];
+    for (int g = 0; g < UN / QG; ++g) {
+      if (j0 + NT * QG * g < bhi) {
+        float X[QG], Y[QG];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int u = 4 * g + t;
+        for (int t = 0; t < QG; ++t) {
+          const int u = QG * g + t;
           const bool in = j0 + NT * u < bhi;
-          X[t] = aff ? (in ? of + (float)(NT * u) : of + (float)(NT * 4 * g)) * fxf
+          X[t] = aff ? (in ? of + (float)(NT * u) : of + (float)(NT * QG * g)) * fxf
                      : d2f_trunc(__dsub_rn(elem_f64(rx[u]), xrd));
           if constexpr (sizeof(YT) == 4) Y[t] = __fsub_rn((float)ry[u], yrf);
           else Y[t] = d2f_trunc(__dsub_rn((double)ry[u], yr));
         }
-        const int o = (int)(j0 + NT * 4 * g - blo);
+        const int o = (int)(j0 + NT * QG * g - blo);
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-          const float v0 = fmaf(cs[k], X[0], sn[k] * Y[0]), v1 = fmaf(cs[k], X[1], sn[k] * Y[1]);
-          const float v2 = fmaf(cs[k], X[2], sn[k] * Y[2]), v3 = fmaf(cs[k], X[3], sn[k] * Y[3]);
-          const float mx = fmaxf(fmaxf(v0, v1), fmaxf(v2, v3)), mn = fminf(fminf(v0, v1), fminf(v2, v3));
+          float mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+          for (int t = 0; t < QG; ++t) {
+            const float v = fmaf(cs[k], X[t], sn[k] * Y[t]);
+            mx = fmaxf(mx, v);
+            mn = fminf(mn, v);
+          }
           if (mx > vmax[k]) { vmax[k] = mx; imax[k] = o; }
           if (mn < vmin[k]) { vmin[k] = mn; imin[k] = o; }
         }
@@ -1688,7 +1696,7 @@ __global__ void __launch_bounds__(NT) k_lttb_dircand(LttbArgs a) {
     float bestv = -INFINITY;
     int bi = ci;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < K3C_QUAD; ++t) {
       const int o = ci + NT * t;
       if (blo + o < bhi) {
         const float X = aff ? (float)o * fxf : d2f_trunc(__dsub_rn(elem_f64(xs[blo + o]), xrd));
