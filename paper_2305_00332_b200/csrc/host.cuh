@@ -80,7 +80,10 @@ inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, i
   ExPlan p;
   const int64_t nb_ = B > 0 ? buckets_total / B : 0;
   const int64_t flat_warps = flat_env >= 0 ? flat_env : (nb_ * max_bucket > 400000000LL ? 148LL * 48 : 148LL * 24);
-  if (closed_form && B > 0 && max_bucket > SMALL_BUCKET && flat_warps > 0) {
+  // flat split above this many elements per bucket (A/B knob MMLTTB_K1_FLAT_MIN; measured on
+  // C3 r=32, 3,128-point buckets: 8-lane groups 117.6 us vs flat 126.8 us per call)
+  static const int64_t flat_min = env_i64("MMLTTB_K1_FLAT_MIN", SMALL_BUCKET);
+  if (closed_form && B > 0 && max_bucket > flat_min && flat_warps > 0) {
     const int64_t nb = nb_;
     p.Ws = std::max<int64_t>(1, flat_warps / B);
     p.E = std::max<int64_t>(min_chunk, cdiv(nb * max_bucket, p.Ws));
