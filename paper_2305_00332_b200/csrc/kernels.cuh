@@ -2700,6 +2700,51 @@ __global__ void __launch_bounds__(NT) k_lttb_verify2(LttbArgs a) {
   }
 }
 
+// Flat path: the certification fix-up and verify2 in one launch.  Phase 1
+// handles the buckets whose flat certification failed (k_lttb_verify_fix),
+// a grid barrier (all CTAs are co-resident: one wave of <= 148) makes their
+// best / flag / flist entries visible, phase 2 is k_lttb_verify2.
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_fix_verify2(LttbArgs a, FlatArgs fl, unsigned* bar) {
+  __shared__ double s_a[NT / 32];
+  __shared__ long long s_i[NT / 32];
+  const int64_t s = 0;  // flat path: one series
+  const int64_t k3 = a.n_out - 2;
+  const int64_t m = a.n;
+  const XT* xs = (const XT*)a.x;
+  const YT* ys = (const YT*)a.y;
+  const int64_t* pos = a.pos;
+  const int nu = *(volatile int*)fl.ucount;
+  for (int q = blockIdx.x; q < nu; q += gridDim.x) {
+    const int64_t b = fl.ulist[q];
+    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, pos[b], s_a, s_i);
+    if (threadIdx.x == 0) {
+      a.best[b] = r;
+      const bool fg = r != pos[b + 1];
+      a.flag[b] = fg;
+      if (fg) a.flist[atomicAdd(&a.fcount[0], 1)] = (int)b;
+    }
+  }
+  if (nu > 0) {  // uniform: without failed certifications phase 1 wrote nothing
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(bar, 1u);
+      while (*(volatile unsigned*)bar < gridDim.x) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  const int nf = *(volatile int*)&a.fcount[0];
+  for (int q = blockIdx.x; q < nf; q += gridDim.x) {  // one flagged bucket f per CTA: bucket f+1
+    const int64_t b = (int64_t)*(volatile int*)&a.flist[q] + 1;
+    if (b >= k3) continue;
+    const int64_t prev = *(volatile long long*)&a.best[b - 1];
+    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
+    if (threadIdx.x == 0) a.best2[b] = r;
+  }
+}
+
 static __device__ unsigned long long g_repair_scans;  // exact bucket scans done by k_lttb_repair (stats)
 
 template <typename XT, typename YT, int NT>

@@ -18,6 +18,10 @@ inline int64_t flat_un(bool verify) {
   static const int64_t uv = env_i64("MMLTTB_K3C_VERIFY_UN", 8), um = env_i64("MMLTTB_K3C_MEANS_UN", 4);
   return verify ? uv : um;
 }
+inline bool fixv2_on() {  // A/B knob MMLTTB_K3C_FIXV2=0: separate fix-up and verify2 launches
+  static const bool on = env_i64("MMLTTB_K3C_FIXV2", 1) != 0;
+  return on;
+}
 inline bool use_hull() {
   static const bool h = env_i64("MMLTTB_K3C_HULL", 0) != 0;  // A/B knob: hull candidates
   return h;
@@ -130,12 +134,15 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
       return f.CP <= flat_cp_max(k3);
     };
     if (!plan(fl, K3C_FLAT_WARPS) || !plan(fl_c, K3C_FLAT_WARPS * 2 / 3)) return fail(MM_ERANGE, "K3c flat partial slots");
-    fcnt = cv.take<unsigned>(3 * k3 + 1);  // arrival counters of the three passes + the failed-certification count
+    // arrival counters of the three passes, the failed-certification count, the
+    // flagged-bucket count and the fix/verify2 grid barrier: one memset
+    fcnt = cv.take<unsigned>(3 * k3 + 3);
     fl.ucount = (int*)(fcnt + 3 * k3);
+    a.fcount = (int*)(fcnt + 3 * k3 + 1);
     fl.part = cv.take<unsigned char>(k3 * flat_cp_max(k3) * K3C_FLAT_PART);
     fl.ulist = cv.take<int>(k3);
     fl_c.part = fl.part;
-    if (cudaMemsetAsync(fcnt, 0, (size_t)(3 * k3 + 1) * sizeof(unsigned), st) != cudaSuccess)
+    if (cudaMemsetAsync(fcnt, 0, (size_t)(3 * k3 + 3) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "memset");
   }
   const unsigned flat_grid = (unsigned)cdiv(fl.W, 8);
@@ -178,24 +185,34 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   k_lttb_ctables<XT, YT, H><<<dim3((unsigned)cdiv(k3, 1024 / H), (unsigned)a.B), 1024, 0, st>>>(a);
   if ((rc = check_launch("k_lttb_ctables"))) return rc;
   if ((rc = launch_chain_scan<H>(a, st))) return rc;
-  if (cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
+  if (!flat && cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess)
+    return fail(MM_ECUDA, "memset");
   static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);  // A/B knob (64: 30 vs 37.5 us at 256 on C2)
   if (flat) {
     fl.cnt = fcnt + 2 * k3;
     if (flat_un(true) == 4) k_lttb_verify_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
     else k_lttb_verify_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
     if ((rc = check_launch("k_lttb_verify_flat"))) return rc;
-    k_lttb_verify_fix<XT, YT, 256><<<dim3(148, 1), 256, 0, st>>>(a, fl);
-    if ((rc = check_launch("k_lttb_verify_fix"))) return rc;
+    // certification fix-up + verify2 in one launch (grid barrier; A/B knob MMLTTB_K3C_FIXV2=0: two)
+    if (fixv2_on()) {
+      // one CTA per SM: every CTA co-resident, as the grid barrier needs
+      k_lttb_fix_verify2<XT, YT, 256><<<(unsigned)sm_count(), 256, 0, st>>>(a, fl, fcnt + 3 * k3 + 2);
+      if ((rc = check_launch("k_lttb_fix_verify2"))) return rc;
+    } else {
+      k_lttb_verify_fix<XT, YT, 256><<<dim3(148, 1), 256, 0, st>>>(a, fl);
+      if ((rc = check_launch("k_lttb_verify_fix"))) return rc;
+    }
   } else {
     if (vnt == 256) k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
     else k_lttb_verify<XT, YT, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_verify"))) return rc;
   }
   static const int64_t v2 = env_i64("MMLTTB_K3C_VERIFY2_NT", 256);  // A/B knob
-  if (v2 == 128) k_lttb_verify2<XT, YT, 128><<<dim3(148, (unsigned)a.B), 128, 0, st>>>(a);
-  else k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
-  if ((rc = check_launch("k_lttb_verify2"))) return rc;
+  if (!(flat && fixv2_on())) {
+    if (v2 == 128) k_lttb_verify2<XT, YT, 128><<<dim3(148, (unsigned)a.B), 128, 0, st>>>(a);
+    else k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
+    if ((rc = check_launch("k_lttb_verify2"))) return rc;
+  }
   static const int64_t rp = env_i64("MMLTTB_K3C_REPAIR_NT", 512);  // A/B knob (512: 22.1 vs 24.4 us at 1024 on C2)
   // chain state staged in shared memory when it fits (A/B knob MMLTTB_K3C_REPAIR_SMEM=0: global)
   static const bool rsm = env_i64("MMLTTB_K3C_REPAIR_SMEM", 1) != 0;
