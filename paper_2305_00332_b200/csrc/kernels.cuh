@@ -1740,28 +1740,48 @@ __global__ void __launch_bounds__(NT) k_lttb_dircand(LttbArgs a) {
 template <typename XT, typename YT, int HMAX>
 __global__ void __launch_bounds__(1024) k_lttb_ctables(LttbArgs a) {
   constexpr int NBK = 1024 / HMAX;
+  // every thread stages one candidate point of the CTA's buckets (and of the
+  // bucket before them, the anchors) in shared memory first: two memory round
+  // trips in all instead of a dependent cand -> (x, y) chain per candidate
+  __shared__ double2 s_pt[NBK + 1][HMAX];
+  __shared__ int s_cnt[NBK + 1];
   const int64_t s = blockIdx.y;
   const int64_t k3 = a.n_out - 2;
   const int bi = threadIdx.x / HMAX, p = threadIdx.x % HMAX;
-  const int64_t b = (int64_t)blockIdx.x * NBK + bi;
-  if (b >= k3) return;
+  const int64_t bb = (int64_t)blockIdx.x * NBK;  // first bucket of the CTA
   const XT* xs = (const XT*)a.x + s * a.x_ld;
   const YT* ys = (const YT*)a.y + s * a.y_ld;
   const int64_t* cand = a.cand + s * a.cand_ld;
   const int* cnt = a.cand_cnt + s * k3;
+  for (int t = threadIdx.x; t < (NBK + 1) * HMAX; t += 1024) {  // row r = bucket bb - 1 + r
+    const int r = t / HMAX, q = t % HMAX;
+    const int64_t b = bb - 1 + r;
+    if (b >= 0 && b < k3) {
+      const int nc = cnt[b];
+      if (q == 0) s_cnt[r] = nc;
+      if (q < nc) {
+        const int64_t jj = cand[b * HMAX + q];
+        s_pt[r][q] = make_double2(to_f64(xs, jj), to_f64(ys, jj));
+      }
+    } else if (q == 0) {
+      s_cnt[r] = 0;
+    }
+  }
+  __syncthreads();
+  const int64_t b = bb + bi;
+  if (b >= k3) return;
   bool valid;
-  int64_t ap;
-  if (b == 0) { valid = p == 0; ap = 0; }
-  else { valid = p < cnt[b - 1]; ap = valid ? cand[(b - 1) * HMAX + p] : 0; }
+  double ax, ay;
+  if (b == 0) { valid = p == 0; ax = to_f64(xs, 0); ay = to_f64(ys, 0); }
+  else { valid = p < s_cnt[bi]; ax = valid ? s_pt[bi][p].x : 0.0; ay = valid ? s_pt[bi][p].y : 0.0; }
   unsigned char r = 0;
   if (valid) {
-    const double ax = to_f64(xs, ap), ay = to_f64(ys, ap);
     const double2 c = a.means[s * a.means_ld + b];
-    const int nc = cnt[b];
+    const int nc = s_cnt[bi + 1];
     long long bestv = -1;
     for (int q = 0; q < nc; ++q) {
-      const int64_t j = cand[b * HMAX + q];
-      const long long ar = lttb_area_key(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
+      const double2 pt = s_pt[bi + 1][q];
+      const long long ar = lttb_area_key(ax, ay, c.x, c.y, pt.x, pt.y);
       if (ar > bestv) { bestv = ar; r = (unsigned char)q; }
     }
   }
