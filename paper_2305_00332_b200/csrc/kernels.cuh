@@ -817,8 +817,12 @@ __device__ __forceinline__ double2 lttb_next_mean(const LttbArgs& a, const XT* x
 // Block = NBB consecutive buckets of one series.
 template <typename XT, typename YT, int SMAX, int NBB>
 __global__ void __launch_bounds__(NBB * SMAX < 1024 ? NBB * SMAX : 1024) k_lttb_tables(LttbArgs a) {
+  // the points of buckets bb-1 .. bb+nbk (anchors, candidates, next-bucket means)
+  // are staged in shared memory once, so no thread waits on a chain of loads
+  constexpr int PMAX = (NBB + 2) * SMAX + 2;
+  __shared__ double s_x[PMAX], s_y[PMAX];
   __shared__ double2 s_mean[NBB];
-  __shared__ int64_t s_bnd[NBB + 2];
+  __shared__ int64_t s_bnd[NBB + 3];
   const int64_t s = blockIdx.y;
   const int64_t k3 = a.n_out - 2;
   const int64_t bb = (int64_t)blockIdx.x * NBB;
@@ -827,9 +831,37 @@ __global__ void __launch_bounds__(NBB * SMAX < 1024 ? NBB * SMAX : 1024) k_lttb_
   const XT* xs = (const XT*)a.x + s * a.x_ld;
   const YT* ys = (const YT*)a.y + s * a.y_ld;
   const int nbk = (int)(k3 - bb < NBB ? k3 - bb : (int64_t)NBB);
-  for (int i = threadIdx.x; i < nbk; i += blockDim.x) s_mean[i] = lttb_next_mean(a, xs, ys, m, bb + i);
-  for (int i = threadIdx.x; i <= nbk; i += blockDim.x) s_bnd[i + 1] = lbound(a, m, bb + i);
-  if (threadIdx.x == 0) s_bnd[0] = bb > 0 ? lbound(a, m, bb - 1) : 0;
+  // s_bnd[i + 1] = lbound(bb + i), i = -1 .. nbk + 1 (lbound(k3) = m - 1; past it: m)
+  for (int i = threadIdx.x; i <= nbk + 2; i += blockDim.x) {
+    const int64_t b = bb - 1 + i;
+    s_bnd[i] = b < 0 ? 0 : (b <= k3 ? lbound(a, m, b) : m);
+  }
+  __syncthreads();
+  const int64_t lo0 = s_bnd[0];  // anchors of bucket bb (point 0 when bb == 0)
+  const int64_t hi0 = bb + nbk >= k3 ? m : s_bnd[nbk + 2];  // through the next bucket, or the last point
+  const int np = (int)(hi0 - lo0);
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    s_x[i] = to_f64(xs, lo0 + i);
+    s_y[i] = to_f64(ys, lo0 + i);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x) {  // next-bucket means, in-order fp64 sums (_kernels.py:95-107)
+    const int64_t b = bb + i;
+    double2 c;
+    if (b + 1 < k3) {
+      const int64_t nlo = s_bnd[i + 2], nhi = s_bnd[i + 3];
+      double sx = 0.0, sy = 0.0;
+      for (int64_t jj = nlo; jj < nhi; ++jj) {
+        sx = __dadd_rn(sx, s_x[jj - lo0]);
+        sy = __dadd_rn(sy, s_y[jj - lo0]);
+      }
+      const double cnt = (double)(nhi - nlo);
+      c = make_double2(__ddiv_rn(sx, cnt), __ddiv_rn(sy, cnt));
+    } else {
+      c = make_double2(s_x[m - 1 - lo0], s_y[m - 1 - lo0]);
+    }
+    s_mean[i] = c;
+  }
   __syncthreads();
   unsigned char* tab = a.tables + s * a.tab_ld + bb * SMAX;
   for (int it = threadIdx.x; it < nbk * SMAX; it += blockDim.x) {
@@ -842,12 +874,12 @@ __global__ void __launch_bounds__(NBB * SMAX < 1024 ? NBB * SMAX : 1024) k_lttb_
     else { const int64_t plo = s_bnd[bi]; valid = p < s_bnd[bi + 1] - plo; ap = plo + p; }
     unsigned char r = 0;
     if (valid) {
-      const double ax = to_f64(xs, ap), ay = to_f64(ys, ap);
+      const double ax = s_x[ap - lo0], ay = s_y[ap - lo0];
       const double2 c = s_mean[bi];
       long long best = -1;
-      for (int64_t j = blo; j < bhi; ++j) {
-        const long long ar = lttb_area_key(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
-        if (ar > best) { best = ar; r = (unsigned char)(j - blo); }  // strict '>' (:115)
+      for (int64_t jj = blo; jj < bhi; ++jj) {
+        const long long ar = lttb_area_key(ax, ay, c.x, c.y, s_x[jj - lo0], s_y[jj - lo0]);
+        if (ar > best) { best = ar; r = (unsigned char)(jj - blo); }  // strict '>' (:115)
       }
     }
     tab[it] = r;
