@@ -558,6 +558,14 @@ __device__ __forceinline__ void compact_pairs_tile(const PairArgs& a, int64_t s,
   const int64_t b_lo = tile * TB;
   const unsigned char* cnt = a.cnt8 + s * a.nb;
   const Ext* ext = a.ext + s * a.nb;
+  // this thread's Ext records: loaded first, in flight across the prefix sum
+  Ext er[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t bl = b_lo + (int64_t)threadIdx.x * ITEMS + i;
+    er[i].imin = er[i].imax = er[i].kmin = er[i].kmax = 0;
+    if (bl < a.nb) er[i] = ext[bl];
+  }
   // 1. offset of this tile = items of buckets [0, b_lo): the 1-byte counts
   //    are summed as masked 32-bit words (independent loads, no byte chain)
   long long pre = 0;
@@ -592,9 +600,7 @@ __device__ __forceinline__ void compact_pairs_tile(const PairArgs& a, int64_t s,
   for (int i = 0; i < ITEMS; ++i) {
     const int64_t bl = b_lo + (int64_t)threadIdx.x * ITEMS + i;
     const bool ok = bl < a.nb;
-    Ext e;
-    e.imin = e.imax = e.kmin = e.kmax = 0;
-    if (ok) e = ext[bl];
+    const Ext e = er[i];
     if (ok && a.status && keys_nonfinite(e.kmin, e.kmax, a.ydt)) atomicOr(a.status, 1);
     const bool mfirst = e.imin <= e.imax;
     v[2 * i] = mfirst ? e.imin : e.imax;  // downsamplers.py:60-69
