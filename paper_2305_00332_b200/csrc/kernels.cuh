@@ -2906,11 +2906,22 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
   int* Nx = (int*)(B2 + k3);       // smallest flagged bucket >= i, or INT_MAX [k3 + 1]
   const int64_t* pos = a.pos + s * a.pos_ld;
   const int* flag = a.flag + s * k3;
-  for (int64_t i = threadIdx.x; i < k3 + 2; i += NT) P[i] = pos[i];
-  for (int64_t i = threadIdx.x; i < k3; i += NT) {  // coalesced staging (flags into Nx first)
-    Bv[i] = a.best[s * k3 + i];
-    B2[i] = a.best2[s * k3 + i];
-    Nx[i] = flag[i];
+  // coalesced staging (flags into Nx first), 4 rows of loads in flight per thread
+  for (int64_t i0 = threadIdx.x; i0 < k3 + 2; i0 += 4 * NT) {
+    long long vp[4], vb[4], v2[4];
+    int vf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q * NT;
+      if (i < k3 + 2) vp[q] = pos[i];
+      if (i < k3) { vb[q] = a.best[s * k3 + i]; v2[q] = a.best2[s * k3 + i]; vf[q] = flag[i]; }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q * NT;
+      if (i < k3 + 2) P[i] = vp[q];
+      if (i < k3) { Bv[i] = vb[q]; B2[i] = v2[q]; Nx[i] = vf[q]; }
+    }
   }
   __syncthreads();
   // next-flagged index: per-thread chunk suffix (shared memory), then a suffix minimum over chunks
