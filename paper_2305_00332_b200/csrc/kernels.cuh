@@ -1128,10 +1128,12 @@ __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
   const int64_t s = blockIdx.x;
   const int64_t k3 = a.n_out - 2;
   const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  int64_t* out = a.out + s * a.n_out;
-  int64_t* pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
-  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
-  const int64_t* cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
+  // restrict: the emit's loads (cand, map) never alias its stores (pos, out), so a
+  // thread's ITEMS emits can have their loads in flight together
+  int64_t* __restrict__ out = a.out + s * a.n_out;
+  int64_t* __restrict__ pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
+  const int64_t* __restrict__ map = a.map ? a.map + s * a.map_ld : nullptr;
+  const int64_t* __restrict__ cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
   scan_chain<W, NT, ITEMS>(a.tables + s * a.tab_ld, k3, [&](int64_t b, int sel) {
     const int64_t p = cand ? cand[b * W + sel] : lbound(a, m, b) + sel;
     if (pos) pos[b + 1] = p;
