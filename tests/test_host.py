@@ -47,6 +47,27 @@ def test_workspace_sizes_are_small_and_independent_of_n():
     assert abs(a - b) / b < 0.10
 
 
+def test_workspace_bytes_memo_matches_library():
+    """The hot path's memoised mmlttb_workspace_bytes returns the library's value."""
+    L = _native.load()
+    for op, B, n, n_out, r, ydt in [(_native.OP_MINMAXLTTB, 1, 1_000_000, 1000, 4, _native.MM_F64),
+                                    (_native.OP_MINMAXLTTB, 3, 1_000_000, 1000, 32, _native.MM_F32),
+                                    (_native.OP_LTTB, 1, 10_000_000, 2000, 0, _native.MM_F64),
+                                    (_native.OP_LTTB, 4, 300_000, 700, 0, _native.MM_F32),
+                                    (_native.OP_PRESELECT, 2, 5_000_000, 2000, 8, _native.MM_F32)]:
+        want = L.mmlttb_workspace_bytes(op, B, n, n_out, r, ydt)
+        assert _native.workspace_bytes(op, B, n, n_out, r, ydt) == want > 0
+        assert _native.workspace_bytes(op, B, n, n_out, r, ydt) == want  # cached
+
+
+def test_flat_k3c_workspace_is_bounded():
+    """The single-series K3c flat passes add O(k3) workspace, not O(N)."""
+    L = _native.load()
+    a = L.mmlttb_workspace_bytes(_native.OP_LTTB, 1, 10_000_000, 2000, 0, _native.MM_F64)
+    b = L.mmlttb_workspace_bytes(_native.OP_LTTB, 1, 1_000_000_000, 2000, 0, _native.MM_F64)
+    assert 0 < a < 32 << 20 and a == b
+
+
 def test_error_hierarchy_matches_reference_names():
     for name in ("NonMonotonicX", "NonFiniteValue", "NOutOfRange", "BadPreselectionRatio", "InvalidPartition",
                  "OddNOut", "NOutNotDivisibleBy4", "RatioTooLargeForSeries", "NotParallelizable"):
