@@ -2424,6 +2424,10 @@ __device__ __forceinline__ void means_scan(const XT* __restrict__ xb, const YT* 
                                            bool try_x) {
   const long long dstep = (long long)((unsigned long long)f.di * 32ull);
   long long xe = (long long)((unsigned long long)f.x0i + (unsigned long long)(t0 + lane) * (unsigned long long)f.di);
+  // y extremes on the HIGH word of the total-order key (32-bit min/max, one
+  // instruction each): a conservative range, exact to ~2^-20 relative, which is
+  // all the direction search and the certification bound need
+  int hmn = INT_MAX, hmx = INT_MIN;
   for (int i = lane; i < n; i += 32 * UN) {
     XT rx[UN];
     YT ry[UN];
@@ -2450,9 +2454,10 @@ __device__ __forceinline__ void means_scan(const XT* __restrict__ xb, const YT* 
         const double vx = elem_f64(rx[q]), vy = elem_f64(ry[q]);
         p.sx = __dadd_rn(p.sx, vx); p.sy = __dadd_rn(p.sy, vy);
         p.ax = __dadd_rn(p.ax, fabs(vx)); p.ay = __dadd_rn(p.ay, fabs(vy));
-        const long long ky = dkey(vy);
-        if (ky < p.kymn) p.kymn = ky;
-        if (ky > p.kymx) p.kymx = ky;
+        const int hy = (int)(__double_as_longlong(vy) >> 32);
+        const int hk = hy ^ ((hy >> 31) & 0x7fffffff);  // == dkey(vy) >> 32
+        hmn = min(hmn, hk);
+        hmx = max(hmx, hk);
         if (TRYY) p.ly = min(p.ly, lsb_exp(vy));
         if constexpr (XForm<XT>::integral) {
           const long long xi = (long long)rx[q];
@@ -2469,6 +2474,10 @@ __device__ __forceinline__ void means_scan(const XT* __restrict__ xb, const YT* 
       }
       xe = (long long)((unsigned long long)xe + (unsigned long long)dstep);
     }
+  }
+  if (hmn <= hmx) {
+    p.kymn = min(p.kymn, (long long)hmn * 4294967296LL);                  // <= every key
+    p.kymx = max(p.kymx, (long long)hmx * 4294967296LL + 4294967295LL);  // >= every key
   }
 }
 
