@@ -18,8 +18,11 @@ inline int64_t flat_un(bool verify) {
   static const int64_t uv = env_i64("MMLTTB_K3C_VERIFY_UN", 8), um = env_i64("MMLTTB_K3C_MEANS_UN", 4);
   return verify ? uv : um;
 }
-inline bool fixv2_on() {  // A/B knob MMLTTB_K3C_FIXV2=0: separate fix-up and verify2 launches
-  static const bool on = env_i64("MMLTTB_K3C_FIXV2", 1) != 0;
+// A/B knob MMLTTB_K3C_FIXV2=1: certification fix-up and verify2 in one launch with a grid
+// barrier (measured on C2: 176.0 vs 175.3 us for the two launches, so the barrier-free pair
+// stays the default)
+inline bool fixv2_on() {
+  static const bool on = env_i64("MMLTTB_K3C_FIXV2", 0) != 0;
   return on;
 }
 inline bool use_hull() {
