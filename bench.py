@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """MinMaxLTTB throughput on B200: input points/s, HBM GB/s and % of roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3_1e9|c1|c2|c3|c4|c5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3_1e9|c1|c2|c3|c4|c5|...] [--impl ours|reference]
 
 A step = one minmaxlttb call (K1 extrema -> K2 compact -> K3 LTTB) over the
 workload's series.  Default workload "c3_1e9": BASELINE.json C3's recipe at
@@ -10,16 +10,21 @@ minmax_ratio = 4) -- the north star's "10^9-point series".
 Inputs are generated ON the device (torch Philox, seed 3; a 4 GB float32 y
 is larger than the 126 MB L2, so consecutive steps never hit in L2) and the
 warm-up output is checked index-exactly against the CPU oracle on the same
-data.  Under torchrun (N > 1) the default workload becomes ONE series of
-N x 1e9 points split by MinMax bucket ranges across the ranks (SURVEY 8(e)
-single-series path: K1 + K2 on each rank's 1e9-point shard, one NCCL
-all_gather of the preselected sets, device merge, LTTB): per-GPU work is
-fixed, "scaling": "weak".  c4 shards its 4096 series across ranks (no
-collective, "strong"); c5s splits the 2e9-point C5 series ("strong").
+data (on every rank; rank 0 reports the AND).
 
---impl reference times the reference algorithm's CPU restatement
-(oracle/, OpenMP over all host threads, float64 inputs as tsdown.TimeSeries
-holds them) on a bounded prefix sample of the same workload; rank 0 only.
+--gpus N > 1 without torchrun: the script relaunches itself under
+``torch.distributed.run`` with N ranks (and refuses, exit 2, when fewer than
+N GPUs are visible or WORLD_SIZE disagrees with --gpus).  With N ranks the
+default workload becomes ONE series of N x 1e9 points split by MinMax bucket
+ranges (SURVEY 8(e) single-series path: K1 + K2 on each rank's 1e9-point
+shard, one NCCL all_gather of the preselected sets, device merge, LTTB):
+per-GPU work is fixed, "scaling": "weak".  c4 shards its 4096 series across
+ranks (no collective, "strong"); c5s splits the 2e9-point C5 series.
+
+--impl reference times the REFERENCE's own CPU implementation (package
+tsdown, unmodified, installed into oracle/_ref; oracle/refbench.py) on the
+box's host cores, rank 0 only; the same code supplies our line's
+``cpu_baseline`` (run in a fresh interpreter so thread pinning applies).
 """
 from __future__ import annotations
 
@@ -183,59 +188,26 @@ def make_inputs(name, dev, seed, batch=None):
 
 
 # ------------------------------------------------------------- CPU legs -----
-def build_sample(name, max_points=100_000_000, threads=0):
-    """The reference algorithm's CPU restatement on a bounded sample.
-
-    Sample: the first min(N, max_points) points of one series of the workload
-    (same recipe, numpy-generated, float64 as tsdown.TimeSeries stores it --
-    the f64 conversion is outside the timed region, as in the reference's
-    bench.py:124-127), same r_ps, n_out scaled so sub-buckets keep the
-    workload's size, OpenMP over `threads` host threads (prange analogue).
-    """
-    from oracle import oracle as O
-
-    n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
-    m = min(n, max_points)
-    rng = np.random.Generator(np.random.PCG64(3))
-    i = np.arange(m, dtype=np.float64)
-    if name.startswith("c3"):
-        y = np.sin(2 * np.pi * i / 1e3) + np.sin(2 * np.pi * i / 1e5) + np.sin(2 * np.pi * i / 1e7)
-        y += rng.standard_normal(m)
-        y = y.astype(np.float32).astype(np.float64)
-    else:
-        y = np.cumsum(rng.standard_normal(m))
-        if ydt == "f32":
-            y = y.astype(np.float32).astype(np.float64)
-    x = np.cumsum(rng.exponential(1.0, m)) if xdt == "f64" else i
-    # all host cores this process may run on (torchrun sets OMP_NUM_THREADS=1 for its
-    # workers, which must not shrink the reference arm to one thread)
-    threads = threads or len(os.sched_getaffinity(0))
-    n_out_s = n_out if m == n else max(3, int(round((n_out - 2) * m / n)) + 2)
-    if op == "lttb":
-        fn = lambda: O.lttb(x, y, n_out_s)  # noqa: E731  (sequential by contract)
-        cores = 1
-    else:
-        fn = lambda: O.minmaxlttb(x, y, n_out_s, r_ps, threads)  # noqa: E731
-        cores = threads
-    desc = (f"{name}: first {m:.3g} points of one series, n_out={n_out_s}, r_ps={r_ps}, {op} on f64 "
-            f"(TimeSeries layout), {cores} thread(s) of {os.cpu_count()} host CPUs")
-    return fn, m, desc, cores
+# The reference arm times at most this many points of the workload per step
+# (the full c3_1e9 series fits; N-GPU weak-scaled series and C5 use a prefix).
+REF_MAX_POINTS = 1_000_000_000
 
 
-def cpu_sample(name, seconds=12.0):
-    fn, m, desc, cores = build_sample(name)
-    fn()  # warm
-    times = []
-    t_end = time.perf_counter() + seconds
-    while time.perf_counter() < t_end or len(times) < 3:
-        t0 = time.perf_counter()
-        fn()
-        times.append(time.perf_counter() - t0)
-        if len(times) >= 500:
-            break
-    med = statistics.median(times)
-    return {"value": m / med, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": desc + f", median of {len(times)} runs", "ms_per_sample": med * 1e3}
+def base_config(name, n, batch, n_out, r_ps, op, ydt, xdt):
+    """The `config` dict shared verbatim by both arms (what was timed)."""
+    return {"workload": name, "n": n, "batch": batch, "n_out": n_out, "minmax_ratio": r_ps, "op": op,
+            "y_dtype": ydt, "x_dtype": xdt}
+
+
+def reference_measure(name, n, batch, n_out, r_ps, op, steps, warmup):
+    from oracle import refbench
+
+    per_series = batch > 1  # C4: per-series calls, as the reference would loop
+    r = refbench.time_reference(name, n, n_out, r_ps, op, steps, warmup, seq_steps=3,
+                                max_points=REF_MAX_POINTS)
+    if per_series:
+        r["sample"] += f"; C4 = {batch} independent series: one series' call timed, points/s per series"
+    return r
 
 
 def run_reference(args):
@@ -244,26 +216,44 @@ def run_reference(args):
         return 0
     name = args.workload
     n, batch, n_out, r_ps, ydt, xdt, op = WORKLOADS[name]
-    fn, m, desc, cores = build_sample(name)
-    times = []
-    for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        fn()
-        dt = time.perf_counter() - t0
-        if s >= args.warmup:
-            times.append(dt)
-    total = sum(times)
-    value = m * len(times) / total
+    gpus = int(os.environ.get("WORLD_SIZE", args.gpus))
+    if name == "c3_1e9" and gpus > 1:
+        n = n * gpus  # our arm's weak-scaled series; the CPU times a 1e9-point prefix of it
+    r = reference_measure(name, n, batch, n_out, r_ps, op, args.steps, args.warmup)
+    value = r["value"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": name, "n": n, "batch": batch, "n_out": n_out, "minmax_ratio": r_ps, "op": op},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (numpy PCG64, BASELINE.json recipe; f64 TimeSeries as the reference holds it)",
+        "config": base_config(name, n, batch, n_out, r_ps, op, ydt, xdt),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["par_cores"], "kind": r["kind"],
+                         "sample": r["sample"], "sequential": r.get("sequential"),
+                         "threading_layer": r.get("threading_layer"), "points_per_step": r["points"],
+                         "timeseries_build_s": r.get("timeseries_build_s")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline_subprocess(name, steps=5, timeout=900):
+    """cpu_baseline = the reference arm's own measurement (same code, fresh
+    interpreter so NUMBA/OMP thread settings apply), median of `steps`."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--workload", name, "--steps", str(steps),
+           "--warmup", "1", "--gpus", "1"]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "OMP_NUM_THREADS")}
+    try:
+        p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=str(ROOT))
+    except subprocess.TimeoutExpired:
+        return {"value": None, "unit": UNIT, "cores": None, "kind": None, "sample": "timed out"}
+    for line in p.stdout.splitlines()[::-1]:
+        if line.startswith("{"):
+            d = json.loads(line)
+            cb = d["cpu_baseline"]
+            cb["config"] = d["config"]
+            return cb
+    return {"value": None, "unit": UNIT, "cores": None, "kind": None, "sample": "failed: " + p.stderr[-500:]}
 
 
 # ------------------------------------------------------------- GPU leg ------
@@ -335,7 +325,73 @@ def _e2e_sharded(x, y, e2e_steps, n, n_out, r_ps, ws, dist, dev):
     return statistics.mean(t_e2e), h2d, res.numel() * res.element_size()
 
 
+def _parity_rows(B):
+    """Rows the warm-up parity check compares: 0, B-1 and >= 64 spread rows."""
+    if B <= 66:
+        return list(range(B))
+    return sorted(set([0, B - 1] + [int(v) for v in np.linspace(0, B - 1, 64).round()]))
+
+
+def _check_parity(out, x, y, n_out, r_ps, op, sharded, shard, n, dist, ws):
+    """Index-exact check of the warm-up output against the CPU oracle, on EVERY rank.
+
+    Batch / replica rows: rows 0, B-1 and >= 64 spread rows of this rank's
+    batch.  Bucket-range sharded series: each rank checks its shard's
+    preselected set (the product's own shard_preselect) against the oracle's
+    shard preselection, then rank 0 checks the final LTTB over the gathered
+    sets against the oracle's lttb on them.  Returns (ok, description)."""
+    from oracle import oracle as O
+
+    if sharded:
+        from paper_2305_00332_b200 import sharding as S
+
+        idx, xs, ys, cnt = S.shard_preselect(x, y, n, n_out, r_ps, shard)
+        c = int(cnt.item())
+        got = idx[:c].cpu().numpy()
+        yh = y.cpu().numpy()
+        want = O.shard_preselect_typed(yh, shard.lo, n, n_out, r_ps, shard.b0, shard.b1, shard.emit_first,
+                                       shard.emit_last)
+        del yh
+        ok = bool(np.array_equal(got, want))
+        mine = (got, xs[:c].cpu().numpy(), ys[:c].cpu().numpy())
+        parts = [None] * ws
+        if ws > 1:
+            dist.all_gather_object(parts, mine)
+        else:
+            parts = [mine]
+        if dist is not None and ws > 1 and dist.get_rank() != 0:
+            return ok, "per-rank shard preselect vs oracle"
+        pi = np.concatenate([p[0] for p in parts])
+        px = np.concatenate([p[1] for p in parts])
+        py = np.concatenate([p[2] for p in parts])
+        final = pi[O.lttb(px, py, n_out)]
+        ok = ok and bool(np.array_equal(out.cpu().numpy(), final))
+        return ok, "every rank's shard preselect vs oracle + final LTTB over the gathered sets vs oracle"
+    xh = x.cpu().numpy()
+    o = out.cpu().numpy().reshape(-1, n_out)
+    rows = _parity_rows(o.shape[0])
+    ok = True
+    for i in rows:
+        yi = (y if y.dim() == 1 else y[i]).cpu().numpy()
+        want = O.lttb(xh, yi, n_out) if op == "lttb" else O.minmaxlttb_typed(xh, yi, n_out, r_ps)
+        ok = ok and bool(np.array_equal(o[i], want))
+    return ok, f"{len(rows)} of {o.shape[0]} rows per rank vs oracle"
+
+
+def _kernel_label(trace):
+    names = [t for t in trace.split(",") if t]
+    if not names:
+        return "none", names
+    if "k_mmlttb_fused" in names:
+        return "fused", names
+    if any(t.startswith("k_extrema") for t in names):
+        return "k1", names
+    return "lttb", names
+
+
 def run_ours(args):
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
@@ -353,12 +409,14 @@ def run_ours(args):
     sharded = name == "c5s" or (name == "c3_1e9" and ws > 1)
     if name == "c3_1e9" and ws > 1:  # one N x 1e9-point series, bucket-range sharded (weak)
         n = n * ws
+    batch_total = batch
     if name == "c4" and ws > 1:  # C4: 4096 series sharded across ranks (strong)
         from paper_2305_00332_b200.sharding import batch_range
 
         lo, hi = batch_range(batch, rank, ws)
         batch = hi - lo
         scaling = "strong"
+    shard = None
     if sharded:
         from paper_2305_00332_b200 import sharding
 
@@ -383,22 +441,22 @@ def run_ours(args):
             return mm.lttb(xx, yy, n_out)
         return mm.minmaxlttb(xx, yy, n_out, minmax_ratio=r_ps)
 
-    # warm-up + parity of the warm-up output against the oracle (rank 0)
+    # warm-up (with the launch trace on: the kernels one step launches) + parity of
+    # the warm-up output against the oracle, on every rank
+    L.mmlttb_trace(1)
     out = step(x, y)
     torch.cuda.synchronize()
+    tbuf = ctypes.create_string_buffer(1 << 16)
+    L.mmlttb_trace_read(tbuf, len(tbuf))
+    L.mmlttb_trace(0)
+    kind, step_kernels = _kernel_label(tbuf.value.decode())
     parity = "unchecked"
-    if rank == 0 and not args.no_check and (not sharded or ws == 1):
-        from oracle import oracle as O
-
-        xh = x.cpu().numpy()
-        yh = (y if y.dim() == 1 else y[0]).cpu().numpy()
-        o = (out if out.dim() == 1 else out[0]).cpu().numpy()
-        if op == "lttb":
-            want = O.lttb(xh, yh, n_out)
-        else:
-            want = O.minmaxlttb_typed(xh, yh, n_out, r_ps)
-        parity = "exact vs oracle" if np.array_equal(o, want) else "MISMATCH vs oracle"
-        del xh, yh
+    if not args.no_check:
+        ok, how = _check_parity(out, x, y, n_out, r_ps, op, sharded, shard, n, dist if ws > 1 else None, ws)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        if ws > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        parity = ("exact vs oracle" if int(flag.item()) else "MISMATCH vs oracle") + f" ({how}; {ws} rank(s))"
     for _ in range(max(0, args.warmup - 1)):
         step(x, y)
     torch.cuda.synchronize()
@@ -426,10 +484,9 @@ def run_ours(args):
     launches = L.mmlttb_launch_count() - l0
     repairs = (L.mmlttb_repair_scans() - rep0) / args.steps
     ms = e0.elapsed_time(e1)
-    import ctypes
 
-    # ---- per-stage device times (roofline.kernel_ms): CUDA events recorded by the
-    # library on the call's stream around K1 / K2 / K3, over a live pass of the same steps
+    # ---- per-stage device times: CUDA events recorded by the library on the
+    # call's stream around K1 / K2 / K3, over a live pass of the same steps
     stage_steps = min(args.steps, 50)
     L.mmlttb_stage_timer(1)
     for _ in range(stage_steps):
@@ -452,33 +509,42 @@ def run_ours(args):
     else:
         e2e_ms, h2d, d2h = _e2e(step, x, y, e2e_steps, n_out, r_ps, batch, op, ws, dist)
         clocks.stop()
-    pts = n * batch if not sharded else n / ws  # c5s: the one series is split across ranks
+    pts = n * batch if not sharded else n / ws  # sharded: the one series is split across ranks
 
     # max over ranks of the device-timed region
     t = torch.tensor([ms, e2e_ms if e2e_steps > 0 else 0.0], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, e2e_ms = float(t[0]), float(t[1])
-    value = pts * ws * args.steps / (ms / 1e3) if scaling == "weak" else pts * ws * args.steps / (ms / 1e3)
+    value = pts * ws * args.steps / (ms / 1e3)
     e2e_value = pts * ws / (e2e_ms / 1e3) if e2e_steps > 0 else None
     if rank == 0:
         peak, peak_src = _peaks()
         ysz = 4 if ydt == "f32" else 8
+        step_ms = ms / args.steps
+        kernel_timing = (f"CUDA events recorded by the library around the kernel on its stream, "
+                         f"{stage_steps} live steps right after the timed region")
         if sharded:  # whole sharded step: K1+K2 on the shard, all_gather, merge, LTTB
             alg_bytes = pts * ysz
-            k_ms = ms / args.steps
-            kname = "minmaxlttb_series_sharded (whole step)"
+            k_ms = step_ms
+            kname = "minmaxlttb_series_sharded (whole step: K1+K2 per shard, all_gather, merge, K3)"
+            kernel_timing = "whole step (device-timed region / steps)"
         elif op == "lttb":
             alg_bytes = pts * (ysz + 8)
-            k_ms = sum(stage_ms) or ms / args.steps
-            kname = "K3c full LTTB (means, candidates, tables, scan, verify, repair)"
+            k_ms = min(step_ms, sum(stage_ms) or step_ms)
+            kname = "K3c full LTTB, every launch of the step (" + "+".join(step_kernels) + ")"
+        elif kind == "fused" or plan is not None or stage_ms[0] <= 0:
+            # one kernel per step (fused per-series kernel) or a graph replay: the
+            # step IS the kernel, so the roofline uses the device-timed step
+            alg_bytes = pts * ysz
+            k_ms = step_ms
+            kname = ("k_mmlttb_fused (K1+K2+K3 per series, one launch)" if kind == "fused"
+                     else "whole minmaxlttb step (CUDA graph replay)")
+            kernel_timing = "whole step (device-timed region / steps)"
         else:
             alg_bytes = pts * ysz
-            k_ms = stage_ms[0]
-            kname = "k_extrema (K1)"
-            if k_ms <= 0:  # graph replay: stage events are not inside the captured graph
-                k_ms = ms / args.steps
-                kname = "whole minmaxlttb step (CUDA graph replay)"
+            k_ms = min(stage_ms[0], step_ms)
+            kname = [t for t in step_kernels if t.startswith("k_extrema")][0] + " (K1)"
         achieved = alg_bytes / (k_ms / 1e3) / 1e9
         tr = _traffic()
         traffic = None
@@ -486,7 +552,8 @@ def run_ours(args):
             traffic = tr.get("dram_bytes_per_launch")
         cpu = None
         if not args.no_cpu and ws == 1:
-            cpu = cpu_sample(name, seconds=args.cpu_seconds)
+            cpu = cpu_baseline_subprocess(name, steps=args.cpu_steps)
+        split = kind == "k1" and plan is None and stage_ms[2] > 0
         line = {
             "metric": METRIC,
             "value": value,
@@ -494,39 +561,43 @@ def run_ours(args):
             "n_gpus": ws,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": ms / args.steps,
+            "ms_per_step": step_ms,
             "higher_is_better": True,
             "scaling": scaling,
             "vs_baseline": None,
             "dtype": ydt,
             "data": "synthetic (device-generated, torch Philox; BASELINE.json recipe shapes)",
-            "config": {"workload": name, "n": n, "batch": batch, "n_out": n_out, "minmax_ratio": r_ps, "op": op,
-                       "sharding": ("bucket-range shards of one series + NCCL all_gather" if sharded
-                                    else "batch rows per rank" if name == "c4" and ws > 1 else
-                                    "independent replica per rank" if ws > 1 else "none"),
-                       "x_dtype": xdt, "graph": bool(plan is not None),
-                       "l2": "inputs larger than L2 (no flush needed)" if n * batch * (4 if ydt == "f32" else 8) > 126e6
-                       else "inputs smaller than L2: steady-state L2-resident repeat calls",
-                       "parity": parity},
+            "config": base_config(name, n, batch_total, n_out, r_ps, op, ydt, xdt),
+            "details": {"parity": parity,
+                        "sharding": ("bucket-range shards of one series + NCCL all_gather" if sharded
+                                     else "batch rows per rank" if name == "c4" and ws > 1 else
+                                     "independent replica per rank" if ws > 1 else "none"),
+                        "graph": bool(plan is not None), "rows_this_rank": batch,
+                        "l2": ("inputs larger than L2 (no flush needed)"
+                               if pts * (4 if ydt == "f32" else 8) > 126e6
+                               else "inputs smaller than L2: steady-state L2-resident repeat calls"),
+                        "kernels_per_step": step_kernels},
             "hbm_gbs": alg_bytes * args.steps / (ms / 1e3) / 1e9,
             "pct_roofline_e2e_device": alg_bytes * args.steps / (ms / 1e3) / 1e9 / peak,
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel_timing": f"CUDA events around the kernel on its stream, {stage_steps} live steps "
-                                          "right after the timed region"},
-            "stage_ms": {"k1_extrema": stage_ms[0], "k2_compact": stage_ms[1], "k3_lttb": stage_ms[2]},
-            # LTTB stage latency per output bucket (the sequential chain the
-            # tables + scan resolve); fused / graph paths do not split stages
-            "lttb_stage": None if stage_ms[2] <= 0 else {
-                "ms": stage_ms[2], "buckets": (n_out - 2) * batch,
-                "ns_per_bucket": stage_ms[2] * 1e6 / max(1, (n_out - 2) * batch)},
+                         "kernel_timing": kernel_timing},
+            "stage_ms": ({"k1_extrema": stage_ms[0], "k2_compact": stage_ms[1], "k3_lttb": stage_ms[2]}
+                         if split else None),
+            # LTTB stage latency per output bucket (the sequential chain the tables +
+            # scan resolve), only where the stages are separate launches
+            "lttb_stage": ({"ms": stage_ms[2], "buckets": (n_out - 2) * batch,
+                            "ns_per_bucket": stage_ms[2] * 1e6 / max(1, (n_out - 2) * batch)} if split else
+                           {"ms": k_ms, "buckets": (n_out - 2) * batch,
+                            "ns_per_bucket": k_ms * 1e6 / max(1, (n_out - 2) * batch)} if op == "lttb" else None),
             "cpu_baseline": cpu,
-            "e2e": None if e2e_value is None else {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": e2e_ms, "steps": e2e_steps,
-                    "path": ("minmaxlttb_series_sharded(pinned host x shard read in place, y shard H2D) -> CPU "
-                             "indices, per rank" if sharded else
-                             "minmaxlttb(pinned host x, pinned host y) -> numpy-free CPU tensor result")},
+            "e2e": None if e2e_value is None else {
+                "value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_ms, "steps": e2e_steps,
+                "path": ("minmaxlttb_series_sharded(pinned host x shard read in place, y shard H2D) -> CPU "
+                         "indices, per rank" if sharded else
+                         "minmaxlttb(pinned host x, pinned host y) -> numpy-free CPU tensor result")},
             "gpu_launches": int(launches),
             "lttb_repair_scans_per_step": repairs,
             "clocks": clocks.summary(),
@@ -538,6 +609,26 @@ def run_ours(args):
     return 0
 
 
+def relaunch_torchrun(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}; refusing to run "
+              "(no silent single-GPU fallback)", file=sys.stderr)
+        return 2
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -546,7 +637,7 @@ def main():
     ap.add_argument("--workload", default="c3_1e9", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-steps", type=int, default=5, help="timed reference runs for cpu_baseline (median)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--graph", action="store_true", help="device loop through MinMaxLTTBPlan (CUDA graph replay)")
@@ -555,6 +646,12 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        return relaunch_torchrun(args)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} disagrees with WORLD_SIZE={ws_env}; refusing to run", file=sys.stderr)
+        return 2
     return run_ours(args)
 
 

@@ -67,6 +67,12 @@ int64_t mmlttb_launch_count(void);
 int64_t mmlttb_repair_scans(void);
 int mmlttb_stage_timer(int enable);
 int mmlttb_stage_timer_read(double *ms3, int64_t *calls);
+/* Launch trace: while enabled, the names of the kernels this host thread
+ * launches are recorded; mmlttb_trace_read copies them comma-separated into
+ * buf (NUL-terminated, truncated to len-1), returns the full length and
+ * clears.  Stage boundaries are also NVTX ranges (no-ops without a tool). */
+int mmlttb_trace(int enable);
+int64_t mmlttb_trace_read(char *buf, int64_t len);
 
 /* Bytes of device workspace an operation needs for B series of N points. */
 int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int y_dtype);
@@ -198,6 +204,13 @@ int mmlttb_pixel_metrics(const uint8_t *a, const uint8_t *b, const uint8_t *mask
  * zeroed by this call. */
 int mmlttb_validate(const void *x, int x_dtype, const void *y, int y_dtype, int64_t N,
                     int32_t *flags, void *stream);
+/* The same for B series in one launch: row s is x + s*x_ld (x_ld 0: one
+ * shared x) and y + s*y_ld; flags[s] gets row s's bits (flags: B device
+ * int32, zeroed by this call).  A batch is B TimeSeries built in row order,
+ * so the first row with a nonzero word decides the error, and within a row
+ * bit 0 wins (core.py:89-92). */
+int mmlttb_validate_batch(const void *x, int x_dtype, int64_t x_ld, const void *y, int y_dtype, int64_t y_ld,
+                          int64_t B, int64_t N, int32_t *flags, void *stream);
 
 #ifdef __cplusplus
 }

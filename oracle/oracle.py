@@ -81,6 +81,8 @@ def lib() -> ctypes.CDLL:
         "or_m4": (i64, [p, i64, i64, p, ctypes.c_int]),
         "or_minmax_preselect_typed": (i64, [p, ctypes.c_int, i64, i64, i64, p, ctypes.c_int]),
         "or_minmaxlttb_typed": (i64, [p, ctypes.c_int, p, ctypes.c_int, i64, i64, i64, p, ctypes.c_int]),
+        "or_shard_preselect_typed": (i64, [p, ctypes.c_int, i64, i64, i64, i64, i64, i64, i64, ctypes.c_int,
+                                           ctypes.c_int, p, ctypes.c_int]),
         "or_max_threads": (ctypes.c_int, []),
     }
     for fn, (res, args) in sig.items():
@@ -195,6 +197,17 @@ def minmaxlttb_typed(xs, ys, n_out: int, r_ps: int = 4, threads: int = 0) -> np.
     out = np.empty(max(n_out, 0), dtype=np.int64)
     m = _check(lib().or_minmaxlttb_typed(_ptr(xs), xdt, _ptr(ys), ydt, ys.shape[0], n_out, r_ps,
                                          _ptr(out), threads))
+    return out[:m].copy()
+
+
+def shard_preselect_typed(ys_shard, lo: int, n: int, n_out: int, r_ps: int, b0: int, b1: int, emit_first: bool,
+                          emit_last: bool, threads: int = 0) -> np.ndarray:
+    """One rank's bucket-range share of minmax_preselect (global indices)."""
+    ys, ydt = _typed(ys_shard)
+    threads = threads or max_threads()
+    out = np.empty(2 * (b1 - b0) + 2, dtype=np.int64)
+    m = _check(lib().or_shard_preselect_typed(_ptr(ys), ydt, lo, ys.shape[0], n, n_out, r_ps, b0, b1,
+                                              int(emit_first), int(emit_last), _ptr(out), threads))
     return out[:m].copy()
 
 

@@ -344,6 +344,66 @@ int64_t or_minmaxlttb_typed(const void *xs, int xdt, const void *ys, int ydt, in
     return rc < 0 ? rc : n_out;
 }
 
+/* One rank's share of the bucket-range sharded preselection (the multi-GPU
+ * single-series path): sub-buckets [b0, b1) of partition(1, n-1, k)
+ * (core.py:161-175 over downsamplers.py:149-155), over a shard holding global
+ * elements [lo, lo + len), emitted as in minmax_preselect (:156-160): 0 first
+ * when emit_first, the interleaved pairs (:60-69) in global indices, n-1 last
+ * when emit_last.  Returns the count written to out. */
+int64_t or_shard_preselect_typed(const void *ys, int ydt, int64_t lo, int64_t len, int64_t n,
+                                 int64_t n_out, int64_t r_ps, int64_t b0, int64_t b1,
+                                 int emit_first, int emit_last, int64_t *out, int nthreads) {
+    if (n_out < 3 || n_out > n) return -1;
+    if (r_ps < 2 || r_ps % 2) return -4;
+    int64_t k = (n_out - 2) * (r_ps / 2);
+    if (k > n - 2) return -5;
+    if (b0 < 0 || b1 > k || b1 < b0) return -1;
+    int64_t nb = b1 - b0;
+    int64_t *bounds = (int64_t *)malloc(sizeof(int64_t) * (size_t)(3 * nb + 3));
+    if (!bounds) return -2;
+    int64_t *imin = bounds + nb + 1, *imax = imin + nb + 1;
+    int64_t smax = 1;
+    for (int64_t b = 0; b <= nb; ++b) bounds[b] = 1 + ((b0 + b) * (n - 2)) / k;
+    for (int64_t b = 0; b < nb; ++b)
+        if (bounds[b + 1] - bounds[b] > smax) smax = bounds[b + 1] - bounds[b];
+    int failed = 0;
+    for (int64_t b = 0; b <= nb; ++b)
+        if (bounds[b] < lo || bounds[b] > lo + len) failed = 1; /* the shard must cover its buckets */
+    if (failed) { free(bounds); return -1; }
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nthreads > 0 ? nthreads : 1)
+#endif
+    {
+        double *buf = (double *)malloc(sizeof(double) * (size_t)smax);
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+        for (int64_t b = 0; b < nb; ++b) {
+            if (!buf) continue;
+            int64_t a0 = bounds[b], a1 = bounds[b + 1];
+            for (int64_t i = a0; i < a1; ++i) buf[i - a0] = or_load(ys, ydt, i - lo);
+            int64_t a, c;
+            or_argminmax_range((const int64_t *)buf, 0, a1 - a0, &a, &c);
+            imin[b] = a + a0;
+            imax[b] = c + a0;
+        }
+        if (!buf) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            failed = 1;
+        }
+        free(buf);
+    }
+    if (failed) { free(bounds); return -2; }
+    int64_t m = 0;
+    if (emit_first) out[m++] = 0;
+    m += or_interleave_minmax(imin, imax, nb, out + m);
+    if (emit_last) out[m++] = n - 1;
+    free(bounds);
+    return m;
+}
+
 int or_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -38,6 +38,8 @@ _SIGS = {
     "mmlttb_repair_scans": (_i64, []),
     "mmlttb_stage_timer": (_i32, [_i32]),
     "mmlttb_stage_timer_read": (_i32, [_p, _p]),
+    "mmlttb_trace": (_i32, [_i32]),
+    "mmlttb_trace_read": (_i64, [_p, _i64]),
     "mmlttb_workspace_bytes": (_i64, [_i32, _i64, _i64, _i64, _i64, _i32]),
     "mmlttb_minmaxlttb": (_i32, [_p, _i32, _i64, _p, _i32, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _i64, _p]),
     "mmlttb_minmax_preselect": (_i32, [_p, _i32, _i64, _i64, _i64, _i64, _i64, _p, _i64, _p, _p, _i64, _p]),
@@ -59,6 +61,7 @@ _SIGS = {
     "mmlttb_lttb_preselected_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "mmlttb_lttb_preselected": (_i32, [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _i64, _p]),
     "mmlttb_validate": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
+    "mmlttb_validate_batch": (_i32, [_p, _i32, _i64, _p, _i32, _i64, _i64, _i64, _p, _p]),
     "mmlttb_deinterleave_f64": (_i32, [_p, _i64, _p, _p, _p]),
     "mmlttb_raster_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "mmlttb_rasterize": (_i32, [_p, _i32, _p, _i32, _p, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,

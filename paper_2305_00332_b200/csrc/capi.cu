@@ -8,6 +8,8 @@
 #include "host.cuh"
 #include "raster.cuh"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: a no-op unless a tool (nsys / ncu) is attached
+
 namespace mmh {
 
 thread_local std::string g_err;
@@ -24,9 +26,17 @@ int fail(int code, const char* fmt, ...) {
 }
 
 std::atomic<int64_t> g_launches{0};
+// launch trace (mmlttb_trace): kernel names of this thread's calls, for
+// bench.py's launch list and roofline labels
+thread_local bool g_trace_on = false;
+thread_local std::string g_trace;
 
 int check_launch(const char* what) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_trace_on) {
+    if (!g_trace.empty()) g_trace += ',';
+    g_trace += what;
+  }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   return MM_OK;
@@ -43,7 +53,11 @@ struct StageTimer {
 };
 thread_local StageTimer g_timer;
 
+// NVTX range per stage of a fused entry (K1 | K2 | K3), matching the events
 void stage_mark(cudaStream_t st, int i) {
+  static const char* names[3] = {"mmlttb K1 extrema", "mmlttb K2 compact", "mmlttb K3 lttb"};
+  if (i > 0) nvtxRangePop();
+  if (i < 3) nvtxRangePushA(names[i]);
   if (!g_timer.on) return;
   if (g_timer.used == g_timer.pool.size()) {
     cudaEvent_t e;
@@ -95,11 +109,31 @@ int launch_pairs(PairArgs pa, int64_t B, cudaStream_t st) {
 }
 
 // First 256 bytes of every fused entry's workspace: status word (bit 0 =
-// non-finite y seen), zeroed on the stream at entry.
+// non-finite y seen), zeroed on the stream at entry (not between the chunks of
+// one call split by batch_chunks, so the word ORs over the whole batch).
+thread_local bool g_chunk_cont = false;
 int* take_status(Carve& cv, cudaStream_t st) {
   int* p = cv.take<int>(1);
-  if (p && cudaMemsetAsync(p, 0, sizeof(int), st) != cudaSuccess) return nullptr;
+  if (p && !g_chunk_cont && cudaMemsetAsync(p, 0, sizeof(int), st) != cudaSuccess) return nullptr;
   return p;
+}
+
+// Batches above the 65,535-series grid.y limit of the per-series kernels run
+// as stream-ordered chunks over the same workspace (each chunk needs no more
+// than the whole batch's workspace).  f(s0, b) runs series [s0, s0 + b).
+constexpr int64_t MAX_CHUNK_B = 65535;
+template <typename F>
+int batch_chunks(int64_t B, F f) {
+  int rc = MM_OK;
+  for (int64_t s0 = 0; s0 < B && rc == MM_OK; s0 += MAX_CHUNK_B) {
+    g_chunk_cont = s0 > 0;
+    rc = f(s0, std::min<int64_t>(MAX_CHUNK_B, B - s0));
+  }
+  g_chunk_cont = false;
+  return rc;
+}
+inline const void* elem_off(const void* p, int dt, int64_t i) {
+  return p ? (const void*)((const char*)p + i * esize(dt)) : nullptr;
 }
 
 int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
@@ -121,6 +155,23 @@ int64_t mmlttb_launch_count(void) { return g_launches.load(); }
 
 int64_t mmlttb_repair_scans(void) {
   return repair_scans_read();
+}
+
+int mmlttb_trace(int enable) {
+  g_trace_on = enable != 0;
+  g_trace.clear();
+  return MM_OK;
+}
+
+int64_t mmlttb_trace_read(char* buf, int64_t len) {
+  const int64_t n = (int64_t)g_trace.size();
+  if (buf && len > 0) {
+    const int64_t c = std::min<int64_t>(n, len - 1);
+    memcpy(buf, g_trace.data(), (size_t)c);
+    buf[c] = 0;
+  }
+  g_trace.clear();
+  return n;
 }
 
 int mmlttb_stage_timer(int enable) {
@@ -169,7 +220,7 @@ int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int6
   return 0;
 }
 
-int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out,
+static int preselect_entry(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out,
                             int64_t r_ps, int64_t* out, int64_t out_ld, int64_t* out_count, void* workspace,
                             int64_t workspace_bytes, void* stream) {
   int rc = check_common(y, y_dtype, B, N, n_out);
@@ -229,17 +280,21 @@ static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t 
 
 int mmlttb_minmax(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int64_t* out,
                   int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream) {
-  return minmax_impl(y, y_dtype, y_ld, B, N, n_out, 0, 0, out, out_count, workspace, workspace_bytes,
-                            (cudaStream_t)stream);
+  return batch_chunks(B, [&](int64_t s0, int64_t b) {
+    return minmax_impl(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, 0, 0, out + s0 * n_out,
+                       out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, (cudaStream_t)stream);
+  });
 }
 
 int mmlttb_m4(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int64_t* out,
               int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream) {
-  return minmax_impl(y, y_dtype, y_ld, B, N, n_out, 1, 0, out, out_count, workspace, workspace_bytes,
-                            (cudaStream_t)stream);
+  return batch_chunks(B, [&](int64_t s0, int64_t b) {
+    return minmax_impl(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, 1, 0, out + s0 * n_out,
+                       out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, (cudaStream_t)stream);
+  });
 }
 
-int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
+static int minmaxlttb_entry(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
                       int64_t N, int64_t n_out, int64_t r_ps, int64_t* out, int64_t* out_count, void* workspace,
                       int64_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -305,23 +360,6 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   pa.x = x; pa.xdt = x_dtype; pa.x_ld = x_ld;
   pa.y = y; pa.ydt = y_dtype; pa.y_ld = y_ld;
   pa.out_x = px; pa.out_y = py; pa.status = status;
-  {  // K2 + K3a in one cooperative launch when it fits (small B, r_ps <= 8)
-    LttbArgs la{};
-    la.x = px; la.x_ld = cap; la.y = py; la.y_ld = cap;
-    la.m_dev = cnt; la.n = 0; la.bounds = nullptr; la.map = pre; la.map_ld = cap;
-    la.B = B; la.n_out = n_out; la.out = out; la.tables = lt;
-    bool launched = false;
-    if ((rc = launch_coop(pa, la, B, smax_for(r_ps), st, &launched))) return rc;
-    if (launched) {
-      stage_mark(st, 2);
-      stage_mark(st, 3);
-      if (out_count) {
-        k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
-        return check_launch("k_fill");
-      }
-      return MM_OK;
-    }
-  }
   if ((rc = launch_pairs(pa, B, st))) return rc;
   stage_mark(st, 2);
   // K3: LTTB over the compacted sub-series, mapped back (:208-209)
@@ -338,7 +376,7 @@ int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, i
   return MM_OK;
 }
 
-int mmlttb_lttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
+static int lttb_entry(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
                 int64_t N, int64_t n_out, int64_t* out, void* workspace, int64_t workspace_bytes, void* stream) {
   int rc = check_common(y, y_dtype, B, N, n_out);
   if (rc) return rc;
@@ -351,6 +389,33 @@ int mmlttb_lttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_d
   la.m_dev = nullptr; la.n = N; la.bounds = nullptr; la.map = nullptr;
   la.B = B; la.n_out = n_out; la.out = out; la.tables = (unsigned char*)workspace;
   return launch_lttb(la, x_dtype, y_dtype, s, (cudaStream_t)stream);
+}
+
+int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out,
+                            int64_t r_ps, int64_t* out, int64_t out_ld, int64_t* out_count, void* workspace,
+                            int64_t workspace_bytes, void* stream) {
+  return batch_chunks(B, [&](int64_t s0, int64_t b) {
+    return preselect_entry(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, r_ps, out + s0 * out_ld,
+                           out_ld, out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, stream);
+  });
+}
+
+int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
+                      int64_t N, int64_t n_out, int64_t r_ps, int64_t* out, int64_t* out_count, void* workspace,
+                      int64_t workspace_bytes, void* stream) {
+  return batch_chunks(B, [&](int64_t s0, int64_t b) {
+    return minmaxlttb_entry(elem_off(x, x_dtype, s0 * x_ld), x_dtype, x_ld, elem_off(y, y_dtype, s0 * y_ld), y_dtype,
+                            y_ld, b, N, n_out, r_ps, out + s0 * n_out, out_count ? out_count + s0 : nullptr,
+                            workspace, workspace_bytes, stream);
+  });
+}
+
+int mmlttb_lttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
+                int64_t N, int64_t n_out, int64_t* out, void* workspace, int64_t workspace_bytes, void* stream) {
+  return batch_chunks(B, [&](int64_t s0, int64_t b) {
+    return lttb_entry(elem_off(x, x_dtype, s0 * x_ld), x_dtype, x_ld, elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld,
+                      b, N, n_out, out + s0 * n_out, workspace, workspace_bytes, stream);
+  });
 }
 
 int mmlttb_every_nth(int64_t N, int64_t n_out, int64_t* out, void* stream) {
@@ -549,16 +614,24 @@ int mmlttb_pixel_metrics(const uint8_t* a, const uint8_t* b, const uint8_t* mask
   return check_launch("k_metrics_final");
 }
 
-int mmlttb_validate(const void* x, int x_dtype, const void* y, int y_dtype, int64_t N, int32_t* flags, void* stream) {
-  if (!x || !y || !flags || N < 1 || !xdt_ok(x_dtype) || !ydt_ok(y_dtype)) return fail(MM_EINVAL, "bad arguments");
+int mmlttb_validate_batch(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld,
+                          int64_t B, int64_t N, int32_t* flags, void* stream) {
+  if (!x || !y || !flags || N < 1 || B < 1 || !xdt_ok(x_dtype) || !ydt_ok(y_dtype) || x_ld < 0 || y_ld < N ||
+      (x_ld != 0 && x_ld < N))
+    return fail(MM_EINVAL, "bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  if (cudaMemsetAsync(flags, 0, sizeof(int32_t), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
-  const bool al = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);  // 16-byte loads of 4 elements
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(al ? cdiv(N, 4) : N, 256), 148 * 8);
-#define MM_V(XT, YT)                                                                                 \
-  do {                                                                                               \
-    if (al) k_validate<XT, YT><<<blocks, 256, 0, st>>>((const XT*)x, (const YT*)y, N, (int*)flags);  \
-    else k_validate_scalar<XT, YT><<<blocks, 256, 0, st>>>((const XT*)x, (const YT*)y, N, (int*)flags); \
+  if (cudaMemsetAsync(flags, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return fail(MM_ECUDA, "memset");
+  const bool al = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && (x_ld * esize(x_dtype)) % 16 == 0 &&
+                  (y_ld * esize(y_dtype)) % 16 == 0;  // 16-byte loads of 4 elements on every row
+  const int64_t per = cdiv(al ? cdiv(N, 4) : N, 256);
+  const int64_t want = (int64_t)sm_count() * 8;  // ~8 CTAs per SM over the whole batch
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(per, cdiv(want, B)));
+  const unsigned gy = (unsigned)std::min<int64_t>(B, 65535);
+  const dim3 g(gx, gy);
+#define MM_V(XT, YT)                                                                                                \
+  do {                                                                                                              \
+    if (al) k_validate<XT, YT><<<g, 256, 0, st>>>((const XT*)x, (const YT*)y, N, x_ld, y_ld, B, (int*)flags);        \
+    else k_validate_scalar<XT, YT><<<g, 256, 0, st>>>((const XT*)x, (const YT*)y, N, x_ld, y_ld, B, (int*)flags);    \
   } while (0)
   if (y_dtype == MM_F32) {
     switch (x_dtype) {
@@ -577,6 +650,10 @@ int mmlttb_validate(const void* x, int x_dtype, const void* y, int y_dtype, int6
   }
 #undef MM_V
   return check_launch("k_validate");
+}
+
+int mmlttb_validate(const void* x, int x_dtype, const void* y, int y_dtype, int64_t N, int32_t* flags, void* stream) {
+  return mmlttb_validate_batch(x, x_dtype, 0, y, y_dtype, N, 1, N, flags, stream);
 }
 
 }  // extern "C"

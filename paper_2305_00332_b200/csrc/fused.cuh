@@ -24,9 +24,6 @@ struct FusedArgs {
   int64_t B, N, n_out, r_ps;
   int64_t* out;                 // [B][n_out]
   int* status;                  // bit 0: non-finite y seen (may be null)
-  int64_t tile_bytes, stages;   // k_mmlttb_fused_tma: ring geometry (0 otherwise)
-  int64_t tile_buckets;
-  int64_t dbg;                  // tuning probe: bit 0 skip phase-1 math, bit 1 skip phases 2-3
 };
 
 // shared-memory bytes for a series with k sub-buckets (m <= 2k + 2 points);
@@ -189,120 +186,6 @@ __global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused(FusedArgs a) {
   fused_phase23<XT, YT, SMAX, NT>(a, s, sm, sh_scan);
 }
 
-// ---- TMA-fed persistent variant --------------------------------------------
-// Phase 1 is decoupled from HBM latency: one thread streams each series as a
-// sequence of tiles (tile_buckets whole sub-buckets, widened to 16-byte
-// alignment) with cp.async.bulk into a ring of `stages` shared-memory slots,
-// completion signalled on an mbarrier per slot; the warps reduce each tile's
-// buckets from shared memory (one warp per bucket) and the slot is refilled
-// with the tile `stages` ahead -- across series boundaries, so the next
-// series' first tiles stream in while this one runs phases 2-3.  Bytes in
-// flight no longer depend on registers or on how many warps are between
-// loads; the CTA is persistent (grid = resident CTAs), series
-// blockIdx.x, blockIdx.x + gridDim.x, ...
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(b))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-          smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-
-// First-occurrence argmin/argmax of a shared-memory range by a G-lane group
-// (lane = index within the group; lexicographic (key, offset), the same
-// result as group_extrema).  Lanes read consecutive 16-byte vectors, so a
-// group's quarter-warp touches 128 contiguous bytes (no bank conflicts); the
-// running extreme remembers only the vector, the element inside it is
-// resolved once at the end from shared memory.
-template <typename T, int G>
-__device__ __forceinline__ void smem_extrema(const T* base, int n, int lane, typename YTr<T>::K& mn, int& omn,
-                                             typename YTr<T>::K& mx, int& omx) {
-  typedef YTr<T> Tr;
-  typedef typename Tr::K K;
-  mn = Tr::kmax();
-  mx = Tr::kmin();
-  omn = INT_MAX;
-  omx = INT_MAX;
-  auto key1 = [](T v) -> K {
-    if constexpr (sizeof(T) == 4) return key32(__float_as_uint(v));
-    else return key64((unsigned long long)__double_as_longlong(v));
-  };
-  if (n > 0) {
-    int head = (int)(((16u - (smem_u32(base) & 15u)) & 15u) / sizeof(T));
-    if (head > n) head = n;
-    if (lane < head) {
-      const K kk = key1(base[lane]);
-      mn = kk; mx = kk; omn = omx = lane;
-    }
-    const int nvec = (n - head) / Tr::VEC;
-    const uint4* vp = reinterpret_cast<const uint4*>(base + head);
-    int vmn = -1, vmx = -1;  // vector holding the running extreme (-1: none / scalar)
-#pragma unroll 4
-    for (int v = lane; v < nvec; v += G) {
-      K kk[Tr::VEC];
-      Tr::keys(vp[v], kk);
-      K vl = kk[0], vh = kk[0];
-#pragma unroll
-      for (int e = 1; e < Tr::VEC; ++e) { vl = min(vl, kk[e]); vh = max(vh, kk[e]); }
-      if (vl < mn) { mn = vl; vmn = v; }
-      if (vh > mx) { mx = vh; vmx = v; }
-    }
-    const int tp = head + nvec * Tr::VEC + lane;
-    if (tp < n) {
-      const K kk = key1(base[tp]);
-      if (kk < mn) { mn = kk; omn = tp; vmn = -1; }
-      if (kk > mx) { mx = kk; omx = tp; vmx = -1; }
-    }
-    if (vmn >= 0) {
-      K kk[Tr::VEC];
-      Tr::keys(vp[vmn], kk);
-      int e = Tr::VEC - 1;
-#pragma unroll
-      for (int q = Tr::VEC - 1; q >= 0; --q) if (kk[q] == mn) e = q;
-      omn = head + vmn * Tr::VEC + e;
-    }
-    if (vmx >= 0) {
-      K kk[Tr::VEC];
-      Tr::keys(vp[vmx], kk);
-      int e = Tr::VEC - 1;
-#pragma unroll
-      for (int q = Tr::VEC - 1; q >= 0; --q) if (kk[q] == mx) e = q;
-      omx = head + vmx * Tr::VEC + e;
-    }
-  }
-  if constexpr (G == 32 && sizeof(K) == 4) {  // whole warp, 32-bit keys: REDUX
-    const int kmn = __reduce_min_sync(FULL, (int)mn);
-    const int kmx = __reduce_max_sync(FULL, (int)mx);
-    omn = (int)__reduce_min_sync(FULL, (int)mn == kmn ? (unsigned)omn : 0xffffffffu);
-    omx = (int)__reduce_min_sync(FULL, (int)mx == kmx ? (unsigned)omx : 0xffffffffu);
-    mn = kmn;
-    mx = kmx;
-  } else {
-#pragma unroll
-    for (int off = G / 2; off; off >>= 1) {
-      const K omn2 = __shfl_xor_sync(FULL, mn, off);
-      const int oo = __shfl_xor_sync(FULL, omn, off);
-      if (omn2 < mn || (omn2 == mn && oo < omn)) { mn = omn2; omn = oo; }
-      const K omx2 = __shfl_xor_sync(FULL, mx, off);
-      const int oq = __shfl_xor_sync(FULL, omx, off);
-      if (omx2 > mx || (omx2 == mx && oq < omx)) { mx = omx2; omx = oq; }
-    }
-  }
-}
-
 // floor(b * L / k) stepped by a fixed number of buckets with adds only
 // (quotient + remainder), so the per-bucket bounds of partition(1, N-1, k)
 // cost no 64-bit division inside the streaming loop.
@@ -321,136 +204,6 @@ struct BoundIter {
     if (r >= k) { r -= k; ++v; }
   }
 };
-
-// Element range [e_lo, e_hi) of the bulk copy for a tile covering [lo, hi):
-// widened to 128-byte lines of the absolute address (the bulk-copy engine
-// moves whole lines at full rate; a merely 16-byte-aligned source is split
-// into small requests), clipped to the row start and to the row's last
-// 16-byte-aligned element (anything past it is read directly).
-// row_off = (row base address % 128) / sizeof(YT).
-template <typename YT>
-__device__ __forceinline__ void tile_span(int64_t lo, int64_t hi, int64_t N, int64_t row_off, int64_t& e_lo,
-                                          int64_t& e_hi) {
-  constexpr int64_t V = 16 / sizeof(YT), A = 128 / sizeof(YT);
-  e_lo = max((int64_t)0, ((row_off + lo) & ~(A - 1)) - row_off);
-  e_hi = min(((row_off + hi + A - 1) & ~(A - 1)) - row_off, N & ~(V - 1));
-  if (e_hi < e_lo) e_hi = e_lo;
-}
-
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-
-// Tiles hold tile_buckets = R * j whole sub-buckets (R = NW * 32/G groups
-// of G lanes); group g of the CTA reduces buckets g, g + R, ... of every tile
-// (bounds stepped by BoundIter: adds only), each warp arrives on the slot's
-// `empty` barrier, and thread 0 refills the slot once all NW warps have
-// arrived -- no block-wide barrier per tile.
-template <typename XT, typename YT, int SMAX, int NT, int MINB, int G>
-__global__ void __launch_bounds__(NT, MINB) k_mmlttb_fused_tma(FusedArgs a) {
-  typedef YTr<YT> Tr;
-  typedef typename Tr::K K;
-  constexpr int NW = NT / 32, R = NT / G;
-  extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ int sh_scan[NT / 32 + 1];
-  __shared__ unsigned long long full[8], empty[8];
-  __shared__ long long s_elo[8];
-
-  const int64_t N = a.N;
-  const int64_t k = (a.n_out - 2) * (a.r_ps / 2);
-  const int64_t L = N - 2;
-  const int64_t TB = a.tile_buckets, NS = a.stages;
-  const int64_t tiles = (k + TB - 1) / TB;  // per series
-  const int64_t nser = (a.B - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t total = nser * tiles;
-  const int64_t p_bytes = (fused_smem(k, a.n_out - 2, SMAX, (int)sizeof(YT)) + 127) / 128 * 128;
-  unsigned char* ring = sm + p_bytes;
-  YT* s_vlo = reinterpret_cast<YT*>(sm);
-  YT* s_vhi = s_vlo + k;
-  int* s_lo = reinterpret_cast<int*>(s_vhi + k);
-  int* s_hi = s_lo + k;
-  const int lane = threadIdx.x & 31;
-
-  // producer state (thread 0): tile t of series j, bounds of its first bucket
-  int64_t pq = 0, pt = 0, pj = 0;
-  BoundIter pb;
-  pb.init(0, TB, L, k);
-  auto produce = [&]() {  // issue tile pq into slot pq % NS
-    if (pq >= total) return;
-    const int st = (int)(pq % NS);
-    if (pq >= NS) mbar_wait(&empty[st], (unsigned)((pq / NS - 1) & 1));
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const int64_t lo = pb.v;
-    pb.next();
-    const int64_t hi = pt + 1 == tiles ? N - 1 : pb.v;
-    const int64_t s = blockIdx.x + pj * gridDim.x;
-    const YT* row = (const YT*)a.y + s * a.y_ld;
-    int64_t e_lo, e_hi;
-    tile_span<YT>(lo, hi, N, (int64_t)(((uintptr_t)row & 127) / sizeof(YT)), e_lo, e_hi);
-    s_elo[st] = e_lo;
-    const unsigned bytes = (unsigned)((e_hi - e_lo) * (int64_t)sizeof(YT));
-    mbar_arrive_tx(&full[st], bytes);
-    if (bytes) bulk_g2s(ring + st * a.tile_bytes, row + e_lo, bytes, &full[st]);
-    ++pq;
-    if (++pt == tiles) { pt = 0; ++pj; pb.init(0, TB, L, k); }
-  };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int i = 0; i < NS; ++i) produce();
-  }
-  __syncthreads();
-
-  int64_t q = 0;
-  for (int64_t j = 0; j < nser; ++j) {
-    const int64_t s = blockIdx.x + j * gridDim.x;
-    const YT* ys = (const YT*)a.y + s * a.y_ld;
-    const int grp = threadIdx.x / G, gl = threadIdx.x & (G - 1);
-    BoundIter wb;  // lower bound of this group's next bucket
-    wb.init(grp, R, L, k);
-    BoundIter wn;  // ... and of the bucket after it
-    wn.init(grp + 1, R, L, k);
-    for (int64_t t = 0; t < tiles; ++t, ++q) {
-      const int st = (int)(q % NS);
-      mbar_wait(&full[st], (unsigned)((q / NS) & 1));
-      const int64_t e_lo = *(volatile long long*)&s_elo[st];
-      const int64_t e_hi_row = N & ~(int64_t)(16 / sizeof(YT) - 1);
-      YT* tile = reinterpret_cast<YT*>(ring + st * a.tile_bytes);
-      const int64_t b0 = t * TB, b1 = min(k, b0 + TB);
-      const int64_t rounds = (b1 - b0 + R - 1) / R;  // warp-uniform (group shuffles)
-      for (int64_t r = 0; r < rounds && !(a.dbg & 1); ++r) {
-        const int64_t b = b0 + r * R + grp;
-        int64_t blo = 0, bhi = 0;
-        if (b < b1) {
-          blo = wb.v;
-          bhi = wn.v;
-          wb.next();
-          wn.next();
-          if (bhi > e_hi_row)  // row tail past the last aligned element: fetch it directly
-            for (int64_t e = max(blo, e_hi_row) + gl; e < bhi; e += G) tile[e - e_lo] = ys[e];
-        }
-        __syncwarp();
-        K mn, mx;
-        int omn, omx;
-        smem_extrema<YT, G>(tile + (blo - e_lo), (int)(bhi - blo), gl, mn, omn, mx, omx);
-        if (gl == 0 && b < b1) {
-          if (a.status && keys_nonfinite((long long)mn, (long long)mx, sizeof(YT) == 4 ? 0 : 1)) atomicOr(a.status, 1);
-          const bool mfirst = omn <= omx;
-          s_lo[b] = (int)(blo + (mfirst ? omn : omx));
-          s_hi[b] = (int)(blo + (mfirst ? omx : omn));
-          s_vlo[b] = (YT)key_value<YT>((long long)(mfirst ? mn : mx));
-          s_vhi[b] = (YT)key_value<YT>((long long)(mfirst ? mx : mn));
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      if (threadIdx.x == 0) produce();
-    }
-    __syncthreads();  // all phase-1 results of series s are in shared memory
-    if (!(a.dbg & 2)) fused_phase23<XT, YT, SMAX, NT>(a, s, sm, sh_scan);
-    __syncthreads();  // phase-3 aliases of the phase-1 arrays are dead
-  }
-}
 
 }  // namespace mm
 
@@ -695,77 +448,6 @@ __global__ void __launch_bounds__(NT) k_post_smem(PostArgs a) {
   if (threadIdx.x == 0) {
     out[0] = 0;
     out[k3 + 1] = N - 1;
-  }
-}
-
-}  // namespace mm
-
-#include <cooperative_groups.h>
-
-namespace mm {
-
-// ---------------------------------------------------------------------------
-// K2 + K3a as ONE cooperative launch (single / few series): the multi-CTA
-// compaction (compact_pairs_tile), a grid barrier, the transition tables
-// split over the same CTAs (next-bucket means recomputed per item: <= SMAX
-// points), a grid barrier, then CTA 0 of each series resolves the chain.
-// Replaces three dependent launches (and their fixed latencies) by one.
-template <typename XT, typename YT, int SMAX, int NT, int ITEMS>
-__global__ void __launch_bounds__(NT) k_post_coop(PairArgs pa, LttbArgs la, int64_t ntiles) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  const int64_t s = blockIdx.y, tile = blockIdx.x;
-  compact_pairs_tile<XT, YT, NT, ITEMS>(pa, s, tile, ntiles);
-  grid.sync();
-  const int64_t k3 = la.n_out - 2;
-  const int64_t m = __ldcg(la.m_dev + s);
-  const double* px = (const double*)la.x + s * la.x_ld;
-  const double* py = (const double*)la.y + s * la.y_ld;
-  auto lb = [&](int64_t b) -> int64_t { return 1 + (b * (m - 2)) / k3; };
-  const int64_t items = k3 * SMAX;
-  const int64_t per = (items + ntiles - 1) / ntiles;
-  const int64_t i0 = tile * per, i1 = min(items, i0 + per);
-  unsigned char* tab = la.tables + s * la.tab_ld;
-  for (int64_t it = i0 + threadIdx.x; it < i1; it += NT) {
-    const int64_t b = it / SMAX;
-    const int p = (int)(it % SMAX);
-    const int64_t blo = lb(b), bhi = lb(b + 1);
-    const bool valid = b == 0 ? p == 0 : p < blo - lb(b - 1);
-    unsigned char r = 0;
-    if (valid) {
-      const int64_t ap = b == 0 ? 0 : lb(b - 1) + p;
-      double cx, cy;  // mean of bucket b+1, in-order sums (_kernels.py:95-104), or the last point
-      if (b + 1 < k3) {
-        const int64_t nlo = bhi, nhi = lb(b + 2);
-        double sx = 0.0, sy = 0.0;
-        for (int64_t j = nlo; j < nhi; ++j) {
-          sx = __dadd_rn(sx, __ldcg(px + j));
-          sy = __dadd_rn(sy, __ldcg(py + j));
-        }
-        const double cnt = (double)(nhi - nlo);
-        cx = __ddiv_rn(sx, cnt);
-        cy = __ddiv_rn(sy, cnt);
-      } else {
-        cx = __ldcg(px + m - 1);
-        cy = __ldcg(py + m - 1);
-      }
-      const double ax = __ldcg(px + ap), ay = __ldcg(py + ap);
-      long long best = -1;
-      for (int64_t j = blo; j < bhi; ++j) {
-        const long long ar = lttb_area_key(ax, ay, cx, cy, __ldcg(px + j), __ldcg(py + j));
-        if (ar > best) { best = ar; r = (unsigned char)(j - blo); }
-      }
-    }
-    tab[it] = r;
-  }
-  grid.sync();
-  if (tile != 0) return;
-  int64_t* out = la.out + s * la.n_out;
-  const int64_t* map = la.map + s * la.map_ld;
-  scan_chain<SMAX, NT, 8>(tab, k3, [&](int64_t b, int sel) { out[b + 1] = __ldcg(map + lb(b) + sel); });
-  if (threadIdx.x == 0) {
-    out[0] = __ldcg(map);
-    out[k3 + 1] = __ldcg(map + m - 1);
   }
 }
 

@@ -123,6 +123,19 @@ inline bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
 }
 
 
+// Opt a kernel into `bytes` of dynamic shared memory.  The attribute is per
+// device (context), so each launch site keeps one bit per device in `mask`.
+inline int smem_optin(std::atomic<unsigned long long>& mask, const void* kern, int bytes, const char* what) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(MM_ECUDA, "cudaGetDevice");
+  const unsigned long long bit = dev < 64 ? 1ULL << dev : 0ULL;
+  if (bit && (mask.load(std::memory_order_acquire) & bit)) return MM_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return fail(MM_ECUDA, "cudaFuncSetAttribute(%s)", what);
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return MM_OK;
+}
+
 inline bool mul_ok(int64_t a, int64_t b) { return a == 0 || b <= INT64_MAX / a; }
 
 // ---- K1 (k1_launch.cu) ----
@@ -156,11 +169,10 @@ bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt);
 int launch_fused(const FusedArgs& fa, int xdt, int ydt, cudaStream_t st);
 int sm_count();
 
-// ---- K2 + K3 single-CTA / cooperative (post_launch.cu) ----
+// ---- K2 + K3 single-CTA (post_launch.cu) ----
 constexpr int PAIR_NT = 128, PAIR_ITEMS = 2;
 bool post_ok(int64_t k, int64_t n_out, int64_t r_ps);
 int launch_post(const PostArgs& pa, int64_t B, int xdt, int ydt, int smax, cudaStream_t st);
-int launch_coop(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched);
 
 }  // namespace mmh
 

@@ -8,8 +8,9 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
     if (cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
     const int64_t blocks = cdiv(a.B * a.Ws, 8);
-    static const int64_t fv = env_i64("MMLTTB_K1_FLAT_VARIANT", 0);  // A/B knob (tools/flat_sweep.sh)
     if (ydt == MM_F32) {
+#ifdef MMLTTB_AB  // tuning build only (tools/flat_sweep.sh)
+      static const int64_t fv = env_i64("MMLTTB_K1_FLAT_VARIANT", 0);
       switch (fv) {
         case 1: k_extrema_flat<float, 6, 3, 4><<<(unsigned)blocks, 256, 0, st>>>(a); break;
         case 2: k_extrema_flat<float, 4, 3, 4><<<(unsigned)blocks, 256, 0, st>>>(a); break;
@@ -18,6 +19,9 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
         case 5: k_extrema_flat<float, 16, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
         default: k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
       }
+#else
+      k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+#endif
     } else {
       k_extrema_flat<double, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
     }
@@ -47,11 +51,12 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
   const int64_t blocks = cdiv(warps, 8);
   if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
   if (a.chunk >= (1LL << 30)) return fail(MM_ERANGE, "bucket chunk too large");
+  const unsigned g = (unsigned)blocks;
+#ifdef MMLTTB_AB  // tuning build only (tools/k1_sweep.sh)
   static const int variant = [] {
     const char* e = getenv("MMLTTB_K1_VARIANT");  // tuning knob, default = tuned choice
     return e ? atoi(e) : 0;
   }();
-  const unsigned g = (unsigned)blocks;
 #define MM_K1(T, U, L) k_extrema<T, U, L><<<g, 256, 0, st>>>(a)
 #define MM_K1B(T, U, L, MB) k_extrema<T, U, L, MB><<<g, 256, 0, st>>>(a)
   if (ydt == MM_F32) {
@@ -81,6 +86,12 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
   }
 #undef MM_K1
 #undef MM_K1B
+#else
+  if (ydt == MM_F32)
+    k_extrema<float, 8, 3><<<g, 256, 0, st>>>(a);  // tuned: U=8 vectors in flight, evict-first
+  else
+    k_extrema<double, 8, 3><<<g, 256, 0, st>>>(a);
+#endif
   return check_launch("k_extrema");
 }
 

@@ -1150,326 +1150,6 @@ __global__ void __launch_bounds__(NT) k_lttb_scan(LttbArgs a) {
   }
 }
 
-// Segmented chain resolution (k3 <= 64 * LTTB_SEG): two short kernels
-// instead of one CTA scanning every map.  Kernel 1: one warp per segment of
-// LTTB_SEG buckets stages the segment's transition maps in shared memory and
-// lane p walks them from entry p, overwriting each map row in place with the
-// path: row b becomes (T_b o ... o T_first)(p) for every entry p.  The
-// segment's last row is then its composed map M_s.  Kernel 2: each segment
-// composes M_0 .. M_{s-1} from entry 0 (the fixed first point) to get its
-// entry e_s, and every bucket's pick is row_b[e_s].
-constexpr int LTTB_SEG = 64;
-
-template <int W>
-__global__ void __launch_bounds__(32) k_lttb_seg_paths(LttbArgs a) {
-  __shared__ unsigned char t[LTTB_SEG][W];
-  const int64_t s = blockIdx.y, seg = blockIdx.x;
-  const int64_t k3 = a.n_out - 2;
-  const int64_t b0 = seg * LTTB_SEG;
-  const int n = (int)min((int64_t)LTTB_SEG, k3 - b0);
-  unsigned char* tab = a.tables + s * a.tab_ld + b0 * W;
-  const int lane = threadIdx.x;
-  for (int i = lane; i < n * W; i += 32) t[i / W][i % W] = tab[i];
-  __syncwarp();
-  if (lane < W) {
-    int st = lane;
-    for (int i = 0; i < n; ++i) {
-      st = t[i][st];
-      tab[i * W + lane] = (unsigned char)st;  // path row (reads come from the staged copy)
-    }
-  }
-}
-
-template <int W>
-__global__ void __launch_bounds__(64) k_lttb_seg_emit(LttbArgs a) {
-  __shared__ int s_e;
-  const int64_t s = blockIdx.y, seg = blockIdx.x;
-  const int64_t k3 = a.n_out - 2;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const unsigned char* tab = a.tables + s * a.tab_ld;
-  int64_t* out = a.out + s * a.n_out;
-  int64_t* pos = a.pos ? a.pos + s * a.pos_ld : nullptr;
-  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
-  const int64_t* cand = a.cand ? a.cand + s * a.cand_ld : nullptr;
-  // entry of this segment: the earlier segments' composed maps (their last path rows),
-  // staged in shared memory in parallel, then applied in order from entry 0
-  __shared__ unsigned char mrow[64][W];
-  for (int i = threadIdx.x; i < seg * W; i += blockDim.x)
-    mrow[i / W][i % W] = tab[((int64_t)(i / W) * LTTB_SEG + LTTB_SEG - 1) * W + i % W];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int e = 0;
-    for (int64_t t = 0; t < seg; ++t) e = mrow[t][e];
-    s_e = e;
-  }
-  __syncthreads();
-  const int e = s_e;
-  const int64_t b0 = seg * LTTB_SEG;
-  const int n = (int)min((int64_t)LTTB_SEG, k3 - b0);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int64_t b = b0 + i;
-    const int sel = tab[b * W + e];
-    const int64_t p = cand ? cand[b * W + sel] : lbound(a, m, b) + sel;
-    if (pos) pos[b + 1] = p;
-    else out[b + 1] = map ? map[p] : p;
-  }
-  if (seg == 0 && threadIdx.x == 0) {
-    if (pos) {
-      pos[0] = 0;
-      pos[k3 + 1] = m - 1;
-    } else {
-      out[0] = map ? map[0] : 0;
-      out[k3 + 1] = map ? map[m - 1] : m - 1;
-    }
-  }
-}
-
-// K3b, part 1: next-bucket means for every (series, bucket), one thread each.
-template <typename XT, typename YT>
-__global__ void k_lttb_means(LttbArgs a) {
-  const int64_t k3 = a.n_out - 2;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.B * k3) return;
-  const int64_t s = g / k3, b = g % k3;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  a.means[s * a.means_ld + b] =
-      lttb_next_mean(a, (const XT*)a.x + s * a.x_ld, (const YT*)a.y + s * a.y_ld, m, b);
-}
-
-// Large-bucket means: one warp per (series, bucket).  The in-order fp64 sum
-// is one dependent chain per bucket (it cannot be re-associated), so the
-// warp's lanes stream the bucket through a double-buffered shared-memory tile
-// with coalesced loads while lane 0 runs the chain (_kernels.py:98-104).
-template <typename XT, typename YT, int TILE>
-__global__ void __launch_bounds__(32) k_lttb_means_staged(LttbArgs a) {
-  __shared__ double s_t[1][2][2][TILE];  // [warp][buffer][x|y][i]
-  const int wid = 0, lane = threadIdx.x & 31;
-  const int64_t k3 = a.n_out - 2;
-  const int64_t g = (int64_t)blockIdx.x;
-  if (g >= a.B * (k3 + 1)) return;
-  // b = -1 .. k3-1: warp b scans bucket b+1 (b = -1 only for bucket 0's y range)
-  const int64_t s = g / (k3 + 1), b = g % (k3 + 1) - 1;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const XT* xs = (const XT*)a.x + s * a.x_ld;
-  const YT* ys = (const YT*)a.y + s * a.y_ld;
-  if (b + 1 < k3) {
-    const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
-    constexpr int PER = TILE / 32;
-    XT rx[PER];
-    YT ry[PER];
-    double ymn = INFINITY, ymx = -INFINITY;
-    // raw loads only: nothing consumes them until stash(), after the sums,
-    // so the next tile's latency hides behind lanes 0/1's add chains
-    auto fetch = [&](int64_t t0) {
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int64_t j = t0 + q * 32 + lane;
-        rx[q] = j < nhi ? xs[j] : (XT)0;
-        ry[q] = j < nhi ? ys[j] : (YT)0;
-      }
-    };
-    auto stash = [&](int buf, int64_t t0) {
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const double vy = (double)ry[q];
-        s_t[wid][buf][0][q * 32 + lane] = (double)rx[q];
-        s_t[wid][buf][1][q * 32 + lane] = vy;
-        if (t0 + q * 32 + lane < nhi) { ymn = fmin(ymn, vy); ymx = fmax(ymx, vy); }
-      }
-    };
-    // lane 0 carries the x chain, lane 1 the y chain: one DADD instruction
-    // advances both in-order sums (sx = 0.0; sx += x_j, _kernels.py:98-102)
-    double acc = 0.0;
-    const int which = lane & 1;
-    fetch(nlo);
-    stash(0, nlo);
-    __syncwarp();
-    int buf = 0;
-    for (int64_t t0 = nlo; t0 < nhi; t0 += TILE) {
-      const bool more = t0 + TILE < nhi;
-      if (more) fetch(t0 + TILE);  // in flight while lanes 0/1 sum this tile
-      if (lane < 2) {
-        const int n = (int)(nhi - t0 < TILE ? nhi - t0 : (int64_t)TILE);
-        const double* src = s_t[wid][buf][which];
-        int i = 0;
-        for (; i + 8 <= n; i += 8) {  // loads issued ahead of the dependent adds
-          double v[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = src[i + q];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
-        }
-        for (; i < n; ++i) acc = __dadd_rn(acc, src[i]);
-      }
-      __syncwarp();
-      if (more) stash(buf ^ 1, t0 + TILE);
-      __syncwarp();
-      buf ^= 1;
-    }
-    const double cnt = (double)(nhi - nlo);
-    const double sy = __shfl_sync(FULL, acc, 1);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      ymn = fmin(ymn, __shfl_xor_sync(FULL, ymn, o));
-      ymx = fmax(ymx, __shfl_xor_sync(FULL, ymx, o));
-    }
-    if (lane == 0) {
-      if (b >= 0) a.means[s * a.means_ld + b] = make_double2(__ddiv_rn(acc, cnt), __ddiv_rn(sy, cnt));
-      if (a.yrange) a.yrange[s * k3 + b + 1] = make_double2(ymn, ymx);
-    }
-  } else if (lane == 0) {
-    a.means[s * a.means_ld + b] = make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
-  }
-}
-
-// Same as k_lttb_means_staged with the global loads issued TWO tiles ahead
-// (two register buffers), so a tile's loads have two chain segments to land.
-template <typename XT, typename YT, int TILE>
-__global__ void __launch_bounds__(32) k_lttb_means_staged2(LttbArgs a) {
-  __shared__ double s_t[2][2][TILE];  // [buffer][x|y][i]
-  const int lane = threadIdx.x & 31;
-  const int64_t k3 = a.n_out - 2;
-  const int64_t g = (int64_t)blockIdx.x;
-  if (g >= a.B * (k3 + 1)) return;
-  const int64_t s = g / (k3 + 1), b = g % (k3 + 1) - 1;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const XT* xs = (const XT*)a.x + s * a.x_ld;
-  const YT* ys = (const YT*)a.y + s * a.y_ld;
-  if (b + 1 >= k3) {
-    if (lane == 0) a.means[s * a.means_ld + b] = make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
-    return;
-  }
-  const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
-  constexpr int PER = TILE / 32;
-  XT ax[PER], bx[PER];
-  YT ay[PER], by[PER];
-  double ymn = INFINITY, ymx = -INFINITY;
-  auto fetch = [&](XT* rx, YT* ry, int64_t t0) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int64_t j = t0 + q * 32 + lane;
-      rx[q] = j < nhi ? xs[j] : (XT)0;
-      ry[q] = j < nhi ? ys[j] : (YT)0;
-    }
-  };
-  auto stash = [&](int buf, const XT* rx, const YT* ry, int64_t t0) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const double vy = (double)ry[q];
-      s_t[buf][0][q * 32 + lane] = (double)rx[q];
-      s_t[buf][1][q * 32 + lane] = vy;
-      if (t0 + q * 32 + lane < nhi) { ymn = fmin(ymn, vy); ymx = fmax(ymx, vy); }
-    }
-  };
-  double acc = 0.0;
-  const int which = lane & 1;
-  auto chain = [&](int buf, int64_t t0) {
-    if (lane < 2) {
-      const int n = (int)(nhi - t0 < TILE ? nhi - t0 : (int64_t)TILE);
-      const double* src = s_t[buf][which];
-      int i = 0;
-      for (; i + 8 <= n; i += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = src[i + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
-      }
-      for (; i < n; ++i) acc = __dadd_rn(acc, src[i]);
-    }
-  };
-  fetch(ax, ay, nlo);
-  fetch(bx, by, nlo + TILE);
-  stash(0, ax, ay, nlo);
-  fetch(ax, ay, nlo + 2 * TILE);
-  __syncwarp();
-  for (int64_t t0 = nlo; t0 < nhi; t0 += 2 * TILE) {
-    chain(0, t0);  // tile t0; b* holds t0+T, a* holds t0+2T (in flight)
-    __syncwarp();
-    if (t0 + TILE >= nhi) break;
-    stash(1, bx, by, t0 + TILE);
-    fetch(bx, by, t0 + 3 * TILE);
-    __syncwarp();
-    chain(1, t0 + TILE);
-    __syncwarp();
-    if (t0 + 2 * TILE >= nhi) break;
-    stash(0, ax, ay, t0 + 2 * TILE);
-    fetch(ax, ay, t0 + 4 * TILE);
-    __syncwarp();
-  }
-  const double cnt = (double)(nhi - nlo);
-  const double sy = __shfl_sync(FULL, acc, 1);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    ymn = fmin(ymn, __shfl_xor_sync(FULL, ymn, o));
-    ymx = fmax(ymx, __shfl_xor_sync(FULL, ymx, o));
-  }
-  if (lane == 0) {
-    if (b >= 0) a.means[s * a.means_ld + b] = make_double2(__ddiv_rn(acc, cnt), __ddiv_rn(sy, cnt));
-    if (a.yrange) a.yrange[s * k3 + b + 1] = make_double2(ymn, ymx);
-  }
-}
-
-// K3b, part 2: one CTA per series carries the bucket-to-bucket dependency.
-template <typename XT, typename YT, int NT>
-__global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
-  __shared__ long long s_area[NT / 32];
-  __shared__ long long s_idx[NT / 32];
-  __shared__ long long s_prev;
-  const int64_t s = blockIdx.x;
-  const int64_t k3 = a.n_out - 2;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const XT* xs = (const XT*)a.x + s * a.x_ld;
-  const YT* ys = (const YT*)a.y + s * a.y_ld;
-  const double2* means = a.means + s * a.means_ld;
-  int64_t* out = a.out + s * a.n_out;
-  const int64_t* map = a.map ? a.map + s * a.map_ld : nullptr;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int64_t prev = 0;
-  int64_t blo = lbound(a, m, 0);
-  for (int64_t b = 0; b < k3; ++b) {
-    const int64_t bhi = lbound(a, m, b + 1);
-    const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
-    const double2 c = means[b];
-    long long best = -1;
-    long long bi = INT64_MAX;
-    for (int64_t j = blo + threadIdx.x; j < bhi; j += NT) {
-      const long long ar = lttb_area_key(ax, ay, c.x, c.y, to_f64(xs, j), to_f64(ys, j));
-      if (ar > best) { best = ar; bi = j; }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const long long oa = __shfl_xor_sync(FULL, best, o);
-      const long long oi = __shfl_xor_sync(FULL, bi, o);
-      if (oa > best || (oa == best && oi < bi)) { best = oa; bi = oi; }
-    }
-    if (lane == 0) { s_area[wid] = best; s_idx[wid] = bi; }
-    __syncthreads();
-    if (wid == 0) {
-      best = lane < NT / 32 ? s_area[lane] : -1LL;
-      bi = lane < NT / 32 ? s_idx[lane] : INT64_MAX;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const long long oa = __shfl_xor_sync(FULL, best, o);
-        const long long oi = __shfl_xor_sync(FULL, bi, o);
-        if (oa > best || (oa == best && oi < bi)) { best = oa; bi = oi; }
-      }
-      if (lane == 0) {
-        const int64_t sel = bi == INT64_MAX ? blo : bi;  // all-NaN bucket keeps bounds[b] (:110)
-        out[b + 1] = map ? map[sel] : sel;
-        s_prev = sel;
-      }
-    }
-    __syncthreads();
-    prev = s_prev;
-    blo = bhi;
-  }
-  if (threadIdx.x == 0) {
-    out[0] = map ? map[0] : 0;
-    out[k3 + 1] = map ? map[m - 1] : m - 1;
-  }
-}
-
 // ---------------------------------------------------------------- K3c ----
 // LTTB over LARGE buckets (e.g. C2: 1998 buckets of 5005 points), bit-exact.
 // area_j = |alpha*(y_j - ay) - (ax - x_j)*beta| is affine in (x_j, y_j), so
@@ -1497,94 +1177,6 @@ __global__ void __launch_bounds__(NT) k_lttb_chain(LttbArgs a) {
 #ifndef K3C_QUAD
 #define K3C_QUAD 8  // points per min/max group in the direction-candidate scan
 #endif
-
-__device__ __forceinline__ double hcross(double ox, double oy, double ax, double ay, double bx, double by) {
-  return (ax - ox) * (by - oy) - (ay - oy) * (bx - ox);
-}
-
-template <typename XT, typename YT, int HMAX>
-__global__ void __launch_bounds__(64) k_lttb_hull(LttbArgs a) {
-  constexpr int LC = 12;  // per-lane, per-side hull capacity (heuristic cap)
-  struct HP { double x, y; long long j; };
-  __shared__ HP s_h[2][2][32 * LC];  // per warp, per side: lane stacks, then the merged hull in place
-  __shared__ int s_n[2][2][32];
-  const int64_t s = blockIdx.y;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t k3 = a.n_out - 2;
-  const int64_t b = (int64_t)blockIdx.x * 2 + wid;
-  if (b >= k3) return;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const XT* xs = (const XT*)a.x + s * a.x_ld;
-  const YT* ys = (const YT*)a.y + s * a.y_ld;
-  const int64_t blo = lbound(a, m, b), bhi = lbound(a, m, b + 1);
-  const int64_t seg = (bhi - blo + 31) / 32;
-  const int64_t j0 = blo + lane * seg, j1 = min(bhi, j0 + seg);
-  HP* U = &s_h[wid][0][lane * LC];
-  HP* Lw = &s_h[wid][1][lane * LC];
-  int nu = 0, nl = 0;
-  // per-lane monotone chain over a contiguous segment (x non-decreasing),
-  // points prefetched 8 at a time
-  for (int64_t t = j0; t < j1; t += 8) {
-    double px[8], py[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int64_t j = t + q < j1 ? t + q : j1 - 1;
-      px[q] = to_f64(xs, j);
-      py[q] = to_f64(ys, j);
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (t + q >= j1) break;
-      const HP p = {px[q], py[q], (long long)(t + q)};
-      while (nu >= 2 && hcross(U[nu - 2].x, U[nu - 2].y, U[nu - 1].x, U[nu - 1].y, p.x, p.y) >= 0.0) --nu;
-      if (nu == LC) --nu;  // cap: keep the newest point
-      U[nu++] = p;
-      while (nl >= 2 && hcross(Lw[nl - 2].x, Lw[nl - 2].y, Lw[nl - 1].x, Lw[nl - 1].y, p.x, p.y) <= 0.0) --nl;
-      if (nl == LC) --nl;
-      Lw[nl++] = p;
-    }
-  }
-  s_n[wid][0][lane] = nu;
-  s_n[wid][1][lane] = nl;
-  __syncwarp();
-  // lanes 0 and 1: hull of the lane hulls (upper / lower), built in place
-  // (the write cursor never passes the read cursor)
-  if (lane < 2) {
-    const int side = lane;
-    HP* H = s_h[wid][side];
-    int n = 0;
-    for (int l = 0; l < 32; ++l) {
-      const int cnt = s_n[wid][side][l];
-      for (int q = 0; q < cnt; ++q) {
-        const HP p = H[l * LC + q];
-        if (side == 0) {
-          while (n >= 2 && hcross(H[n - 2].x, H[n - 2].y, H[n - 1].x, H[n - 1].y, p.x, p.y) >= 0.0) --n;
-        } else {
-          while (n >= 2 && hcross(H[n - 2].x, H[n - 2].y, H[n - 1].x, H[n - 1].y, p.x, p.y) <= 0.0) --n;
-        }
-        H[n++] = p;
-      }
-    }
-    s_n[wid][side][0] = n;
-  }
-  __syncwarp();
-  if (lane != 0) return;
-  // sorted union of the two hulls, dedup, capped (keep ascending prefix)
-  const HP* Hu = s_h[wid][0];
-  const HP* Hl = s_h[wid][1];
-  const int fu = s_n[wid][0][0], fl = s_n[wid][1][0];
-  int64_t* cand = a.cand + s * a.cand_ld + b * HMAX;
-  const int cap = a.cand_cap > 0 && a.cand_cap < HMAX ? a.cand_cap : HMAX;
-  int iu = 0, il = 0, c = 0;
-  long long last = -1;
-  while ((iu < fu || il < fl) && c < cap) {
-    long long v;
-    if (il >= fl || (iu < fu && Hu[iu].j <= Hl[il].j)) v = Hu[iu++].j;
-    else v = Hl[il++].j;
-    if (v != last) { cand[c++] = v; last = v; }
-  }
-  a.cand_cnt[s * k3 + b] = c;
-}
 
 // Direction-sampled candidates (default K3c heuristic; cheaper than hulls).
 // Over anchors a in bucket b-1's bounding box and the fixed mean c_b+1, the
@@ -2570,162 +2162,6 @@ __global__ void __launch_bounds__(256, K3C_FLAT_MINB) k_lttb_means_flat(LttbArgs
   }
 }
 
-// Flat direction-sampled candidates (k_lttb_dircand's heuristic): per warp
-// segment the D directions' argmax/argmin, merged by the last-arriving warp,
-// which sorts, dedups and writes the bucket's candidate list.  Points enter
-// as float32 offsets from (x_lo, c_y), converted without the XU pipe.
-template <int D> struct CPart { float v[2 * D]; int i[2 * D]; };
-
-template <typename XT, typename YT, int HMAX, int D, int UN>
-__global__ void __launch_bounds__(256, K3C_FLAT_MINB - 1) k_lttb_dircand_flat(LttbArgs a, FlatArgs fl) {
-  static_assert(2 * D <= HMAX && 2 * D <= 32, "candidates must fit");
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int64_t s = blockIdx.y;
-  const int64_t k3 = a.n_out - 2, m = a.n;
-  const int64_t e0 = 1 + gw * fl.E, e1 = min(m - 1, e0 + fl.E);
-  if (gw >= fl.W || e0 >= e1) return;
-  const XT* xs = (const XT*)a.x + s * a.x_ld;
-  const YT* ys = (const YT*)a.y + s * a.y_ld;
-  CPart<D>* part = (CPart<D>*)fl.part + s * k3 * fl.CP;
-  int64_t b = lttb_bucket_of(e0, m, k3);
-  for (int64_t j = e0; j < e1; ++b) {
-    const int64_t blo = lbound(a, m, b), bhi = lbound(a, m, b + 1);
-    const int64_t s1 = min(e1, bhi);
-    const double2 c = a.means[s * a.means_ld + b];
-    double ax0, ax1, ay0, ay1;  // anchor box of bucket b-1 (or the fixed first point)
-    if (b == 0) {
-      ax0 = ax1 = to_f64(xs, 0);
-      ay0 = ay1 = to_f64(ys, 0);
-    } else {
-      const double2 rx = a.xrange[s * k3 + b - 1], ry = a.yrange[s * k3 + b - 1];
-      ax0 = rx.x; ax1 = rx.y; ay0 = ry.x; ay1 = ry.y;
-    }
-    float th_lo = 1e30f, th_hi = -1e30f;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double dxv = c.y - ((q & 1) ? ay1 : ay0);
-      const double dyv = ((q & 2) ? ax1 : ax0) - c.x;
-      float th = atan2f((float)dyv, (float)dxv);
-      if (th > 3.0f) th -= 6.2831853f;  // keep the (x <= c.x) half-plane contiguous
-      th_lo = fminf(th_lo, th);
-      th_hi = fmaxf(th_hi, th);
-    }
-    float cs[D], sn[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const float th = D > 1 ? th_lo + (th_hi - th_lo) * (float)k / (float)(D - 1) : th_lo;
-      sincosf(th, &sn[k], &cs[k]);
-    }
-    const double xrd = to_f64(xs, blo);
-    const double yr = c.y;
-    const float yrf = (float)yr;
-    const bool aff = a.xaff && a.xaff[s * k3 + b].ok;
-    const float fxf = aff ? (float)(XForm<XT>::integral ? (double)a.xaff[s * k3 + b].di : a.xaff[s * k3 + b].d) : 0.f;
-    const int n = (int)(s1 - j), ob = (int)(j - blo);  // segment [j, s1), offsets from the bucket start
-    const XT* xb = xs + j;
-    const YT* yb = ys + j;
-    float vmax[D], vmin[D];
-    int imax[D], imin[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) { vmax[k] = -INFINITY; vmin[k] = INFINITY; imax[k] = INT_MAX; imin[k] = INT_MAX; }
-    float of = (float)(ob + lane);  // running offset (exact below 2^24)
-    for (int i = lane; i < n; i += 32 * UN, of += (float)(32 * UN)) {
-      XT rx[UN];
-      YT ry[UN];
-      const bool full = i + 32 * (UN - 1) < n;
-#pragma unroll
-      for (int q = 0; q < UN; ++q) {
-        const int ii = full || i + 32 * q < n ? i + 32 * q : i;
-        if (!aff) rx[q] = xb[ii];
-        ry[q] = yb[ii];
-      }
-#pragma unroll
-      for (int q = 0; q < UN; ++q) {
-        if (full || i + 32 * q < n) {
-          const int o = ob + i + 32 * q;
-          const float X = aff ? (of + (float)(32 * q)) * fxf : d2f_trunc(__dsub_rn(elem_f64(rx[q]), xrd));
-          float Y;
-          if constexpr (sizeof(YT) == 4) Y = __fsub_rn((float)ry[q], yrf);
-          else Y = d2f_trunc(__dsub_rn((double)ry[q], yr));
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            const float v = fmaf(cs[k], X, sn[k] * Y);
-            if (v > vmax[k]) { vmax[k] = v; imax[k] = o; }
-            if (v < vmin[k]) { vmin[k] = v; imin[k] = o; }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const float ov = __shfl_xor_sync(FULL, vmax[k], off);
-        const int oi = __shfl_xor_sync(FULL, imax[k], off);
-        if (ov > vmax[k] || (ov == vmax[k] && oi < imax[k])) { vmax[k] = ov; imax[k] = oi; }
-        const float ow = __shfl_xor_sync(FULL, vmin[k], off);
-        const int oj = __shfl_xor_sync(FULL, imin[k], off);
-        if (ow < vmin[k] || (ow == vmin[k] && oj < imin[k])) { vmin[k] = ow; imin[k] = oj; }
-      }
-    }
-    const int64_t w0 = (blo - 1) / fl.E;
-    const unsigned ns = (unsigned)((bhi - 2) / fl.E - w0 + 1);
-    CPart<D>* mine = part + b * fl.CP + (gw - w0);
-    if (lane < 2 * D) {  // lane 2k: max of direction k; lane 2k+1: min (stored negated: both as "max")
-      float v = 0.f;
-      int ix = 0;
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        if (lane == 2 * k) { v = vmax[k]; ix = imax[k]; }
-        if (lane == 2 * k + 1) { v = -vmin[k]; ix = imin[k]; }
-      }
-      mine->v[lane] = v;
-      mine->i[lane] = ix;
-      __threadfence();
-    }
-    __syncwarp();
-    bool last = false;
-    if (lane == 0) last = flat_arrive(fl.cnt + s * k3 + b, ns);
-    if (__shfl_sync(FULL, (int)last, 0)) {
-      int ci = INT_MAX;
-      if (lane < 2 * D) {
-        float bv = -INFINITY;
-        for (unsigned q = 0; q < ns; ++q) {
-          const CPart<D>* pp = part + b * fl.CP + q;
-          const float v = __ldcg(&pp->v[lane]);
-          const int i = __ldcg(&pp->i[lane]);
-          if (v > bv || (v == bv && i < ci)) { bv = v; ci = i; }
-        }
-      }
-      // sort the <= 32 candidate offsets across the warp (bitonic), then dedup
-#pragma unroll
-      for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-          const int o = __shfl_xor_sync(FULL, ci, jj);
-          const bool up = ((lane & k) == 0);
-          const bool lower = (lane & jj) == 0;
-          ci = (lower == up) ? min(ci, o) : max(ci, o);
-        }
-      }
-      const int prv = __shfl_up_sync(FULL, ci, 1);
-      const bool keep = ci != INT_MAX && (lane == 0 || prv != ci);
-      const unsigned km = __ballot_sync(FULL, keep);
-      const int rank = __popc(km & ((1u << lane) - 1));
-      const int cap = a.cand_cap > 0 && a.cand_cap < HMAX ? a.cand_cap : HMAX;
-      int64_t* cand = a.cand + s * a.cand_ld + b * HMAX;
-      if (keep && rank < cap) cand[rank] = blo + ci;
-      if (lane == 0) {
-        const int w = min(__popc(km), cap);
-        if (w == 0) cand[0] = blo;
-        a.cand_cnt[s * k3 + b] = w ? w : 1;
-      }
-    }
-    j = s1;
-  }
-}
-
 template <typename XT, typename YT, int NT>
 __global__ void __launch_bounds__(NT) k_lttb_verify(LttbArgs a) {
   __shared__ double s_a[NT / 32];
@@ -2766,51 +2202,6 @@ __global__ void __launch_bounds__(NT) k_lttb_verify2(LttbArgs a) {
     const int64_t prev = a.best[s * k3 + b - 1];
     const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
     if (threadIdx.x == 0) a.best2[s * k3 + b] = r;
-  }
-}
-
-// Flat path: the certification fix-up and verify2 in one launch.  Phase 1
-// handles the buckets whose flat certification failed (k_lttb_verify_fix),
-// a grid barrier (all CTAs are co-resident: one wave of <= 148) makes their
-// best / flag / flist entries visible, phase 2 is k_lttb_verify2.
-template <typename XT, typename YT, int NT>
-__global__ void __launch_bounds__(NT) k_lttb_fix_verify2(LttbArgs a, FlatArgs fl, unsigned* bar) {
-  __shared__ double s_a[NT / 32];
-  __shared__ long long s_i[NT / 32];
-  const int64_t s = 0;  // flat path: one series
-  const int64_t k3 = a.n_out - 2;
-  const int64_t m = a.n;
-  const XT* xs = (const XT*)a.x;
-  const YT* ys = (const YT*)a.y;
-  const int64_t* pos = a.pos;
-  const int nu = *(volatile int*)fl.ucount;
-  for (int q = blockIdx.x; q < nu; q += gridDim.x) {
-    const int64_t b = fl.ulist[q];
-    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, pos[b], s_a, s_i);
-    if (threadIdx.x == 0) {
-      a.best[b] = r;
-      const bool fg = r != pos[b + 1];
-      a.flag[b] = fg;
-      if (fg) a.flist[atomicAdd(&a.fcount[0], 1)] = (int)b;
-    }
-  }
-  if (nu > 0) {  // uniform: without failed certifications phase 1 wrote nothing
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(bar, 1u);
-      while (*(volatile unsigned*)bar < gridDim.x) __nanosleep(64);
-      __threadfence();
-    }
-    __syncthreads();
-  }
-  const int nf = *(volatile int*)&a.fcount[0];
-  for (int q = blockIdx.x; q < nf; q += gridDim.x) {  // one flagged bucket f per CTA: bucket f+1
-    const int64_t b = (int64_t)*(volatile int*)&a.flist[q] + 1;
-    if (b >= k3) continue;
-    const int64_t prev = *(volatile long long*)&a.best[b - 1];
-    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
-    if (threadIdx.x == 0) a.best2[b] = r;
   }
 }
 
@@ -3079,59 +2470,69 @@ template <typename T> struct V4 {  // 4 consecutive elements from 16-byte loads
   }
 };
 
+// Batched: series s (blockIdx.y, grid-strided past 65,535) checks x + s*x_ld
+// (x_ld 0: shared x) and y + s*y_ld into flags[s].
 template <typename XT, typename YT>
-__global__ void __launch_bounds__(256) k_validate(const XT* __restrict__ x, const YT* __restrict__ y, int64_t n,
-                                                 int* flags) {
+__global__ void __launch_bounds__(256) k_validate(const XT* __restrict__ x0, const YT* __restrict__ y0, int64_t n,
+                                                 int64_t x_ld, int64_t y_ld, int64_t B, int* flags) {
   // thread t checks elements [4t, 4t+4) per round (16-byte loads; the host
-  // guarantees 16-byte aligned x and y), plus the pair (4t+3, 4t+4)
-  int f = 0;
+  // guarantees 16-byte aligned rows of x and y), plus the pair (4t+3, 4t+4)
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c * 4 < n; c += T) {
-    const int64_t i0 = c * 4;
-    XT xv[5];
-    YT yv[4];
-    if (i0 + 4 <= n) {
-      V4<XT> a;
-      V4<YT> b;
-      a.load(x + i0);
-      b.load(y + i0);
+  for (int64_t s = blockIdx.y; s < B; s += gridDim.y) {
+    const XT* x = x0 + s * x_ld;
+    const YT* y = y0 + s * y_ld;
+    int f = 0;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c * 4 < n; c += T) {
+      const int64_t i0 = c * 4;
+      XT xv[5];
+      YT yv[4];
+      if (i0 + 4 <= n) {
+        V4<XT> a;
+        V4<YT> b;
+        a.load(x + i0);
+        b.load(y + i0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { xv[q] = a.v[q]; yv[q] = b.v[q]; }
-      xv[4] = i0 + 4 < n ? x[i0 + 4] : xv[3];
-    } else {
+        for (int q = 0; q < 4; ++q) { xv[q] = a.v[q]; yv[q] = b.v[q]; }
+        xv[4] = i0 + 4 < n ? x[i0 + 4] : xv[3];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t i = i0 + q < n ? i0 + q : n - 1;
+          xv[q] = x[i];
+          yv[q] = y[i];
+        }
+        xv[4] = xv[3];
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int64_t i = i0 + q < n ? i0 + q : n - 1;
-        xv[q] = x[i];
-        yv[q] = y[i];
-      }
-      xv[4] = xv[3];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (i0 + q < n) {
-        if (v_nonfinite(xv[q]) || v_nonfinite(yv[q])) f |= 1;  // core.py:89-90
-        const XT nx = i0 + q + 1 < n ? xv[q + 1] : xv[q];
-        if (v_order(nx) < v_order(xv[q])) f |= 2;               // core.py:91-92
+        if (i0 + q < n) {
+          if (v_nonfinite(xv[q]) || v_nonfinite(yv[q])) f |= 1;  // core.py:89-90
+          const XT nx = i0 + q + 1 < n ? xv[q + 1] : xv[q];
+          if (v_order(nx) < v_order(xv[q])) f |= 2;               // core.py:91-92
+        }
       }
     }
+    f = __reduce_or_sync(FULL, f);
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(flags + s, f);
   }
-  f = __reduce_or_sync(FULL, f);
-  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
 }
 
 // unaligned inputs (views): one element per thread per round
 template <typename XT, typename YT>
-__global__ void __launch_bounds__(256) k_validate_scalar(const XT* __restrict__ x, const YT* __restrict__ y,
-                                                        int64_t n, int* flags) {
-  int f = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const XT xv = x[i];
-    if (v_nonfinite(xv) || v_nonfinite(y[i])) f |= 1;
-    if (i + 1 < n && v_order(x[i + 1]) < v_order(xv)) f |= 2;
+__global__ void __launch_bounds__(256) k_validate_scalar(const XT* __restrict__ x0, const YT* __restrict__ y0,
+                                                        int64_t n, int64_t x_ld, int64_t y_ld, int64_t B, int* flags) {
+  for (int64_t s = blockIdx.y; s < B; s += gridDim.y) {
+    const XT* x = x0 + s * x_ld;
+    const YT* y = y0 + s * y_ld;
+    int f = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const XT xv = x[i];
+      if (v_nonfinite(xv) || v_nonfinite(y[i])) f |= 1;
+      if (i + 1 < n && v_order(x[i + 1]) < v_order(xv)) f |= 2;
+    }
+    f = __reduce_or_sync(FULL, f);
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(flags + s, f);
   }
-  f = __reduce_or_sync(FULL, f);
-  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
 }
 
 // TSB1 ingest (seriesio.py:75-95): interleaved little-endian f64 (x, y)

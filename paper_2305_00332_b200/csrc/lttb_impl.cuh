@@ -18,52 +18,17 @@ inline int64_t flat_un(bool verify) {
   static const int64_t uv = env_i64("MMLTTB_K3C_VERIFY_UN", 8), um = env_i64("MMLTTB_K3C_MEANS_UN", 4);
   return verify ? uv : um;
 }
-// A/B knob MMLTTB_K3C_FIXV2=1: certification fix-up and verify2 in one launch with a grid
-// barrier (measured on C2: 176.0 vs 175.3 us for the two launches, so the barrier-free pair
-// stays the default)
-inline bool fixv2_on() {
-  static const bool on = env_i64("MMLTTB_K3C_FIXV2", 0) != 0;
-  return on;
-}
-inline bool use_hull() {
-  static const bool h = env_i64("MMLTTB_K3C_HULL", 0) != 0;  // A/B knob: hull candidates
-  return h;
-}
-inline bool use_chain() {
-  static const bool c = env_i64("MMLTTB_LTTB_CHAIN", 0) != 0;  // A/B knob: old sequential chain
-  return c;
-}
-
-
-// chain resolution over transition maps of width W: the one-CTA scan (default), or
-// the segmented two-kernel version (A/B knob MMLTTB_LTTB_SEGSCAN=1, k3 <= 64 segments;
-// measured: C3 r=4 96.9 vs 92.7 us, r=32 114.2 vs 116.7, C2 189.3 vs 187.2 -- the
-// second launch costs what the parallel walk saves)
+// chain resolution over transition maps of width W: one CTA per series scans
+// the composed maps (a segmented two-kernel version measured no faster)
 template <int W>
 int launch_chain_scan(LttbArgs a, cudaStream_t st) {
-  const int64_t k3 = a.n_out - 2;
-  static const bool seg_on = env_i64("MMLTTB_LTTB_SEGSCAN", 0) != 0;
-  const int64_t S = cdiv(k3, LTTB_SEG);
-  if (seg_on && S <= 64) {
-    const dim3 g((unsigned)S, (unsigned)a.B);
-    k_lttb_seg_paths<W><<<g, 32, 0, st>>>(a);
-    int rc = check_launch("k_lttb_seg_paths");
-    if (rc) return rc;
-    k_lttb_seg_emit<W><<<g, 64, 0, st>>>(a);
-    return check_launch("k_lttb_seg_emit");
-  }
   k_lttb_scan<W, 512, 4><<<(unsigned)a.B, 512, 0, st>>>(a);
   return check_launch("k_lttb_scan");
 }
 
 template <int SMAX> int jump_attr() {
-  static bool done = false;
-  if (!done) {
-    if (cudaFuncSetAttribute(k_lttb_jump<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JUMP_SMEM_MAX) != cudaSuccess)
-      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_lttb_jump)");
-    done = true;
-  }
-  return MM_OK;
+  static std::atomic<unsigned long long> attr{0};
+  return smem_optin(attr, (const void*)k_lttb_jump<SMAX>, (int)JUMP_SMEM_MAX, "k_lttb_jump");
 }
 
 template <int SMAX>
@@ -122,8 +87,7 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   a.cand_cap = (int)env_i64("MMLTTB_K3C_CAND_CAP", H);  // test knob: a poor heuristic must still be exact
   // flat passes (one series with closed-form buckets; A/B knob MMLTTB_K3C_FLAT=0: per-bucket CTAs)
   static const bool flat_on = env_i64("MMLTTB_K3C_FLAT", 1) != 0;
-  static const int64_t mv = env_i64("MMLTTB_K3C_MEANS", 0);
-  const bool flat = flat_on && mv == 0 && a.B == 1 && !a.bounds && !a.m_dev;
+  const bool flat = flat_on && a.B == 1 && !a.bounds && !a.m_dev;
   a.xrange = cv.take<double2>(a.B * k3);
   FlatArgs fl{}, fl_c{};  // fl_c: the candidate pass (16 resident warps per SM instead of 24)
   unsigned* fcnt = nullptr;
@@ -149,17 +113,11 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
       return fail(MM_ECUDA, "memset");
   }
   const unsigned flat_grid = (unsigned)cdiv(fl.W, 8);
-  // default: any-order means + error bounds (one bandwidth-bound pass; the
-  // exact argmaxes certify against the bounds).  A/B knob MMLTTB_K3C_MEANS:
-  // 1 / 2 = the exact in-order chains (one warp per bucket, one / two tiles ahead)
+  // any-order means + error bounds (one bandwidth-bound pass; the exact
+  // argmaxes certify against the bounds)
   static const int cforce = (int)env_i64("MMLTTB_K3C_CERT_FORCE", 0);  // test knob: every certification fails
   a.cert_force = cforce;
-  if (mv == 1 || mv == 2) {
-    a.merr = nullptr;
-    a.xaff = nullptr;
-    if (mv == 1) k_lttb_means_staged<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
-    else k_lttb_means_staged2<XT, YT, 256><<<(unsigned)(a.B * (k3 + 1)), 32, 0, st>>>(a);
-  } else if (flat) {
+  if (flat) {
     fl.cnt = fcnt;
     if (flat_un(false) == 8) k_lttb_means_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
     else k_lttb_means_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
@@ -171,18 +129,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   }
   int rc = check_launch("k_lttb_means");
   if (rc) return rc;
-  if (use_hull()) {
-    k_lttb_hull<XT, YT, H><<<dim3((unsigned)cdiv(k3, 2), (unsigned)a.B), 64, 0, st>>>(a);
-    if ((rc = check_launch("k_lttb_hull"))) return rc;
-  } else {
-    static const int64_t dnt = env_i64("MMLTTB_K3C_DIRCAND_NT", 64);  // A/B knob (64: 64 vs 68 us at 128 on C2)
-    static const bool dflat = env_i64("MMLTTB_K3C_DIRCAND_FLAT", 0) != 0;  // A/B knob: flat candidate pass
-    if (flat && dflat) {
-      fl_c.cnt = fcnt + k3;
-      static_assert(sizeof(CPart<H / 2>) <= K3C_FLAT_PART, "flat partial buffer");
-      k_lttb_dircand_flat<XT, YT, H, H / 2, 4><<<dim3((unsigned)cdiv(fl_c.W, 8), 1), 256, 0, st>>>(a, fl_c);
-    } else if (dnt == 128) k_lttb_dircand<XT, YT, H, H / 2, 128><<<dim3((unsigned)k3, (unsigned)a.B), 128, 0, st>>>(a);
-    else k_lttb_dircand<XT, YT, H, H / 2, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
+  {
+    k_lttb_dircand<XT, YT, H, H / 2, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_dircand"))) return rc;
   }
   k_lttb_ctables<XT, YT, H><<<dim3((unsigned)cdiv(k3, 1024 / H), (unsigned)a.B), 1024, 0, st>>>(a);
@@ -196,24 +144,15 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
     if (flat_un(true) == 4) k_lttb_verify_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
     else k_lttb_verify_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
     if ((rc = check_launch("k_lttb_verify_flat"))) return rc;
-    // certification fix-up + verify2 in one launch (grid barrier; A/B knob MMLTTB_K3C_FIXV2=0: two)
-    if (fixv2_on()) {
-      // one CTA per SM: every CTA co-resident, as the grid barrier needs
-      k_lttb_fix_verify2<XT, YT, 256><<<(unsigned)sm_count(), 256, 0, st>>>(a, fl, fcnt + 3 * k3 + 2);
-      if ((rc = check_launch("k_lttb_fix_verify2"))) return rc;
-    } else {
-      k_lttb_verify_fix<XT, YT, 256><<<dim3(148, 1), 256, 0, st>>>(a, fl);
-      if ((rc = check_launch("k_lttb_verify_fix"))) return rc;
-    }
+    k_lttb_verify_fix<XT, YT, 256><<<dim3((unsigned)sm_count(), 1), 256, 0, st>>>(a, fl);
+    if ((rc = check_launch("k_lttb_verify_fix"))) return rc;
   } else {
     if (vnt == 256) k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
     else k_lttb_verify<XT, YT, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_verify"))) return rc;
   }
-  static const int64_t v2 = env_i64("MMLTTB_K3C_VERIFY2_NT", 256);  // A/B knob
-  if (!(flat && fixv2_on())) {
-    if (v2 == 128) k_lttb_verify2<XT, YT, 128><<<dim3(148, (unsigned)a.B), 128, 0, st>>>(a);
-    else k_lttb_verify2<XT, YT, 256><<<dim3(148, (unsigned)a.B), 256, 0, st>>>(a);
+  {
+    k_lttb_verify2<XT, YT, 256><<<dim3((unsigned)sm_count(), (unsigned)a.B), 256, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_verify2"))) return rc;
   }
   static const int64_t rp = env_i64("MMLTTB_K3C_REPAIR_NT", 512);  // A/B knob (512: 22.1 vs 24.4 us at 1024 on C2)
@@ -223,12 +162,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   const int64_t rbytes = repair_smem_bytes(k3);
   if (rsm && rbytes <= RSMEM_MAX) {
     auto kern = k_lttb_repair_smem<XT, YT, 512>;
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RSMEM_MAX) != cudaSuccess)
-        return fail(MM_ECUDA, "cudaFuncSetAttribute(k_lttb_repair_smem)");
-      attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if ((rc = smem_optin(attr, (const void*)kern, (int)RSMEM_MAX, "k_lttb_repair_smem"))) return rc;
     kern<<<(unsigned)a.B, 512, (size_t)rbytes, st>>>(a);
     return check_launch("k_lttb_repair_smem");
   }
@@ -239,7 +174,6 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
 
 template <typename XT, typename YT>
 int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
-  const int64_t k3 = a.n_out - 2;
   if (a.B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
   if (use_tables(s)) {
     switch (smax_for(s)) {
@@ -250,19 +184,7 @@ int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
       default: return launch_tables_jump<XT, YT, 64>(a, st);
     }
   }
-  if (!use_chain()) {
-    static const int64_t h = env_i64("MMLTTB_K3C_HMAX", 16);  // A/B knob: 16 or 32 candidates
-    if (h == 8) return launch_lttb_large<XT, YT, 8>(a, st);  // 4 directions
-    return h == 32 ? launch_lttb_large<XT, YT, 32>(a, st) : launch_lttb_large<XT, YT, 16>(a, st);
-  }
-  a.means = reinterpret_cast<double2*>(a.tables);
-  a.means_ld = k3;
-  const int64_t n = a.B * k3;
-  k_lttb_means<XT, YT><<<(unsigned)cdiv(n, 128), 128, 0, st>>>(a);
-  int rc = check_launch("k_lttb_means");
-  if (rc) return rc;
-  k_lttb_chain<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
-  return check_launch("k_lttb_chain");
+  return launch_lttb_large<XT, YT, 16>(a, st);
 }
 
 template <typename XT>

@@ -10,7 +10,6 @@ namespace mmh {
 int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s) {
   const int64_t k3 = n_out - 2;
   if (use_tables(s)) return up(B * tab_ld(k3, smax_for(s)));
-  if (use_chain()) return up(B * k3 * (int64_t)sizeof(double2));
   return up(B * k3 * (int64_t)sizeof(double2)) + up(B * k3 * HMAX * 8) + up(B * k3 * 4) + up(B * tab_ld(k3, HMAX)) +
          up(B * (k3 + 2) * 8) + up(B * k3 * 8) + up(B * k3 * 4) + up(B * k3 * (int64_t)sizeof(double2)) +
          up(B * k3 * 8) + up(B * k3 * 4) + up(B * 4) + up(B * k3 * (int64_t)sizeof(double2)) +

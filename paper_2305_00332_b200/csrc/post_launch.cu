@@ -1,4 +1,4 @@
-// post_launch.cu -- single-CTA K2+K3 (k_post_smem / k_post_fused) and cooperative K2+K3a launch.
+// post_launch.cu -- single-CTA K2+K3 (k_post_smem / k_post_fused).
 #include "host.cuh"
 
 namespace mmh {
@@ -21,23 +21,15 @@ int launch_post_t(const PostArgs& pa, int64_t B, cudaStream_t st) {
   static const bool global_staging = env_i64("MMLTTB_POST_GLOBAL", 0) != 0;  // A/B knob
   const int64_t sm2 = post_smem2(pa.n_out - 2, SMAX, pa.cap);
   if (!global_staging && sm2 <= POST_SMEM2_MAX) {  // preselected set staged in shared memory
-    static bool attr2 = false;
-    if (!attr2) {
-      if (cudaFuncSetAttribute(k_post_smem<XT, YT, SMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)POST_SMEM2_MAX) != cudaSuccess)
-        return fail(MM_ECUDA, "cudaFuncSetAttribute(k_post_smem)");
-      attr2 = true;
-    }
+    static std::atomic<unsigned long long> attr2{0};
+    if (int rc = smem_optin(attr2, (const void*)k_post_smem<XT, YT, SMAX, 1024>, (int)POST_SMEM2_MAX, "k_post_smem"))
+      return rc;
     k_post_smem<XT, YT, SMAX, 1024><<<(unsigned)B, 1024, (size_t)sm2, st>>>(pa);
     return check_launch("k_post_smem");
   }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_post_fused<XT, YT, SMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)POST_SMEM_MAX) != cudaSuccess)
-      return fail(MM_ECUDA, "cudaFuncSetAttribute(k_post_fused)");
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (int rc = smem_optin(attr, (const void*)k_post_fused<XT, YT, SMAX, 1024>, (int)POST_SMEM_MAX, "k_post_fused"))
+    return rc;
   k_post_fused<XT, YT, SMAX, 1024><<<(unsigned)B, 1024, (size_t)post_smem(pa.n_out - 2, SMAX), st>>>(pa);
   return check_launch("k_post_fused");
 }
@@ -57,62 +49,5 @@ int launch_post(const PostArgs& pa, int64_t B, int xdt, int ydt, int smax, cudaS
     default: return y32 ? launch_post_y<int, float>(pa, B, smax, st) : launch_post_y<int, double>(pa, B, smax, st);
   }
 }
-
-// ---- cooperative K2+K3a ----------------------------------------------------
-template <typename XT, typename YT, int SMAX>
-int launch_coop_t(PairArgs pa, LttbArgs la, int64_t B, cudaStream_t st, bool* launched) {
-  constexpr int NT = PAIR_NT, IT = PAIR_ITEMS;
-  auto fn = k_post_coop<XT, YT, SMAX, NT, IT>;
-  static int cap = -1;
-  if (cap < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, NT, 0);
-    cap = sms * per;
-  }
-  int64_t ntiles = std::max<int64_t>(1, cdiv(pa.nb, NT * IT));
-  if (ntiles * B > cap || B > 65535) { *launched = false; return MM_OK; }
-  *launched = true;
-  la.tab_ld = tab_ld(la.n_out - 2, SMAX);
-  void* args[] = {(void*)&pa, (void*)&la, (void*)&ntiles};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)ntiles, (unsigned)B), dim3(NT),
-                                                    args, 0, st);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (e != cudaSuccess) return fail(MM_ECUDA, "k_post_coop: %s", cudaGetErrorString(e));
-  return MM_OK;
-}
-
-template <typename XT, typename YT>
-int launch_coop_y(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched) {
-  return smax <= 4 ? launch_coop_t<XT, YT, 4>(pa, la, B, st, launched)
-                   : launch_coop_t<XT, YT, 8>(pa, la, B, st, launched);
-}
-
-// Try the cooperative K2+K3a; *launched = false when it does not apply.
-int launch_coop(PairArgs pa, LttbArgs la, int64_t B, int smax, cudaStream_t st, bool* launched) {
-  // opt-in (MMLTTB_COOP=1): measured neutral-to-slower than the separate
-  // launches on B200 (c3_1e9 28 vs 26 us, c3 1e8 27 vs 24 us) -- the fixed
-  // cost is the phases' dependent memory round trips, not the launches
-  static const bool on = env_i64("MMLTTB_COOP", 0) != 0;
-  *launched = false;
-  if (!on || smax <= 0 || smax > 8) return MM_OK;
-  const bool y32 = pa.ydt == MM_F32;
-  switch (pa.xdt) {
-    case MM_F32:
-      return y32 ? launch_coop_y<float, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<float, double>(pa, la, B, smax, st, launched);
-    case MM_F64:
-      return y32 ? launch_coop_y<double, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<double, double>(pa, la, B, smax, st, launched);
-    case MM_I64:
-      return y32 ? launch_coop_y<long long, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<long long, double>(pa, la, B, smax, st, launched);
-    default:
-      return y32 ? launch_coop_y<int, float>(pa, la, B, smax, st, launched)
-                 : launch_coop_y<int, double>(pa, la, B, smax, st, launched);
-  }
-}
-
 
 }  // namespace mmh

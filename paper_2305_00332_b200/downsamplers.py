@@ -103,24 +103,26 @@ class Batch:
         return self
 
     def _full_validate(self):
-        """TimeSeries invariants (core.py:80-94) on device, per row: one sync."""
+        """TimeSeries invariants (core.py:80-94) for every row: one batched launch, one sync.
+
+        The rows are B series built in order, so the first failing row decides,
+        and within it non-finite values are reported before a decreasing x."""
         if self.x is None:
             return
         xs = self.x if self.x.is_cuda else self.x.to(self.device)
-        flags = torch.zeros(self.B, dtype=torch.int32, device=self.device)  # one word per row: one sync in all
+        flags = torch.empty(self.B, dtype=torch.int32, device=self.device)
         with torch.cuda.device(self.device):
-            st = N.stream_ptr(self.device)
-            for i in range(self.B):
-                xi = xs if xs.dim() == 1 else xs[i]
-                N.check(N.lib().mmlttb_validate(xi.data_ptr(), N.DTYPE_CODE[xi.dtype], self.y[i].data_ptr(),
-                                                N.DTYPE_CODE[self.y.dtype], self.n, flags[i:].data_ptr(), st),
-                        "validate", self.n)
-        bad = torch.stack([(flags & 1).any(), (flags & 2).any()]).tolist()
-        acc = (1 if bad[0] else 0) | (2 if bad[1] else 0)
-        if acc & 1:
+            N.check(N.lib().mmlttb_validate_batch(xs.data_ptr(), N.DTYPE_CODE[xs.dtype], self.n if xs.dim() == 2 else 0,
+                                                  self.y.data_ptr(), N.DTYPE_CODE[self.y.dtype], self.n, self.B, self.n,
+                                                  flags.data_ptr(), N.stream_ptr(self.device)), "validate", self.n)
+        fl = flags.cpu().numpy()
+        bad = np.flatnonzero(fl)
+        if bad.shape[0] == 0:
+            return
+        f = int(fl[bad[0]])
+        if f & 1:
             raise NonFiniteValue("series contains NaN or infinite values")
-        if acc & 2:
-            raise NonMonotonicX("xs must be sorted in non-decreasing order")
+        raise NonMonotonicX("xs must be sorted in non-decreasing order")
 
     def post_check(self, ws: torch.Tensor) -> None:
         """Raise the reference's NonFiniteValue from the kernels' status word."""
@@ -173,6 +175,19 @@ def _is_flat(first) -> bool:
     return not isinstance(first, TimeSeries)
 
 
+def _int_arg(v, what: str) -> int:
+    """Strict integer argument: a bool or an array in an integer slot means the
+    reference form and the flat form were mixed up -- raise, never rebind."""
+    if isinstance(v, (bool, np.bool_)) or not isinstance(v, (int, np.integer)):
+        raise TypeError(f"{what} must be an integer, got {type(v).__name__}")
+    return int(v)
+
+
+def _no_extra(fn: str, args) -> None:
+    if args:
+        raise TypeError(f"{fn}() got {len(args)} unexpected positional argument(s)")
+
+
 # ------------------------------------------------------------- checks -------
 def _check_n_out(n: int, n_out: int) -> int:
     if not 3 <= n_out <= n:  # downsamplers.py:37-41
@@ -204,11 +219,13 @@ def _counted(b, out, cnt):
 # ------------------------------------------------------------ algorithms ----
 def every_nth(series, n_out, *args):
     """Select floor(i * N / n_out), i in [0, n_out) (downsamplers.py:44-47)."""
-    if _is_flat(series):
-        b = Batch(series, n_out, None)  # every_nth(x, y, n_out)
-        n_out = args[0]
+    if _is_flat(series):  # every_nth(x, y, n_out)
+        if len(args) != 1:
+            raise TypeError("flat form: every_nth(x, y, n_out)")
+        b, n_out = Batch(series, n_out, None), _int_arg(args[0], "n_out")
     else:
-        b = _Series(series)
+        _no_extra("every_nth", args)
+        b, n_out = _Series(series), _int_arg(n_out, "n_out")
     _check_n_out(b.n, n_out)
     b.ready()
     out = torch.empty((1, n_out), dtype=torch.int64, device=b.device)
@@ -249,9 +266,11 @@ def minmax(series, n_out, parallel=False, *args, **kw):
     Flat form: ``minmax(x, y, n_out)``.
     """
     if _is_flat(series):
-        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), parallel
+        _no_extra("minmax", args)
+        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), _int_arg(parallel, "n_out")
     else:
-        b = _Series(series)
+        _no_extra("minmax", args)
+        b, n_out = _Series(series), _int_arg(n_out, "n_out")
     _check_n_out(b.n, n_out)
     if n_out % 2:
         raise OddNOut(f"minmax needs an even n_out, got {n_out}")
@@ -259,11 +278,15 @@ def minmax(series, n_out, parallel=False, *args, **kw):
 
 
 def m4(series, n_out, parallel=False, *args, **kw):
-    """First, min, max and last sample per bucket (downsamplers.py:95-112)."""
+    """First, min, max and last sample per bucket (downsamplers.py:95-112).
+
+    Flat form: ``m4(x, y, n_out)``.
+    """
+    _no_extra("m4", args)
     if _is_flat(series):
-        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), parallel
+        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), _int_arg(parallel, "n_out")
     else:
-        b = _Series(series)
+        b, n_out = _Series(series), _int_arg(n_out, "n_out")
     _check_n_out(b.n, n_out)
     if n_out % 4:
         raise NOutNotDivisibleBy4(f"m4 needs n_out divisible by 4, got {n_out}")
@@ -276,9 +299,12 @@ def lttb(series, n_out, *args, **kw):
     Flat form: ``lttb(x, y, n_out)``.
     """
     if _is_flat(series):
-        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), args[0]
+        if len(args) != 1:
+            raise TypeError("flat form: lttb(x, y, n_out)")
+        b, n_out = Batch(series, n_out, kw.get("device"), kw.get("validate")), _int_arg(args[0], "n_out")
     else:
-        b = _Series(series)
+        _no_extra("lttb", args)
+        b, n_out = _Series(series), _int_arg(n_out, "n_out")
     _check_n_out(b.n, n_out)
     b.ready()
     xdt, ydt = _codes(b)
@@ -300,10 +326,12 @@ def minmax_preselect(series, n_out, r_ps, parallel=False, *args, **kw):
 
     Flat form: ``minmax_preselect(x, y, n_out, r_ps)``.
     """
+    _no_extra("minmax_preselect", args)
     if _is_flat(series):
-        b, n_out, r_ps = Batch(series, n_out, kw.get("device"), kw.get("validate")), r_ps, parallel
+        b = Batch(series, n_out, kw.get("device"), kw.get("validate"))
+        n_out, r_ps = _int_arg(r_ps, "n_out"), _int_arg(parallel, "r_ps")
     else:
-        b = _Series(series)
+        b, n_out, r_ps = _Series(series), _int_arg(n_out, "n_out"), _int_arg(r_ps, "r_ps")
     k = _check_preselect(b.n, n_out, r_ps)
     b.ready()
     _, ydt = _codes(b)
@@ -342,15 +370,20 @@ def minmaxlttb(series, n_out, r_ps=4, parallel=False, *args, minmax_ratio=None, 
     Flat form (north star): ``minmaxlttb(x, y, n_out, minmax_ratio=4)`` with
     ``y`` of shape [N] or [B, N]; returns [n_out] or [B, n_out].
     """
-    if _is_flat(series):
+    _no_extra("minmaxlttb", args)
+    if _is_flat(series):  # minmaxlttb(x, y, n_out[, minmax_ratio])
         x, y = series, n_out
-        n_out = r_ps
-        ratio = minmax_ratio if minmax_ratio is not None else (parallel if not isinstance(parallel, bool) else 4)
+        n_out = _int_arg(r_ps, "n_out")
+        if minmax_ratio is not None and parallel is not False:
+            raise TypeError("minmax_ratio given both positionally and by keyword")
+        r_ps = _int_arg(minmax_ratio if minmax_ratio is not None else (4 if parallel is False else parallel),
+                        "minmax_ratio")
         b = Batch(x, y, device, validate)
-        r_ps = int(ratio)
     else:
+        n_out = _int_arg(n_out, "n_out")
         if minmax_ratio is not None:
             r_ps = minmax_ratio
+        r_ps = _int_arg(r_ps, "r_ps")
         b = _Series(series, device)
     if r_ps == 1:
         _check_n_out(b.n, n_out)

@@ -47,13 +47,14 @@ def _read_header(fh, path):
 def read_series(path, fmt: str = "auto", device=None) -> TimeSeries:
     """Load a series file; ``fmt`` is 'csv', 'bin' or 'auto' (seriesio.py:30-38).
 
-    With ``device`` (or for 'bin' when a GPU is present) the TSB1 payload goes
-    straight to HBM and a device-backed TimeSeries is returned.
+    With ``device`` the TSB1 payload goes straight to HBM (pinned chunked H2D +
+    device de-interleave) and a device-backed TimeSeries is returned; without it
+    every format gives a host series, as the reference does.
     """
     if fmt == "auto":
         fmt = detect_format(path)
     if fmt == "bin":
-        if device is None and not torch.cuda.is_available():
+        if device is None:
             return _read_bin_host(path)
         return _read_bin_device(path, device)
     if fmt == "csv":
@@ -83,6 +84,9 @@ def _read_bin_device(path, device=None) -> TimeSeries:
         copy_stream = torch.cuda.Stream(dev)
         done = 0
         i = 0
+        # x, y and the staging buffers come from the current stream's pool: the
+        # copy stream must not write them before that stream's pending work ends
+        copy_stream.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.device(dev):
             while done < count:
                 n = min(chunk, count - done)

@@ -27,7 +27,8 @@ import torch
 import torch.distributed as dist
 
 from . import _native as N
-from .downsamplers import Batch, _check_n_out, _check_preselect, _minmaxlttb_batch
+from .downsamplers import Batch, _check_n_out, _check_preselect, _minmax_like, _minmaxlttb_batch
+from .errors import OddNOut
 
 
 # ------------------------------------------------------------ batch path ----
@@ -40,21 +41,60 @@ def minmaxlttb_batch_sharded(x, y_local, n_out: int, r_ps: int = 4, *, B: int | 
                              gather: bool = False, group=None):
     """MinMaxLTTB over this rank's rows of a batch (no collective on the data path).
 
-    ``y_local``: this rank's [b, N] rows (see :func:`batch_range`).  With
-    ``gather=True`` the [B, n_out] result is all-gathered to every rank.
+    ``y_local``: this rank's [b, N] rows (see :func:`batch_range`).  The
+    reference's checks run first, in its order (downsamplers.py:182-209 with
+    :37-41, :146-153; r_ps == 1 diverts to MinMax with endpoints, :164-179).
+    With ``gather=True`` the [B, n_out] result is all-gathered to every rank;
+    ``B`` (the global series count) is then required, since rows may be split
+    unevenly.  r_ps == 1 rows can be shorter than n_out: they come back (and
+    are gathered) as a list of per-series index tensors.
     """
-    out = _minmaxlttb_batch(_prepared(x, y_local), n_out, r_ps)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if gather and world > 1 and B is None:
+        raise ValueError("gather=True needs the global series count B")
+    b = _prepared(x, y_local)
+    if r_ps == 1:
+        _check_n_out(b.n, n_out)
+        if n_out % 2:
+            raise OddNOut(f"minmax needs an even n_out, got {n_out}")
+        rows = _minmax_like(b, n_out, "minmax", force=True)
+        rows = rows if isinstance(rows, list) else [rows]
+        if not gather or world == 1:
+            return rows
+        got = [None] * world
+        dist.all_gather_object(got, [r.cpu() for r in rows], group=group)
+        dev = b.device
+        return [r.to(dev) for part in got for r in part]
+    _check_preselect(b.n, n_out, r_ps)
+    out = _minmaxlttb_batch(b, n_out, r_ps)
     if not gather or world == 1:
         return out
-    B = B if B is not None else out.shape[0] * world
+    rank = dist.get_rank(group)
+    lo, hi = batch_range(B, rank, world)
+    if out.shape[0] != hi - lo:
+        raise ValueError(f"rank {rank} must hold rows [{lo}, {hi}) of the {B}-series batch, got {out.shape[0]}")
     per = -(-B // world)
     buf = torch.full((per, n_out), -1, dtype=torch.int64, device=out.device)
     buf[: out.shape[0]] = out
-    allb = torch.empty((world * per, n_out), dtype=torch.int64, device=out.device)
-    dist.all_gather_into_tensor(allb, buf, group=group)
+    allb = all_gather_flat(buf.reshape(-1), world, group).view(world * per, n_out)
     rows = [allb[r * per: r * per + (batch_range(B, r, world)[1] - batch_range(B, r, world)[0])] for r in range(world)]
     return torch.cat(rows, 0)
+
+
+def all_gather_flat(buf: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """[world * buf.numel()] concatenation of every rank's `buf`, on buf's device.
+
+    NCCL gathers in place over NVLink; any other backend (gloo: the CPU test
+    groups, or several ranks sharing one GPU) is staged through host memory."""
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        allbuf = torch.empty(world * buf.numel(), dtype=buf.dtype, device=buf.device)
+        dist.all_gather_into_tensor(allbuf, buf, group=group)
+        return allbuf
+    host = buf.detach().cpu()
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    return torch.cat(parts).to(buf.device)
 
 
 def _prepared(x, y):
@@ -132,9 +172,7 @@ def unpack(allbuf: torch.Tensor, world: int, cap: int):
 
 def exchange(buf: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """The one collective of the path: all_gather of the packed shard sets."""
-    allbuf = torch.empty(world * buf.numel(), dtype=buf.dtype, device=buf.device)
-    dist.all_gather_into_tensor(allbuf, buf, group=group)
-    return allbuf
+    return all_gather_flat(buf, world, group)
 
 
 class PeerExchange:

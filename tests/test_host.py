@@ -109,7 +109,9 @@ def test_timeseries_invariants():
         mm.TimeSeries(np.zeros((2, 2)), np.zeros((2, 2)))
     ts = mm.TimeSeries([0, 1, 1, 2], [1, 2, 3, 4])  # non-decreasing x is fine
     assert len(ts) == 4 and ts.ys.dtype == np.float64  # ints -> float64 like core.py:49
-    assert mm.TimeSeries(np.arange(3), np.ones(3, np.float32)).ys.dtype == np.float32
+    t32 = mm.TimeSeries(np.arange(3), np.ones(3, np.float32))
+    assert t32.y_data.dtype == np.float32 and t32.ys.dtype == np.float64  # stored f32, exposed f64 (core.py:48-53)
+    assert not t32.xs.flags.writeable and not t32.ys.flags.writeable
     with pytest.raises(AttributeError):
         ts.foo = 1
     big = np.array([2**53 + 1, 2**53], dtype=np.int64)  # equal once converted to f64
@@ -173,3 +175,45 @@ def test_no_cpu_fallback():
         mm.minmaxlttb(ts, 6, 2)
     with pytest.raises(errors.CudaError):
         mm.lttb(np.arange(20), np.arange(20.0), 6)
+
+
+def test_timeseries_owns_its_arrays():
+    """the caller's arrays stay writable and later writes do not reach the series."""
+    x = np.arange(5, dtype=np.int64)
+    y = np.linspace(0.0, 1.0, 5)
+    ts = mm.TimeSeries(x, y)
+    assert x.flags.writeable and y.flags.writeable
+    x[0] = 100  # would make x non-monotonic if it were shared
+    y[1] = -7.0
+    assert ts.xs[0] == 0.0 and ts.ys[1] == 0.25
+    assert ts.xs.dtype == np.float64 and ts.ys.dtype == np.float64
+    with pytest.raises(ValueError):
+        ts.ys[0] = 1.0  # read-only like the reference's frozen arrays
+    base = np.arange(10, dtype=np.float64)
+    ts2 = mm.TimeSeries(base[::2], base[1::2])
+    base[:] = -1.0
+    assert ts2.xs[0] == 0.0 and ts2.ys[0] == 1.0
+
+
+def test_flat_and_reference_forms_never_rebind():
+    """Mixing the flat form (x, y, n_out, minmax_ratio) with the reference form
+    (series, n_out, r_ps, parallel) raises TypeError instead of misbinding."""
+    x = np.arange(100, dtype=np.int64)
+    y = np.zeros(100)
+    with pytest.raises(TypeError):
+        mm.minmaxlttb(x, y, 10, True)  # a bool in the ratio slot
+    with pytest.raises(TypeError):
+        mm.minmaxlttb(x, y, 10, 4, minmax_ratio=4)  # ratio twice
+    with pytest.raises(TypeError):
+        mm.minmax(x, y)  # flat minmax without n_out
+    with pytest.raises(TypeError):
+        mm.minmax(x, y, 10, True)
+    with pytest.raises(TypeError):
+        mm.lttb(x, y)
+    with pytest.raises(TypeError):
+        mm.minmax_preselect(x, y, 10)  # flat preselect without r_ps
+    ts = mm.TimeSeries(x, y)
+    with pytest.raises(TypeError):
+        mm.minmaxlttb(ts, y, 10)  # an array in the n_out slot
+    with pytest.raises(TypeError):
+        mm.lttb(ts, 10, 4)

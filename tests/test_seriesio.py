@@ -61,8 +61,9 @@ def test_device_ingest(tmp_path):
         ts = mm.read_series(tmp_path / "s.bin", device="cuda:0")
     finally:
         seriesio._CHUNK_PAIRS = old
-    assert not ts.is_host and ts.xs.is_cuda
-    assert np.array_equal(ts.xs.cpu().numpy(), x) and np.array_equal(ts.ys.cpu().numpy(), y)
+    assert not ts.is_host and ts.x_data.is_cuda
+    assert np.array_equal(ts.x_data.cpu().numpy(), x) and np.array_equal(ts.y_data.cpu().numpy(), y)
+    assert np.array_equal(ts.xs, x) and ts.ys.dtype == np.float64  # reference surface: host float64
     from oracle import oracle as O
 
     out = mm.minmaxlttb(ts, 1000, 4)
