@@ -30,6 +30,7 @@ int check_launch(const char* what);
 void stage_mark(cudaStream_t st, int i);
 
 constexpr int64_t ALIGN = 256;
+constexpr int MM_ENOTSUP = -100;  // internal: a fast path declines, the caller falls back (never returned by the C ABI)
 inline int64_t up(int64_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int esize(int dt) { return (dt == MM_F32 || dt == MM_I32) ? 4 : 8; }

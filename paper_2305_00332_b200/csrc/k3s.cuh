@@ -1,0 +1,1074 @@
+// k3s.cuh -- K3s: exact full LTTB of ONE series with many large buckets
+// (BASELINE C2: 1,998 buckets of ~5,005 points) in a SINGLE persistent launch.
+//
+// Same algorithm and exactness argument as K3c (kernels.cuh: direction
+// candidates -> candidate transition tables -> chain -> exact verification
+// -> repair), re-organised as one cooperative kernel (one CTA per SM, all
+// co-resident).  CTA c owns the contiguous buckets [B0, B1); inside a phase a
+// WARP owns a whole bucket, so every reduction is a warp reduction amortised
+// over ~150 points per lane and no phase needs more than one pass:
+//
+//   1 stats   per bucket: any-order sums with rigorous error bounds, x / y
+//             ranges, the affine-x test ("certified means") --
+//             the only pass that reads HBM (x and y once)            | grid sync
+//   2 cand    per bucket: argmax / argmin of Y + lambda*T for D slopes sampled
+//             over the anchor box (bucket b-1's ranges) and the mean c_b;
+//             points in octets, winners resolved by 16 lanes in parallel | grid sync
+//   3 chain   transition tables T_b over the candidate sets (exact areas),
+//             CTA aggregate A_c = T_{B1-1} o ... o T_{B0} (16-byte maps), the
+//             chain entering CTA c = (A_{c-1} o ... o A_0)(0), then positions
+//   4 verify  every bucket re-scanned with the reference's formula, tie rule
+//             and (certified) mean given the chain's previous pick; a
+//             mismatching bucket's successor gets its exact pick given the
+//             exact anchor (verify2)
+//   5 repair  the last CTA to finish walks the mismatches (repair_walk_smem)
+//             and writes the n_out indices.
+//
+// The candidate heuristic never affects the result: every bucket is verified
+// exactly and every deviation repaired (_kernels.py:81-119 semantics).
+#pragma once
+#include "kernels.cuh"
+#include <type_traits>
+
+namespace mm {
+
+constexpr int K3S_NT = 512;          // 16 warps per CTA
+constexpr int K3S_NW = K3S_NT / 32;
+constexpr int K3S_D = 8;             // sampled slopes -> <= 16 candidates per bucket
+constexpr int K3S_H = 2 * K3S_D;     // candidate slots per bucket (== the K3c table width)
+constexpr int K3S_U = 8;             // loads in flight per lane per array
+constexpr int K3S_GMAX = 1024;       // CTA bound for the workspace
+
+struct K3sArgs {
+  int G;                 // CTAs, all co-resident (cooperative launch)
+  int maxb;              // >= buckets per CTA
+  unsigned* sync;        // K3S_SYNC_WORDS counters / flags (zeroed per call); fcount at K3S_FCOUNT
+  unsigned char* agg;    // [G][16] aggregate maps
+  double2* cpt;          // [k3][16] candidate points (x, y)
+  unsigned long long* prof;  // optional [G][8] %globaltimer stamps per phase (tools), or null
+};
+// sync words: barrier i = counter at 64 i, release flag at 64 i + 32 (separate
+// 128-byte lines: the pollers never delay the arrivals); done counter, fcount
+constexpr int K3S_DONE = 64 * 4, K3S_FCOUNT = 64 * 4 + 32, K3S_CONFLICT = 64 * 5, K3S_SYNC_WORDS = 64 * 6;
+
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// bounded spin: a protocol bug traps (the launch fails) instead of hanging the GPU
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+__device__ __forceinline__ void spin_until_set(const unsigned* p, unsigned want) {
+  const unsigned long long t0 = gtimer();
+  while (ld_acq(p) < want) {
+    __nanosleep(100);
+    if (gtimer() - t0 > 2000000000ull) __trap();  // 2 s
+  }
+}
+// grid-wide barrier i over the G co-resident CTAs: the last arriver releases
+// a flag the others poll (counter and flag on different lines)
+__device__ __forceinline__ void k3s_grid_sync(unsigned* sync, int i, unsigned G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(sync + 64 * i, 1u) == G - 1) {
+      __threadfence();
+      st_rel(sync + 64 * i + 32, 1u);
+    } else {
+      spin_until_set(sync + 64 * i + 32, 1u);
+    }
+  }
+  __syncthreads();
+}
+
+// float -> int32 key with the same order (IEEE total order)
+__device__ __forceinline__ int fkey(float f) {
+  const int b = __float_as_int(f);
+  return b ^ ((b >> 31) & 0x7fffffff);
+}
+
+// sum_{i<n} (x0 + i d) in 128-bit integer arithmetic, rounded once to f64
+// (exact whenever the result is below 2^53)
+__device__ __forceinline__ double k3s_affine_sum(long long x0, long long d, long long n) {
+  const long long tt = n * (n - 1) / 2;
+  const unsigned long long lo1 = (unsigned long long)x0 * (unsigned long long)n;
+  const long long hi1 = __mul64hi(x0, n);
+  const unsigned long long lo2 = (unsigned long long)d * (unsigned long long)tt;
+  const long long hi2 = __mul64hi(d, tt);
+  const unsigned long long lo = lo1 + lo2;
+  const long long hi = hi1 + hi2 + (lo < lo1 ? 1 : 0);
+  if (hi == ((long long)lo >> 63)) return (double)(long long)lo;  // fits int64: one rounding
+  return __dadd_rn(__dmul_rn((double)hi, 18446744073709551616.0), (double)lo);
+}
+
+__device__ __forceinline__ double warp_dsum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+// ---- 16-byte vector windows --------------------------------------------
+// Bucket [lo, hi) of a 16-byte-aligned array of T: full vectors [vf, vl) are
+// loaded as uint4 (EV elements each, lane-strided: coalesced 512 B per warp
+// load), the < EV head elements [lo, vf*EV) and tail elements [vl*EV, hi)
+// individually.
+template <typename T> struct Vec {
+  static constexpr int EV = 16 / (int)sizeof(T);
+  __device__ __forceinline__ static T get(const uint4& v, int e) {
+    if constexpr (sizeof(T) == 8) {
+      const unsigned long long b = e == 0 ? ((unsigned long long)v.y << 32 | v.x) : ((unsigned long long)v.w << 32 | v.z);
+      if constexpr (std::is_same<T, double>::value) return __longlong_as_double((long long)b);
+      else return (T)(long long)b;
+    } else {
+      const unsigned b = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+      if constexpr (std::is_same<T, float>::value) return __uint_as_float(b);
+      else return (T)(int)b;
+    }
+  }
+};
+struct VWin {
+  int64_t vf, vl;  // full vectors
+  int nh, nt;      // head / tail element counts
+  int64_t tl;      // first tail element
+};
+template <typename T>
+__device__ __forceinline__ VWin vwin(int64_t lo, int64_t hi) {
+  constexpr int EV = Vec<T>::EV;
+  VWin w;
+  w.vf = (lo + EV - 1) / EV;
+  w.vl = hi / EV;
+  if (w.vl < w.vf) w.vl = w.vf;
+  w.nh = (int)(min(hi, w.vf * EV) - lo);
+  w.tl = max(lo, w.vl * EV);
+  w.nt = (int)(hi - w.tl);
+  if (w.vf * EV >= hi) w.nt = 0;  // no full vector: the head covers everything
+  return w;
+}
+// element index handled by `lane` in the head / tail step (or -1)
+__device__ __forceinline__ int64_t vwin_edge(const VWin& w, int64_t lo, int lane) {
+  if (lane < w.nh) return lo + lane;
+  if (lane >= 16 && lane - 16 < w.nt) return w.tl + (lane - 16);
+  return -1;
+}
+
+// Lane-strided rounds over a window's full vectors: body(r, v0, cnt, g) gets
+// this lane's UV vectors of round g (r[u] = vector v0 + 32u) of which the
+// first cnt are in range (cnt == UV in every round but the last, which the
+// compiler specialises; out-of-range slots repeat vector v0).
+template <int UV, bool STREAM, bool PREFETCH, typename F>
+__device__ __forceinline__ void vrounds(const uint4* base, const VWin& w, int L, int NL, F&& body) {
+  const int64_t nfull = (w.vl - w.vf) / ((int64_t)NL * UV);
+  int64_t v0 = w.vf + L;
+  const uint4* p = base + v0;
+  const int step = NL * UV;
+  auto ld = [&](uint4 (&r)[UV], const uint4* q) {
+#pragma unroll
+    for (int u = 0; u < UV; ++u) r[u] = STREAM ? __ldcs(q + NL * u) : q[NL * u];  // immediate offsets
+  };
+  int g = 0;
+  if constexpr (!PREFETCH) {
+    for (; g < nfull; ++g, v0 += step, p += step) {
+      uint4 r[UV];
+      ld(r, p);
+      body(r, v0, UV, g);
+    }
+  } else {
+    // software-pipelined: round g+1's loads are in flight while round g is processed
+    uint4 ra[UV], rb[UV];
+    if (nfull > 0) ld(ra, p);
+    for (; g + 1 < nfull; g += 2) {
+      ld(rb, p + step);
+      body(ra, v0, UV, g);
+      if (g + 2 < nfull) ld(ra, p + 2 * step);
+      body(rb, v0 + step, UV, g + 1);
+      v0 += 2 * step;
+      p += 2 * step;
+    }
+    if (g < nfull) {
+      body(ra, v0, UV, g);
+      ++g;
+      v0 += step;
+      p += step;
+    }
+  }
+  if (v0 < w.vl) {
+    const int cnt = (int)((w.vl - v0 + NL - 1) / NL);
+    uint4 r[UV];
+#pragma unroll
+    for (int u = 0; u < UV; ++u) r[u] = STREAM ? __ldcs(p + (u < cnt ? NL * u : 0)) : p[u < cnt ? NL * u : 0];
+    body(r, v0, cnt, g);
+  }
+}
+
+// ---------------------------------------------------------------- phase 1 --
+// One warp: statistics of bucket b = [lo, hi), published for every later phase.
+template <typename XT, typename YT>
+__device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const YT* ys, int64_t b, int64_t lo,
+                                          int64_t hi, int64_t m) {
+  constexpr int EY = Vec<YT>::EV, EX = Vec<XT>::EV;
+  constexpr int UY = 16 / EY, UX = 16 / EX;  // 16 elements per lane per round
+  const int lane = threadIdx.x & 31;
+  const int64_t k3 = a.n_out - 2;
+  const int n = (int)(hi - lo);
+  const double nb = (double)n;
+  XAff f;
+  {
+    const XT x0r = xs[lo], x1r = n > 1 ? xs[lo + 1] : xs[lo];
+    f.x0 = (double)x0r;
+    f.d = __dsub_rn((double)x1r, (double)x0r);
+    f.x0i = (long long)x0r;
+    f.di = (long long)((unsigned long long)(long long)x1r - (unsigned long long)(long long)x0r);
+    f.pad = 0;
+  }
+  const double yfirst = (double)ys[lo];
+  const bool try_y = yfirst == 0.0 || (double)lsb_exp(yfirst) + 55.0 > (double)exp_of(yfirst) + log2(nb);
+  const double xfirst = (double)xs[lo];
+  const bool try_x = !XForm<XT>::integral && (xfirst == 0.0 || (double)lsb_exp(xfirst) + 55.0 > (double)exp_of(xfirst) + log2(nb));
+  // ---- y: any-order sum, range keys (f32: exact; f64: high words, conservative), lowest set bit
+  double sy = 0.0;
+  int kmn = INT_MAX, kmx = INT_MIN, ly = 4096;
+  auto ykey = [&](YT y) -> int {
+    if constexpr (sizeof(YT) == 4) return fkey((float)y);
+    else {
+      const int hy = (int)(__double_as_longlong((double)y) >> 32);
+      return hy ^ ((hy >> 31) & 0x7fffffff);
+    }
+  };
+  auto yel = [&](YT y) {
+    sy = __dadd_rn(sy, (double)y);
+    const int k = ykey(y);
+    kmn = min(kmn, k);
+    kmx = max(kmx, k);
+  };
+  {
+    const VWin w = vwin<YT>(lo, hi);
+    const int64_t e = vwin_edge(w, lo, lane);
+    if (e >= 0) {
+      yel(ys[e]);
+      if (try_y) ly = min(ly, lsb_exp((double)ys[e]));
+    }
+    auto body = [&](const uint4 (&r)[UY], int64_t, int cnt, int) {
+#pragma unroll
+      for (int u = 0; u < UY; ++u)
+        if (u < cnt) {
+#pragma unroll
+          for (int q = 0; q < EY; ++q) yel(Vec<YT>::get(r[u], q));
+        }
+    };
+    auto body_lsb = [&](const uint4 (&r)[UY], int64_t, int cnt, int) {
+#pragma unroll
+      for (int u = 0; u < UY; ++u)
+        if (u < cnt) {
+#pragma unroll
+          for (int q = 0; q < EY; ++q) {
+            const YT y = Vec<YT>::get(r[u], q);
+            yel(y);
+            ly = min(ly, lsb_exp((double)y));
+          }
+        }
+    };
+    if (try_y) vrounds<UY, false, false>(reinterpret_cast<const uint4*>(ys), w, lane, 32, body_lsb);
+    else vrounds<UY, false, false>(reinterpret_cast<const uint4*>(ys), w, lane, 32, body);
+  }
+  // ---- x: affine test (integral: XOR-accumulated difference from the formula),
+  // float x: bit compare + sum, keys, lowest bits
+  double sx = 0.0;
+  int lx = XForm<XT>::integral ? 0 : 4096, aff = 1;
+  long long kxm = LLONG_MAX, kxM = LLONG_MIN;
+  unsigned long long dacc = 0;  // integral x: OR of (x ^ formula) over the bucket
+  auto xel = [&](XT x, long long xe) {  // xe: integral: the formula's value here; float: the offset j - lo
+    if constexpr (XForm<XT>::integral) {
+      dacc |= (unsigned long long)((long long)x ^ xe);
+    } else {
+      const double vx = (double)x;
+      aff &= __double_as_longlong(vx) == __double_as_longlong(XForm<XT>::at(f, xe));
+      sx = __dadd_rn(sx, vx);
+      const long long kk = dkey(vx);
+      kxm = min(kxm, kk);
+      kxM = max(kxM, kk);
+      if (try_x) lx = min(lx, lsb_exp(vx));
+    }
+  };
+  auto xexp = [&](int64_t j) -> long long {
+    if constexpr (XForm<XT>::integral) return (long long)((unsigned long long)f.x0i + (unsigned long long)(j - lo) * (unsigned long long)f.di);
+    else return (long long)(j - lo);
+  };
+  const long long xstep = XForm<XT>::integral ? f.di : 1;
+  {
+    const VWin w = vwin<XT>(lo, hi);
+    const int64_t e = vwin_edge(w, lo, lane);
+    if (e >= 0) xel(xs[e], xexp(e));
+    const long long vstep = (long long)((unsigned long long)xstep * (unsigned long long)(32 * EX));
+    vrounds<UX, true, false>(reinterpret_cast<const uint4*>(xs), w, lane, 32, [&](const uint4 (&r)[UX], int64_t v0, int cnt, int) {
+      long long xe = xexp(v0 * EX);
+#pragma unroll
+      for (int u = 0; u < UX; ++u) {
+        if (u < cnt) {
+#pragma unroll
+          for (int q = 0; q < EX; ++q)
+            xel(Vec<XT>::get(r[u], q), (long long)((unsigned long long)xe + (unsigned long long)(q * xstep)));
+        }
+        xe = (long long)((unsigned long long)xe + (unsigned long long)vstep);
+      }
+    });
+  }
+  if constexpr (XForm<XT>::integral) aff = dacc == 0;
+  aff = __all_sync(FULL, aff);
+  f.ok = aff;
+  sy = warp_dsum(sy);
+  kmn = __reduce_min_sync(FULL, kmn);
+  kmx = __reduce_max_sync(FULL, kmx);
+  ly = __reduce_min_sync(FULL, try_y ? ly : -4096);
+  double x0, x1, Ax;
+  if (XForm<XT>::integral && aff) {  // closed-form sum of the verified arange
+    sx = k3s_affine_sum(f.x0i, f.di, n);
+    const long long xl = (long long)((unsigned long long)f.x0i + (unsigned long long)(n - 1) * (unsigned long long)f.di);
+    x0 = elem_f64((XT)f.x0i);
+    x1 = elem_f64((XT)xl);
+    if (x1 < x0) { const double tt = x0; x0 = x1; x1 = tt; }
+    Ax = __dmul_rn(nb, fmax(fabs(x0), fabs(x1))) * (1.0 + 4.0 * K3C_U);
+    lx = 0;
+  } else {
+    if constexpr (XForm<XT>::integral) {  // (rare) non-affine integer x: second pass
+      for (int64_t j = lo + lane; j < hi; j += 32) {
+        const double vx = elem_f64(xs[j]);
+        sx = __dadd_rn(sx, vx);
+        const long long kk = dkey(vx);
+        kxm = min(kxm, kk);
+        kxM = max(kxM, kk);
+      }
+    }
+    sx = warp_dsum(sx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      kxm = min(kxm, __shfl_xor_sync(FULL, kxm, o));
+      kxM = max(kxM, __shfl_xor_sync(FULL, kxM, o));
+    }
+    lx = __reduce_min_sync(FULL, XForm<XT>::integral ? 0 : (try_x ? lx : -4096));
+    x0 = dkey_inv(kxm);
+    x1 = dkey_inv(kxM);
+    Ax = __dmul_rn(nb, fmax(fabs(x0), fabs(x1))) * (1.0 + 4.0 * K3C_U);
+  }
+  if (lane == 0) {
+    double y0, y1;
+    if constexpr (sizeof(YT) == 4) {
+      y0 = (double)__int_as_float(kmn ^ ((kmn >> 31) & 0x7fffffff));
+      y1 = (double)__int_as_float(kmx ^ ((kmx >> 31) & 0x7fffffff));
+    } else {
+      y0 = dkey_inv((long long)kmn * 4294967296LL);                 // <= every value
+      y1 = dkey_inv((long long)kmx * 4294967296LL + 4294967295LL);  // >= every value
+    }
+    const double Ay = __dmul_rn(nb, fmax(fabs(y0), fabs(y1))) * (1.0 + 4.0 * K3C_U);
+    a.yrange[b] = make_double2(y0, y1);
+    a.xrange[b] = make_double2(x0, x1);
+    if (a.xaff) a.xaff[b] = f;
+    if (b >= 1) {
+      double ex = mean_err_bound(sx, Ax, lx, nb), ey = mean_err_bound(sy, Ay, ly, nb);
+      if (!(Ay <= 1.7e308)) ey = INFINITY;  // non-finite y: never certified (the exact path decides)
+      if (!(Ax <= 1.7e308)) ex = INFINITY;
+      a.means[b - 1] = make_double2(__ddiv_rn(sx, nb), __ddiv_rn(sy, nb));
+      a.merr[b - 1] = make_double2(ex, ey);
+    }
+    if (b == k3 - 1) {  // the last bucket anchors on point m-1 itself (_kernels.py:105-107): exact
+      a.means[k3 - 1] = make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
+      a.merr[k3 - 1] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- phase 2 --
+// One warp: direction candidates of bucket b = [lo, hi).  D slopes lambda over
+// the anchor box (bucket b-1's ranges, or point 0) and the mean c = means[b];
+// per slope the argmax and argmin of Y + lambda*T (T: index offset for affine
+// x, else x - x_lo) -- in f32, a heuristic (phase 4 makes the result exact).
+// A lane's points of a round form one group: per slope the group's max / min
+// (3-input min/max trees) meet the running extremes, which remember the
+// round; afterwards 2D lanes resolve the 2D winning groups to their points in
+// parallel, recomputing the same f32 values.  Affine x: with T = tb + c_p
+// (tb the lane's round base, c_p a compile-time offset), a group's extreme is
+// fmaf(lambda, tb, max_p fmaf(lambda, c_p, Y_p)) -- one FFMA per point and slope.
+template <typename XT, typename YT, bool AFF>
+__device__ __forceinline__ void k3s_cand_t(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
+                                           int64_t lo, int64_t hi, const float (&lam)[K3S_D], double xlo) {
+  constexpr int D = K3S_D, H = K3S_H;
+  constexpr int EV = Vec<YT>::EV, UV = 16 / EV, PR = 16;  // points per lane per round
+  const int lane = threadIdx.x & 31;
+  auto tval = [&](int64_t j) -> float { return AFF ? (float)(j - lo) : (float)(elem_f64(xs[j]) - xlo); };
+  float vmax[D], vmin[D];
+  int gmax[D], gmin[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) { vmax[k] = -INFINITY; vmin[k] = INFINITY; gmax[k] = -1; gmin[k] = -1; }
+  const VWin w = vwin<YT>(lo, hi);
+  const uint4* yv = reinterpret_cast<const uint4*>(ys);
+  int ng = 0;
+  vrounds<UV, false, false>(yv, w, lane, 32, [&](const uint4 (&r)[UV], int64_t v0, int cnt, int g) {
+    ng = g + 1;
+    float Y[PR];
+#pragma unroll
+    for (int u = 0; u < UV; ++u)
+#pragma unroll
+      for (int q = 0; q < EV; ++q) Y[u * EV + q] = (float)Vec<YT>::get(r[u], q);
+    float T[PR];
+    if constexpr (!AFF) {
+#pragma unroll
+      for (int u = 0; u < UV; ++u)
+#pragma unroll
+        for (int q = 0; q < EV; ++q) T[u * EV + q] = tval((u < cnt ? v0 + 32 * u : v0) * EV + q);
+    }
+    const float tb = (float)(v0 * EV - lo);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      float mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+      for (int u = 0; u < UV; ++u) {
+        if (u < cnt) {
+#pragma unroll
+          for (int q = 0; q < EV; ++q) {
+            const float val = AFF ? fmaf(lam[k], (float)(32 * EV * u + q), Y[u * EV + q]) : fmaf(lam[k], T[u * EV + q], Y[u * EV + q]);
+            mx = fmaxf(mx, val);
+            mn = fminf(mn, val);
+          }
+        }
+      }
+      if (AFF) { mx = fmaf(lam[k], tb, mx); mn = fmaf(lam[k], tb, mn); }
+      if (mx > vmax[k]) { vmax[k] = mx; gmax[k] = g; }
+      if (mn < vmin[k]) { vmin[k] = mn; gmin[k] = g; }
+    }
+  });
+  ng = __reduce_max_sync(FULL, ng);  // the head / tail group id (lanes without a partial round saw fewer)
+  const int64_t ej = vwin_edge(w, lo, lane);
+  if (ej >= 0) {  // head / tail elements: group ng
+    const float Yj = (float)ys[ej], Tj = tval(ej);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float val = fmaf(lam[k], Tj, Yj);
+      if (val > vmax[k]) { vmax[k] = val; gmax[k] = ng; }
+      if (val < vmin[k]) { vmin[k] = val; gmin[k] = ng; }
+    }
+  }
+  // winner lane + group of each of the 2D extremes (warp REDUX on order keys)
+  int my_g = -1, my_l = 0, my_key = 0;  // lane e < 2D keeps extreme e's winner
+#pragma unroll
+  for (int e = 0; e < 2 * D; ++e) {
+    const int k = e >> 1;
+    const int key = (e & 1) ? fkey(-vmin[k]) : fkey(vmax[k]);
+    const int wk = __reduce_max_sync(FULL, key);
+    const int wl = __ffs(__ballot_sync(FULL, key == wk)) - 1;
+    const int wg = __shfl_sync(FULL, (e & 1) ? gmin[k] : gmax[k], wl);
+    if (lane == e) { my_g = wg; my_l = wl; my_key = wk; }
+  }
+  // lanes 0..2D-1 resolve their extreme's group to its first point (parallel re-reads)
+  int64_t off = -1;
+  if (lane < 2 * D && my_g >= 0) {
+    const int k = lane >> 1;
+    float lk = lam[0];
+#pragma unroll
+    for (int q = 1; q < D; ++q) lk = k == q ? lam[q] : lk;
+    if (my_g == ng) {
+      off = vwin_edge(w, lo, my_l);
+    } else {
+      const int64_t v0 = w.vf + (int64_t)my_g * 32 * UV + my_l;
+      const int cnt = (int)min((int64_t)UV, (w.vl - v0 + 31) / 32);
+      const float tb = (float)(v0 * EV - lo);
+      uint4 r[UV];
+#pragma unroll
+      for (int u = 0; u < UV; ++u) r[u] = yv[u < cnt ? v0 + 32 * u : v0];
+#pragma unroll
+      for (int u = UV - 1; u >= 0; --u) {
+        if (u < cnt) {
+#pragma unroll
+          for (int q = EV - 1; q >= 0; --q) {
+            const int64_t j = (v0 + 32 * u) * EV + q;
+            const float Yq = (float)Vec<YT>::get(r[u], q);
+            const float val = AFF ? fmaf(lk, tb, fmaf(lk, (float)(32 * EV * u + q), Yq)) : fmaf(lk, tval(j), Yq);
+            const int kk = (lane & 1) ? fkey(-val) : fkey(val);
+            if (kk == my_key) off = j;
+          }
+        }
+      }
+    }
+  }
+  int o32 = off < 0 ? INT_MAX : (int)(off - lo);
+  // sort the <= 2D offsets across the warp (bitonic), de-duplicate, cap
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int o = __shfl_xor_sync(FULL, o32, j);
+      const bool up = ((lane & k) == 0);
+      const bool lower = (lane & j) == 0;
+      o32 = (lower == up) ? min(o32, o) : max(o32, o);
+    }
+  }
+  const int prev = __shfl_up_sync(FULL, o32, 1);
+  const bool keep = o32 != INT_MAX && (lane == 0 || prev != o32);
+  const unsigned km = __ballot_sync(FULL, keep);
+  const int rank = __popc(km & ((1u << lane) - 1));
+  const int cap = a.cand_cap > 0 && a.cand_cap < H ? a.cand_cap : H;
+  const int cw = max(1, min(__popc(km), cap));
+  if (keep && rank < cap) {
+    const int64_t p = lo + o32;
+    a.cand[b * H + rank] = p;
+    ka.cpt[b * H + rank] = make_double2(to_f64(xs, p), to_f64(ys, p));
+  }
+  if (lane == 0) {
+    if (km == 0) { a.cand[b * H] = lo; ka.cpt[b * H] = make_double2(to_f64(xs, lo), to_f64(ys, lo)); }
+    a.cand_cnt[b] = cw;
+  }
+}
+
+template <typename XT, typename YT>
+__device__ __forceinline__ void k3s_cand(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
+                                         int64_t lo, int64_t hi) {
+  constexpr int D = K3S_D;
+  double bx0, bx1, by0, by1;
+  if (b == 0) {
+    bx0 = bx1 = to_f64(xs, 0);
+    by0 = by1 = to_f64(ys, 0);
+  } else {
+    const double2 xr = __ldcg(a.xrange + b - 1), yr = __ldcg(a.yrange + b - 1);
+    bx0 = xr.x; bx1 = xr.y; by0 = yr.x; by1 = yr.y;
+  }
+  const double2 c = __ldcg(a.means + b);
+  XAff f;
+  f.ok = 0;
+  if (a.xaff) {
+    const XAff* fp = a.xaff + b;
+    f.d = __ldcg(&fp->d); f.di = __ldcg(&fp->di); f.ok = __ldcg(&fp->ok);
+  }
+  // area ~ P*Y + S*X with P = ax - cx, S = cy - ay over the anchor box corners;
+  // affine x: X = d*T -> extremes of Y + lambda*T with lambda = S*d/P
+  const bool aff = f.ok;
+  const double dsc = aff ? (XForm<XT>::integral ? (double)f.di : f.d) : 1.0;
+  double lmin = INFINITY, lmax = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double ax = (q & 1) ? bx1 : bx0, ay = (q & 2) ? by1 : by0;
+    double l = (c.y - ay) * dsc / (ax - c.x);
+    if (l != l) l = 0.0;
+    l = fmin(fmax(l, -1e20), 1e20);
+    lmin = fmin(lmin, l);
+    lmax = fmax(lmax, l);
+  }
+  float lam[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) lam[k] = (float)(lmin + (lmax - lmin) * ((double)k / (double)(D - 1)));
+  if (aff) k3s_cand_t<XT, YT, true>(a, ka, xs, ys, b, lo, hi, lam, 0.0);
+  else k3s_cand_t<XT, YT, false>(a, ka, xs, ys, b, lo, hi, lam, elem_f64(xs[lo]));
+}
+
+// ---------------------------------------------------------------- phase 3 --
+// One warp: T_b[p] = argmax_q exact area(anchor p, candidate q, c_b), strict
+// '>' in ascending candidate order (lowest index on ties, NaN never wins).
+// Lane l: anchor p = l/2, candidates q in [8(l&1), 8(l&1)+8).
+static __device__ __noinline__ void k3s_table(const LttbArgs& a, const K3sArgs& ka, int64_t b, double x0, double y0,
+                                          unsigned char* tab) {
+  constexpr int H = K3S_H;
+  const int lane = threadIdx.x & 31;
+  const int p = lane >> 1, q0 = (lane & 1) * 8;
+  int na = 1;
+  double ax = x0, ay = y0;
+  if (b > 0) {
+    na = __ldcg(a.cand_cnt + b - 1);
+    if (p < na) {
+      const double2 v = __ldcg(ka.cpt + (b - 1) * H + p);
+      ax = v.x; ay = v.y;
+    }
+  }
+  const int nq = __ldcg(a.cand_cnt + b);
+  const double2 c = __ldcg(a.means + b);
+  double2 pts[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) pts[i] = q0 + i < nq ? __ldcg(ka.cpt + b * H + q0 + i) : make_double2(0.0, 0.0);
+  long long bk = -2;
+  int bq = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (q0 + i < nq) {
+      const long long k = lttb_area_key(ax, ay, c.x, c.y, pts[i].x, pts[i].y);
+      if (k > bk) { bk = k; bq = q0 + i; }
+    }
+  }
+  const long long ok = __shfl_xor_sync(FULL, bk, 1);
+  const int oq = __shfl_xor_sync(FULL, bq, 1);
+  if (ok > bk || (ok == bk && oq < bq)) { bk = ok; bq = oq; }
+  if ((lane & 1) == 0) tab[p] = (unsigned char)(p < na && bk >= -1 ? bq : 0);
+}
+
+// ---------------------------------------------------------------- phase 4 --
+// In-order fp64 mean of bucket b+1 (_kernels.py:98-104) by lanes 0 / 1 of a warp
+// (the rare path of a failed certification), broadcast to the warp.
+template <typename XT, typename YT>
+__device__ __noinline__ double2 warp_exact_mean(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k3 = a.n_out - 2;
+  if (b + 1 >= k3) return make_double2(to_f64(xs, m - 1), to_f64(ys, m - 1));
+  const int64_t nlo = lbound(a, m, b + 1), nhi = lbound(a, m, b + 2);
+  double acc = 0.0;
+  if (lane < 2) {
+    for (int64_t j = nlo; j < nhi; ++j) acc = __dadd_rn(acc, lane == 0 ? to_f64(xs, j) : to_f64(ys, j));
+    acc = __ddiv_rn(acc, (double)(nhi - nlo));
+  }
+  return make_double2(__shfl_sync(FULL, acc, 0), __shfl_sync(FULL, acc, 1));
+}
+
+// One warp: exact |area| keys over bucket [lo, hi) given anchor (ax, ay) and
+// mean c (lttb_area's op order), every point exactly once: top-2 keys and the
+// first index of the top (warp-reduced).
+template <typename XT, typename YT>
+__device__ __forceinline__ void warp_scan_area(const XT* xs, const YT* ys, int64_t lo, int64_t hi, double ax, double ay,
+                                               double2 c, const XAff& f, bool afi, long long& k1, long long& k2,
+                                               long long& i1, int& bad) {
+  constexpr int EV = Vec<YT>::EV, UV = 16 / EV;
+  const int lane = threadIdx.x & 31;
+  const double P = __dsub_rn(ax, c.x), S = __dsub_rn(c.y, ay);
+  k1 = -1; k2 = -1; bad = 0;
+  int64_t il = LLONG_MAX;
+  auto xat = [&](int64_t j) -> double {
+    return f.ok ? (afi ? i2d_magic((long long)((unsigned long long)f.x0i + (unsigned long long)(j - lo) * (unsigned long long)f.di))
+                       : XForm<XT>::at(f, j - lo))
+                : elem_f64(xs[j]);
+  };
+  auto el = [&](double xj, YT y, int64_t j) {
+    const double R = __dsub_rn(ax, xj), Q = __dsub_rn((double)y, ay);
+    const double tt = __dsub_rn(__dmul_rn(P, Q), __dmul_rn(R, S));  // lttb_area, same op order
+    long long k = __double_as_longlong(tt) & 0x7fffffffffffffffLL;
+    bad |= (int)(k >> 32) >= 0x7ff00000;      // inf / NaN: no certification
+    k = k > 0x7ff0000000000000LL ? -1LL : k;  // NaN never wins
+    if (k > k2) {
+      if (k > k1) { k2 = k1; k1 = k; il = j; }
+      else k2 = k;
+    }
+  };
+  const VWin w = vwin<YT>(lo, hi);
+  {
+    const int64_t j = vwin_edge(w, lo, lane);
+    if (j >= 0) el(xat(j), ys[j], j);
+  }
+  const uint4* yv = reinterpret_cast<const uint4*>(ys);
+  // affine integer x: exact integer-valued doubles stepped by exact adds
+  const double dvec = afi ? i2d_magic(f.di * (32 * EV)) : 0.0, d1 = afi ? i2d_magic(f.di) : 0.0;
+  for (int64_t v0 = w.vf + lane; v0 < w.vl; v0 += 32 * UV) {
+    uint4 r[UV];
+#pragma unroll
+    for (int u = 0; u < UV; ++u) r[u] = yv[v0 + 32 * u < w.vl ? v0 + 32 * u : v0];
+    double xv = afi ? xat(v0 * EV) : 0.0;
+#pragma unroll
+    for (int u = 0; u < UV; ++u) {
+      const int64_t v = v0 + 32 * u;
+      if (v < w.vl) {
+        double xq = xv;
+#pragma unroll
+        for (int q = 0; q < EV; ++q) {
+          const int64_t j = v * EV + q;
+          el(afi ? xq : xat(j), Vec<YT>::get(r[u], q), j);
+          if (afi) xq = __dadd_rn(xq, d1);
+        }
+      }
+      if (afi) xv = __dadd_rn(xv, dvec);
+    }
+  }
+  i1 = il;
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+    vpart_merge(k1, i1, k2, bad, __shfl_xor_sync(FULL, k1, o), __shfl_xor_sync(FULL, i1, o),
+                __shfl_xor_sync(FULL, k2, o), __shfl_xor_sync(FULL, bad, o));
+}
+
+// One warp: the reference's pick of bucket b given anchor `prev`, certified
+// against the mean's error bound (k3c_area_err); a failed certification takes
+// the in-order mean and re-scans.  Never writes means/merr (other warps of the
+// launch may be reading them).
+template <typename XT, typename YT>
+__device__ __noinline__ int64_t warp_pick(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b, int64_t prev) {
+  const int64_t lo = lbound(a, m, b), hi = lbound(a, m, b + 1);
+  const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
+  const double2 c = __ldcg(a.means + b);
+  const double2 ce = __ldcg(a.merr + b);
+  const double2 yr = __ldcg(a.yrange + b), xr = __ldcg(a.xrange + b);
+  XAff f;
+  f.ok = 0;
+  if (a.xaff) {
+    const XAff* fp = a.xaff + b;
+    f.x0 = __ldcg(&fp->x0); f.d = __ldcg(&fp->d); f.x0i = __ldcg(&fp->x0i); f.di = __ldcg(&fp->di);
+    f.ok = __ldcg(&fp->ok);
+  }
+  const bool afi = f.ok && XForm<XT>::integral && fmax(fabs(xr.x), fabs(xr.y)) < 1125899906842624.0 &&
+                   fabs((double)f.di) * 128.0 < 1125899906842624.0;
+  long long k1, k2, i1;
+  int bad;
+  warp_scan_area<XT, YT>(xs, ys, lo, hi, ax, ay, c, f, afi, k1, k2, i1, bad);
+  const double u = K3C_U;
+  bool ok = !bad && ((ce.x == 0.0 && ce.y == 0.0) || hi - lo == 1);
+  if (!ok && !bad && !a.cert_force) {
+    const double P = __dsub_rn(ax, c.x), S = __dsub_rn(c.y, ay);
+    // |Q_j| <= (1+u) max|y - ay| over the bucket's y range (likewise R)
+    const double qmax = fmax(fabs(__dsub_rn(yr.y, ay)), fabs(__dsub_rn(yr.x, ay))) * (1.0 + 4.0 * u);
+    const double rmax = fmax(fabs(__dsub_rn(ax, xr.x)), fabs(__dsub_rn(ax, xr.y))) * (1.0 + 4.0 * u);
+    const double v1 = k1 < 0 ? -1.0 : __longlong_as_double(k1), v2 = k2 < 0 ? -1.0 : __longlong_as_double(k2);
+    const double E = k3c_area_err(ce, P, S, qmax, rmax, v1);
+    ok = __dsub_rn(v1, v2) > 2.0 * E * (1.0 + 1e-9);  // NaN bounds fail
+  }
+  if (ok) return i1 == LLONG_MAX ? lo : i1;  // all-NaN bucket keeps bounds[b] (:110)
+  const double2 ce2 = warp_exact_mean<XT, YT>(a, xs, ys, m, b);
+  warp_scan_area<XT, YT>(xs, ys, lo, hi, ax, ay, ce2, f, afi, k1, k2, i1, bad);
+  return i1 == LLONG_MAX ? lo : i1;
+}
+
+// Phase 4's common case, for a group of NWG warps (1: one warp per bucket;
+// K3S_NW: the whole CTA on one bucket, for the few re-scans of 4b and the
+// repair): is r the reference's pick of bucket b given anchor `prev`?  Every
+// point's exact |area| key (lttb_area's op order) is compared with r's key Kr
+// only -- a point before r must stay below Kr, a point after r must not
+// exceed it (lowest index wins ties), one 64-bit compare against a per-vector
+// threshold.  The runner-up needed by the certification is bounded by the
+// second-largest HIGH word of all keys (32-bit top-2), whose first point is
+// also the next guess (*alt) when r is wrong.  Returns false when anything is
+// off (violation, inf / NaN, failed certification).
+struct GrpRed { int v, m1, m2, j1; };
+// tool counters (prof mode): [0] verify calls, [1] violations, [2] shared high word, [3] cert fails,
+// [4] full-path picks, [5] flagged buckets, [6] 4b picks, [7] repair picks
+__device__ unsigned long long* g_k3s_cnt;
+__device__ __forceinline__ void k3s_count(int i) {
+  if (g_k3s_cnt && (threadIdx.x & 31) == 0 && ((threadIdx.x >> 5) == 0 || i < 0)) atomicAdd(g_k3s_cnt + (i < 0 ? -i : i), 1ull);
+}
+__device__ __forceinline__ void top2_merge(int& m1, int& m2, int& j1, int om1, int om2, int oj1) {
+  m2 = max(max(m2, om2), min(m1, om1));
+  j1 = om1 > m1 ? oj1 : (om1 < m1 ? j1 : min(j1, oj1));
+  m1 = max(m1, om1);
+}
+
+template <int NWG, typename XT, typename YT>
+__device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b, int64_t prev,
+                           int64_t r, int64_t* alt, GrpRed* sh) {
+  constexpr int EV = Vec<YT>::EV, UV = 8 / EV, NL = 32 * NWG;
+  const int lane = threadIdx.x & 31, wg = NWG == 1 ? 0 : (int)(threadIdx.x >> 5);
+  const int L = wg * 32 + lane;
+  const int64_t lo = lbound(a, m, b), hi = lbound(a, m, b + 1);
+  if (alt) *alt = -1;
+  if (r < lo || r >= hi) return false;
+  const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
+  const double2 c = __ldcg(a.means + b);
+  const double2 ce = __ldcg(a.merr + b);
+  const double2 yr = __ldcg(a.yrange + b), xr = __ldcg(a.xrange + b);
+  XAff f;
+  f.ok = 0;
+  if (a.xaff) {
+    const XAff* fp = a.xaff + b;
+    f.x0i = __ldcg(&fp->x0i); f.di = __ldcg(&fp->di); f.x0 = __ldcg(&fp->x0); f.d = __ldcg(&fp->d);
+    f.ok = __ldcg(&fp->ok);
+  }
+  // affine integer x, every value (and the anchor's) an integer below 2^50: R_j = ax - x_j is
+  // exact, so it is stepped by exact subtractions instead of recomputed
+  const bool afi = f.ok && XForm<XT>::integral && fmax(fmax(fabs(xr.x), fabs(xr.y)), fabs(ax)) < 1125899906842624.0 &&
+                   fabs((double)f.di) * (4.0 * NL) < 1125899906842624.0;
+  const double P = __dsub_rn(ax, c.x), S = __dsub_rn(c.y, ay);
+  auto xat = [&](int64_t j) -> double {
+    return f.ok ? (afi ? i2d_magic((long long)((unsigned long long)f.x0i + (unsigned long long)(j - lo) * (unsigned long long)f.di))
+                       : XForm<XT>::at(f, j - lo))
+                : elem_f64(xs[j]);
+  };
+  auto keyR = [&](double R, double yj) -> long long {
+    const double tt = __dsub_rn(__dmul_rn(P, __dsub_rn(yj, ay)), __dmul_rn(R, S));  // lttb_area, same op order
+    return __double_as_longlong(tt) & 0x7fffffffffffffffLL;
+  };
+  const long long Kr = keyR(__dsub_rn(ax, xat(r)), to_f64(ys, r));
+  if (Kr >= 0x7ff0000000000000LL) return false;  // inf / NaN pick: the full path decides
+  const int hr = (int)(Kr >> 32);
+  // 32-bit top-2 of the keys' HIGH words (inf / NaN keys have the largest) and the
+  // first point of the top: r is the exact pick iff it holds the top high word alone
+  int m1 = -1, m2 = -1, j1 = INT_MAX;
+  auto el = [&](double R, double yj, int jr) {
+    const int h = (int)(keyR(R, yj) >> 32);
+    const bool up = h > m1;
+    m2 = max(m2, min(m1, h));
+    j1 = up ? jr : j1;
+    m1 = max(m1, h);
+  };
+  const VWin w = vwin<YT>(lo, hi);
+  if (NWG == 1 || wg == 0) {  // head / tail elements
+    const int64_t j = vwin_edge(w, lo, lane);
+    if (j >= 0) el(__dsub_rn(ax, xat(j)), to_f64(ys, j), (int)(j - lo));
+  }
+  auto run = [&](auto afi_tag) {
+    constexpr bool AFI = decltype(afi_tag)::value;
+    const double d1 = AFI ? i2d_magic(f.di) : 0.0;
+    const double dvec = AFI ? i2d_magic(f.di * (NL * EV)) : 0.0;
+    vrounds<UV, false, true>(reinterpret_cast<const uint4*>(ys), w, L, NL, [&](const uint4 (&rr)[UV], int64_t v0, int cnt, int) {
+      const int jb = (int)(v0 * EV - lo);
+      double Rv = AFI ? __dsub_rn(ax, xat(v0 * EV)) : 0.0;
+#pragma unroll
+      for (int u = 0; u < UV; ++u) {
+        if (u < cnt) {
+          double Rq = Rv;
+#pragma unroll
+          for (int q = 0; q < EV; ++q) {
+            const int jr = jb + NL * EV * u + q;
+            if constexpr (AFI) {
+              el(Rq, (double)Vec<YT>::get(rr[u], q), jr);
+              Rq = __dsub_rn(Rq, d1);
+            } else {
+              el(__dsub_rn(ax, xat(lo + jr)), (double)Vec<YT>::get(rr[u], q), jr);
+            }
+          }
+        }
+        if (AFI) Rv = __dsub_rn(Rv, dvec);
+      }
+    });
+  };
+  if (afi) run(std::true_type{});
+  else run(std::false_type{});
+  // group reduction
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+    top2_merge(m1, m2, j1, __shfl_xor_sync(FULL, m1, o), __shfl_xor_sync(FULL, m2, o), __shfl_xor_sync(FULL, j1, o));
+  if constexpr (NWG > 1) {
+    __syncthreads();
+    if (lane == 0) sh[wg] = GrpRed{0, m1, m2, j1};
+    __syncthreads();
+    m1 = -1; m2 = -1; j1 = INT_MAX;
+    for (int q = 0; q < NWG; ++q) {
+      const GrpRed g = sh[q];
+      top2_merge(m1, m2, j1, g.m1, g.m2, g.j1);
+    }
+  }
+  if (NWG == 1) k3s_count(-0); else k3s_count(0);
+  if (m1 > hr) {  // a point beats r: where the exact pick most likely is
+    if (alt && m1 < 0x7ff00000 && j1 != INT_MAX) *alt = lo + j1;
+    if (NWG == 1) k3s_count(-1); else k3s_count(1);
+    return false;
+  }
+  if (m2 >= hr) {  // another point shares r's high word: the full comparison decides
+    if (NWG == 1) k3s_count(-2); else k3s_count(2);
+    return false;
+  }
+  if ((ce.x == 0.0 && ce.y == 0.0) || hi - lo == 1) return true;  // exact mean: r is the reference's pick
+  if (a.cert_force) return false;
+  const double u = K3C_U;
+  const double qmax = fmax(fabs(__dsub_rn(yr.y, ay)), fabs(__dsub_rn(yr.x, ay))) * (1.0 + 4.0 * u);
+  const double rmax = fmax(fabs(__dsub_rn(ax, xr.x)), fabs(__dsub_rn(ax, xr.y))) * (1.0 + 4.0 * u);
+  const double v1 = __longlong_as_double(Kr);
+  const double v2 = m2 < 0 ? -1.0 : __longlong_as_double(((long long)m2 << 32) | 0xffffffffLL);  // >= every other area
+  const double E = k3c_area_err(ce, P, S, qmax, rmax, v1);
+  const bool ok = __dsub_rn(v1, v2) > 2.0 * E * (1.0 + 1e-9);
+  if (!ok) { if (NWG == 1) k3s_count(-3); else k3s_count(3); }
+  return ok;
+}
+
+// The reference's pick of bucket b given anchor `prev`, starting from a
+// guess: the guess verified (one scan), else the scan's best high-word point
+// verified (a second scan), else the full certified top-2 scan (warp: warp_pick;
+// CTA: block_bucket_argmax_cert, never storing means back).
+template <int NWG, typename XT, typename YT>
+__device__ int64_t grp_pick(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b, int64_t prev,
+                            int64_t guess, GrpRed* sh, double* s_a, long long* s_i) {
+  int64_t alt = -1;
+  if (grp_verify<NWG, XT, YT>(a, xs, ys, m, b, prev, guess, &alt, sh)) return guess;
+  if (alt >= 0 && alt != guess && grp_verify<NWG, XT, YT>(a, xs, ys, m, b, prev, alt, nullptr, sh)) return alt;
+  if (NWG == 1) k3s_count(-4); else k3s_count(4);
+  if constexpr (NWG == 1) return warp_pick<XT, YT>(a, xs, ys, m, b, prev);
+  else return block_bucket_argmax_cert<XT, YT, 32 * NWG>(a, 0, m, xs, ys, b, prev, s_a, s_i, false);
+}
+
+// One warp: argmax of the exact area over bucket b's candidate points given
+// anchor `prev` (lowest index on ties): the table's answer for any anchor.
+template <typename XT, typename YT>
+__device__ __noinline__ int64_t warp_cand_guess(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
+                                   int64_t prev) {
+  constexpr int H = K3S_H;
+  const int lane = threadIdx.x & 31;
+  const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
+  const double2 c = __ldcg(a.means + b);
+  const int nq = __ldcg(a.cand_cnt + b);
+  long long k = -2;
+  if (lane < nq) {
+    const double2 p = __ldcg(ka.cpt + b * H + lane);
+    k = lttb_area_key(ax, ay, c.x, c.y, p.x, p.y);
+  }
+  long long bk = k;
+  int bq = lane;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const long long ok = __shfl_xor_sync(FULL, bk, o);
+    const int oq = __shfl_xor_sync(FULL, bq, o);
+    if (ok > bk || (ok == bk && oq < bq)) { bk = ok; bq = oq; }
+  }
+  return bk >= -1 ? __ldcg(a.cand + b * H + bq) : lbound(a, a.n, b);
+}
+
+// ----------------------------------------------------------------- kernel --
+template <typename XT, typename YT>
+__global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) {
+  constexpr int NT = K3S_NT, NW = K3S_NW, H = K3S_H;
+  extern __shared__ __align__(16) unsigned char dsm[];  // tables [maxb][16] | pos [maxb+1] | entry [maxb]; repair state
+  __shared__ int s_e;
+  __shared__ int s_last;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t k3 = a.n_out - 2, m = a.n;
+  const int c = blockIdx.x;
+  const unsigned G = (unsigned)ka.G;
+  const int64_t B0 = (int64_t)c * k3 / G, B1 = (int64_t)(c + 1) * k3 / G;
+  const XT* xs = (const XT*)a.x;
+  const YT* ys = (const YT*)a.y;
+  unsigned char* c_tab = dsm;
+  long long* c_pos = reinterpret_cast<long long*>(dsm + ((int64_t)ka.maxb * 16 + 15) / 16 * 16);
+  int* c_e = reinterpret_cast<int*>(c_pos + ka.maxb + 1);
+  int* fcount = reinterpret_cast<int*>(ka.sync + K3S_FCOUNT);
+  auto stamp = [&](int i) {
+    if (ka.prof && t == 0) ka.prof[c * 8 + i] = gtimer();
+  };
+  if (t == 0) g_k3s_cnt = ka.prof ? ka.prof + K3S_GMAX * 8 : nullptr;  // (every CTA: same value)
+  __syncthreads();
+  stamp(0);
+
+  // ---- 1: statistics (HBM) ----
+  for (int64_t b = B0 + wid; b < B1; b += NW) k3s_stats<XT, YT>(a, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), m);
+  __syncthreads();
+  stamp(1);
+  k3s_grid_sync(ka.sync, 0, G);
+  // ---- 2: candidates (L2) ----
+  for (int64_t b = B0 + wid; b < B1; b += NW) k3s_cand<XT, YT>(a, ka, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1));
+  __syncthreads();
+  stamp(2);
+  k3s_grid_sync(ka.sync, 1, G);
+  // ---- 3: tables, aggregate A_c = T_{B1-1} o ... o T_{B0}, chain entry, positions ----
+  const double px0 = to_f64(xs, 0), py0 = to_f64(ys, 0);
+  for (int64_t b = B0 + wid; b < B1; b += NW) k3s_table(a, ka, b, px0, py0, c_tab + (b - B0) * H);
+  __syncthreads();
+  typedef PMapN<16> M;
+  if (wid == 0) {
+    M acc = M::ident();
+    for (int64_t b = B0; b < B1; ++b) acc = M::comp(M::load(c_tab + (b - B0) * H), acc);
+    if (lane == 0)
+      *reinterpret_cast<uint4*>(ka.agg + (int64_t)c * H) = make_uint4(acc.v[0], acc.v[1], acc.v[2], acc.v[3]);
+  }
+  k3s_grid_sync(ka.sync, 2, G);
+  stamp(3);
+  if (wid == 0) {
+    // entry = (A_{c-1} o ... o A_0)(0): lane l composes a contiguous run, then an ordered tree
+    int e = 0;
+    if (c > 0) {
+      const int per = (c + 31) / 32;
+      M r = M::ident();
+      for (int i = 0; i < per; ++i) {
+        const int cc = lane * per + i;
+        if (cc < c) {
+          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(ka.agg + (int64_t)cc * H));
+          M g;
+          g.v[0] = v.x; g.v[1] = v.y; g.v[2] = v.z; g.v[3] = v.w;
+          r = M::comp(g, r);
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        M other;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) other.v[i] = __shfl_down_sync(FULL, r.v[i], o);
+        if ((lane & (2 * o - 1)) == 0 && lane + o < 32) r = M::comp(other, r);
+      }
+      e = __shfl_sync(FULL, r.at0(), 0);
+    }
+    if (lane == 0) {
+      s_e = e;
+      int ee = e;
+      for (int64_t b = B0; b < B1; ++b) {
+        ee = c_tab[(b - B0) * H + ee];
+        c_e[b - B0] = ee;
+      }
+    }
+  }
+  __syncthreads();
+  for (int64_t i = t; i <= B1 - B0; i += NT) {
+    int64_t p;
+    if (i == 0) p = B0 == 0 ? 0 : __ldcg(a.cand + (B0 - 1) * H + s_e);
+    else p = __ldcg(a.cand + (B0 + i - 1) * H + c_e[i - 1]);
+    c_pos[i] = p;
+    a.pos[B0 + i] = p;
+  }
+  if (t == 0 && B1 == k3) a.pos[k3 + 1] = m - 1;
+  __syncthreads();
+  stamp(4);
+  // ---- 4a: verification (L2), one warp per bucket; the chain's picks go to
+  // the output (patched in 4b where a deviation is repaired) ----
+  __shared__ GrpRed s_red[NW];
+  __shared__ double s_a[NW];
+  __shared__ long long s_i[NW];
+  int64_t* out = a.out;
+  auto omap = [&](int64_t p) -> int64_t { return a.map ? a.map[p] : p; };
+  for (int64_t i = t; i < B1 - B0; i += NT) out[B0 + i + 1] = omap(c_pos[i + 1]);
+  if (t == 0 && B0 == 0) out[0] = omap(0);
+  if (t == 0 && B1 == k3) out[k3 + 1] = omap(m - 1);
+  for (int64_t b = B0 + wid; b < B1; b += NW) {
+    const int64_t chain = c_pos[b - B0 + 1];
+    const int64_t r = grp_pick<1, XT, YT>(a, xs, ys, m, b, c_pos[b - B0], chain, nullptr, nullptr, nullptr);
+    if (lane == 0) {
+      const bool fg = r != chain;
+      a.best[b] = r;
+      a.flag[b] = fg;
+      if (fg) a.flist[atomicAdd(fcount, 1)] = (int)b;
+    }
+    if (r != chain) k3s_count(-5);
+  }
+  stamp(5);
+  k3s_grid_sync(ka.sync, 3, G);
+  // ---- 4b: one CTA per mismatch f: the true pick of bucket f is best[f]; walk
+  // on with exact whole-CTA picks (guessed from the candidate sets) until the
+  // chain is re-joined, patching the output.  A walk that meets another
+  // mismatch (the deviations interact) leaves everything to the sequential
+  // repair walk of step 5 ----
+  {
+    const int nf = *(volatile int*)fcount;
+    for (int q = c; q < nf; q += (int)G) {
+      const int64_t f = __ldcg(a.flist + q);
+      int64_t anc = __ldcg(a.best + f);
+      if (t == 0) out[f + 1] = omap(anc);
+      for (int64_t b = f + 1; b < k3; ++b) {
+        const bool dbg = ka.prof && q == 0 && t == 0 && b - f - 1 < 4;
+        if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1)] = gtimer();
+        const int64_t guess = warp_cand_guess<XT, YT>(a, ka, xs, ys, b, anc);
+        if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1) + 1] = gtimer();
+        const int64_t r = grp_pick<NW, XT, YT>(a, xs, ys, m, b, anc, guess, s_red, s_a, s_i);
+        if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1) + 2] = gtimer();
+        if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1) + 3] = (unsigned long long)(r == guess);
+        k3s_count(6);
+        if (t == 0 && b == f + 1) a.best2[b] = r;  // (the sequential walk's speculative pick)
+        if (__ldcg(a.flag + b)) {
+          if (t == 0) atomicOr(ka.sync + K3S_CONFLICT, 1u);
+          break;
+        }
+        if (r == __ldcg(a.pos + b + 1)) break;  // re-joined the verified chain
+        if (t == 0) out[b + 1] = omap(r);
+        anc = r;
+      }
+    }
+  }
+  // ---- 5: the last CTA to finish: only if deviations interacted, the
+  // sequential repair walk over all mismatches (rewrites the output) ----
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    s_last = atomicAdd(ka.sync + K3S_DONE, 1u) == G - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  stamp(6);
+  if (*(volatile unsigned*)(ka.sync + K3S_CONFLICT)) {
+    repair_walk_smem_p<XT, YT, NT>(a, 0, dsm, [&](int64_t b, int64_t prev, double* sa, long long* si) {
+      const int64_t guess = warp_cand_guess<XT, YT>(a, ka, xs, ys, b, prev);
+      k3s_count(7);
+      return grp_pick<NW, XT, YT>(a, xs, ys, m, b, prev, guess, s_red, sa, si);
+    });
+  }
+  __syncthreads();
+  stamp(7);
+}
+
+}  // namespace mm

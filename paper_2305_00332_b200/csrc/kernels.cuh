@@ -1655,7 +1655,7 @@ __device__ double2 block_exact_mean(const LttbArgs& a, const XT* xs, const YT* y
 // (stored back: merr[b] = 0) and re-scan.
 template <typename XT, typename YT, int NT>
 __device__ int64_t block_bucket_argmax_cert(const LttbArgs& a, int64_t s, int64_t m, const XT* xs, const YT* ys,
-                                            int64_t b, int64_t prev, double* s_a, long long* s_i) {
+                                            int64_t b, int64_t prev, double* s_a, long long* s_i, bool store = true) {
   const int64_t k3 = a.n_out - 2;
   const int64_t lo = lbound(a, m, b), hi = lbound(a, m, b + 1);
   const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
@@ -1750,7 +1750,8 @@ __device__ int64_t block_bucket_argmax_cert(const LttbArgs& a, int64_t s, int64_
   if (threadIdx.x == 0) printf("exact-mean fallback: bucket %lld\n", (long long)b);
 #endif
   const double2 ce2 = block_exact_mean<XT, YT, NT>(a, xs, ys, m, b);
-  if (threadIdx.x == 0) { *mp = ce2; *ep = make_double2(0.0, 0.0); }
+  // store=false: other CTAs of a persistent kernel may be reading means/merr[b]
+  if (threadIdx.x == 0 && store) { *mp = ce2; *ep = make_double2(0.0, 0.0); }
   return block_bucket_argmax<XT, YT, NT>(xs, ys, lo, hi, ax, ay, ce2, s_a, s_i, xa);
 }
 
@@ -2291,17 +2292,14 @@ __global__ void __launch_bounds__(NT) k_lttb_repair(LttbArgs a) {
 // flagged-list sort is needed.
 __host__ __device__ inline int64_t repair_smem_bytes(int64_t k3) { return 8 * (k3 + 2) + 16 * k3 + 4 * (k3 + 1); }
 
-template <typename XT, typename YT, int NT>
-__global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
-  extern __shared__ __align__(16) unsigned char dsm[];
+// (device function: also run by the last CTA of the single-launch K3s kernel,
+// which reads state other CTAs wrote in the same launch -- hence the L2 loads)
+template <typename XT, typename YT, int NT, typename Pick>
+__device__ void repair_walk_smem_p(const LttbArgs& a, int64_t s, unsigned char* dsm, Pick pick) {
   __shared__ double s_a[NT / 32];
   __shared__ long long s_i[NT / 32];
   __shared__ int s_cm[NT];
-  const int64_t s = blockIdx.x;
   const int64_t k3 = a.n_out - 2;
-  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
-  const XT* xs = (const XT*)a.x + s * a.x_ld;
-  const YT* ys = (const YT*)a.y + s * a.y_ld;
   long long* P = (long long*)dsm;  // chain positions [k3 + 2]
   long long* Bv = P + (k3 + 2);    // verified pick given P[b] [k3]
   long long* B2 = Bv + k3;         // pick given Bv[b-1] (valid where b-1 is flagged) [k3]
@@ -2315,8 +2313,8 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t i = i0 + q * NT;
-      if (i < k3 + 2) vp[q] = pos[i];
-      if (i < k3) { vb[q] = a.best[s * k3 + i]; v2[q] = a.best2[s * k3 + i]; vf[q] = flag[i]; }
+      if (i < k3 + 2) vp[q] = __ldcg(pos + i);
+      if (i < k3) { vb[q] = __ldcg(a.best + s * k3 + i); v2[q] = __ldcg(a.best2 + s * k3 + i); vf[q] = __ldcg(flag + i); }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -2395,7 +2393,7 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
 #ifdef MM_REPAIR_TRACE
     const long long t0s = clock64();
 #endif
-    const int64_t r = k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, rb, s_rp, s_a, s_i);
+    const int64_t r = pick(rb, (int64_t)s_rp, s_a, s_i);
     if (threadIdx.x == 0) {
       scanned = r;
       atomicAdd(&g_repair_scans, 1ull);
@@ -2419,6 +2417,23 @@ __global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
     const int64_t p = P[i];
     out[i] = map ? map[p] : p;
   }
+}
+
+// the walk with K3c's certified block argmax as the exact re-scan
+template <typename XT, typename YT, int NT>
+__device__ void repair_walk_smem(const LttbArgs& a, int64_t s, unsigned char* dsm) {
+  const int64_t m = a.m_dev ? a.m_dev[s] : a.n;
+  const XT* xs = (const XT*)a.x + s * a.x_ld;
+  const YT* ys = (const YT*)a.y + s * a.y_ld;
+  repair_walk_smem_p<XT, YT, NT>(a, s, dsm, [&](int64_t b, int64_t prev, double* s_a, long long* s_i) {
+    return k3c_argmax<XT, YT, NT>(a, s, m, xs, ys, b, prev, s_a, s_i);
+  });
+}
+
+template <typename XT, typename YT, int NT>
+__global__ void __launch_bounds__(NT) k_lttb_repair_smem(LttbArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  repair_walk_smem<XT, YT, NT>(a, blockIdx.x, dsm);
 }
 
 // ----------------------------------------------------------- misc -------

@@ -2,6 +2,7 @@
 // lttb_x_{f32,f64,i64,i32}.cu (parallel compilation); dispatch in lttb_launch.cu.
 #pragma once
 #include "host.cuh"
+#include "k3s.cuh"
 
 namespace mmh {
 
@@ -57,6 +58,51 @@ int launch_tables_jump(LttbArgs a, cudaStream_t st) {
   }
 }
 
+// K3s (k3s.cuh): the whole large-bucket LTTB of one series in one cooperative
+// launch.  MM_ENOTSUP when the shape does not suit it (too few buckets to fill
+// the SMs' warps, or a repair state beyond shared memory; MMLTTB_K3S=0, the
+// A/B knob): the caller falls back to the K3c kernels.
+unsigned long long* k3s_prof_buffer();
+
+template <typename XT, typename YT>
+int launch_k3s(LttbArgs a, void* scratch, cudaStream_t st) {
+  static const bool on = env_i64("MMLTTB_K3S", 1) != 0;
+  if (!on) return MM_ENOTSUP;
+  const int64_t k3 = a.n_out - 2;
+  int dev = 0, nsm = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(MM_ECUDA, "cudaGetDevice");
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (nsm < 1 || nsm > K3S_GMAX || k3 < 8LL * nsm) return MM_ENOTSUP;
+  if (((uintptr_t)a.x & 15) || ((uintptr_t)a.y & 15)) return MM_ENOTSUP;  // 16-byte vector loads  // < 8 busy warps per SM: K3c's flat passes win
+  auto kern = k_lttb_k3s<XT, YT>;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, (const void*)kern) != cudaSuccess) return fail(MM_ECUDA, "cudaFuncGetAttributes(k3s)");
+  const int64_t G = nsm;
+  const int64_t maxb = cdiv(k3, G) + 1;
+  const int64_t dyn = std::max<int64_t>(up(maxb * 16) + (maxb + 1) * 8 + maxb * 4, repair_smem_bytes(k3));
+  if (dyn + (int64_t)fa.sharedSizeBytes > optin) return MM_ENOTSUP;
+  static std::atomic<unsigned long long> attr{0};
+  if (int rc = smem_optin(attr, (const void*)kern, (int)(optin - fa.sharedSizeBytes), "k_lttb_k3s")) return rc;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K3S_NT, (size_t)dyn) != cudaSuccess || occ < 1)
+    return MM_ENOTSUP;
+  K3sArgs ka{};
+  ka.G = (int)G;
+  ka.maxb = (int)maxb;
+  ka.sync = (unsigned*)scratch;  // K3S_SYNC_WORDS counters / flags (fcount among them)
+  a.fcount = (int*)(ka.sync + K3S_FCOUNT);
+  ka.agg = (unsigned char*)scratch + up(K3S_SYNC_WORDS * 4);
+  ka.cpt = (double2*)(ka.agg + up((int64_t)K3S_GMAX * 16));
+  ka.prof = k3s_prof_buffer();  // tools only (MMLTTB_K3S_PROF=1)
+  if (ka.prof) cudaMemsetAsync(ka.prof, 0, (size_t)(K3S_GMAX * 8 + 64) * 8, st);
+  if (cudaMemsetAsync(ka.sync, 0, (size_t)K3S_SYNC_WORDS * 4, st) != cudaSuccess) return fail(MM_ECUDA, "memset(k3s)");
+  void* args[] = {(void*)&a, (void*)&ka};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(K3S_NT), args, (size_t)dyn, st);
+  if (e != cudaSuccess) { (void)cudaGetLastError(); return fail(MM_ECUDA, "k_lttb_k3s: %s", cudaGetErrorString(e)); }
+  return check_launch("k_lttb_k3s");
+}
+
 // K3c: large buckets (see kernels.cuh): means, hull candidates, candidate
 // tables, jump (positions), verification, repair + output
 template <typename XT, typename YT, int H>
@@ -109,6 +155,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
     fl.part = cv.take<unsigned char>(k3 * flat_cp_max(k3) * K3C_FLAT_PART);
     fl.ulist = cv.take<int>(k3);
     fl_c.part = fl.part;
+    const int rk = launch_k3s<XT, YT>(a, fl.part, st);
+    if (rk != MM_ENOTSUP) return rk;  // otherwise: the multi-kernel K3c below
     if (cudaMemsetAsync(fcnt, 0, (size_t)(3 * k3 + 3) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "memset");
   }

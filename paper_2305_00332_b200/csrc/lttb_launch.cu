@@ -37,6 +37,17 @@ int launch_lttb(LttbArgs a, int xdt, int ydt, int64_t s, cudaStream_t st) {
   return fail(MM_EINVAL, "x dtype");
 }
 
+// K3s phase timestamps (tools/k3s_check.py --prof): [G][8] %globaltimer values
+unsigned long long* k3s_prof_buffer() {
+  static const bool on = env_i64("MMLTTB_K3S_PROF", 0) != 0;
+  static unsigned long long* buf = nullptr;
+  if (on && !buf) {
+    if (cudaMalloc(&buf, (K3S_GMAX * 8 + 64) * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+    if (buf) cudaMemset(buf + K3S_GMAX * 8, 0, 64 * 8);
+  }
+  return on ? buf : nullptr;
+}
+
 int64_t repair_scans_read() {
   const int64_t v[4] = {repair_scans_f32(), repair_scans_f64(), repair_scans_i64(), repair_scans_i32()};
   int64_t t = 0;
@@ -48,3 +59,10 @@ int64_t repair_scans_read() {
 }
 
 }  // namespace mmh
+
+extern "C" int64_t mmlttb_debug_k3s_prof(unsigned long long* host, int64_t n) {
+  unsigned long long* b = mmh::k3s_prof_buffer();
+  if (!b || n > mm::K3S_GMAX * 8 + 64) return -1;
+  if (cudaMemcpy(host, b, (size_t)n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return n;
+}
