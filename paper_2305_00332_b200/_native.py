@@ -7,6 +7,7 @@ raises instead of silently computing somewhere else.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -78,7 +79,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # MMLTTB_LIB: an alternative in-tree build (A/B tuning builds under tools/)
+        p = Path(path) if path else Path(os.environ.get("MMLTTB_LIB", LIB_PATH))
         if not p.exists():
             raise ImportError(
                 f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -34,8 +34,17 @@ namespace mm {
 
 constexpr int K3S_NT = 512;          // 16 warps per CTA
 constexpr int K3S_NW = K3S_NT / 32;
-constexpr int K3S_D = 8;             // sampled slopes -> <= 16 candidates per bucket
-constexpr int K3S_H = 2 * K3S_D;     // candidate slots per bucket (== the K3c table width)
+#ifndef K3S_DIRS
+#define K3S_DIRS 16
+#endif
+// sampled slopes -> <= 2D candidates per bucket (2D <= 32).  Measured on C2
+// (1,998 buckets): 8 slopes leave ~5 buckets per call whose pick is outside
+// the candidate set (each costing a whole-CTA walk step after the
+// verification), 12 leave ~2, 16 leave none (117 vs 124 us per call); two
+// clusters of slopes at the anchor box's y edges instead of an even spread
+// are worse (6 misses with 8 or 12)
+constexpr int K3S_D = K3S_DIRS;
+constexpr int K3S_H = K3S_D <= 8 ? 16 : 32;  // candidate slots per bucket (table width: 16 or 32)
 constexpr int K3S_U = 8;             // loads in flight per lane per array
 constexpr int K3S_GMAX = 1024;       // CTA bound for the workspace
 
@@ -49,7 +58,9 @@ struct K3sArgs {
 };
 // sync words: barrier i = counter at 64 i, release flag at 64 i + 32 (separate
 // 128-byte lines: the pollers never delay the arrivals); done counter, fcount
-constexpr int K3S_DONE = 64 * 4, K3S_FCOUNT = 64 * 4 + 32, K3S_CONFLICT = 64 * 5, K3S_SYNC_WORDS = 64 * 6;
+constexpr int K3S_DONE = 64 * 4, K3S_FCOUNT = 64 * 4 + 32, K3S_CONFLICT = 64 * 5;
+// per-CTA "statistics published" / "candidates published" flags (neighbours wait on them)
+constexpr int K3S_FLAGS = 64 * 6, K3S_SYNC_WORDS = 64 * 6 + 2 * K3S_GMAX;
 
 __device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
   unsigned v;
@@ -398,7 +409,8 @@ template <typename XT, typename YT, bool AFF>
 __device__ __forceinline__ void k3s_cand_t(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
                                            int64_t lo, int64_t hi, const float (&lam)[K3S_D], double xlo) {
   constexpr int D = K3S_D, H = K3S_H;
-  constexpr int EV = Vec<YT>::EV, UV = 16 / EV, PR = 16;  // points per lane per round
+  constexpr int PR = K3S_D >= 12 ? 8 : 16;  // points per lane per round
+  constexpr int EV = Vec<YT>::EV, UV = PR / EV;
   const int lane = threadIdx.x & 31;
   auto tval = [&](int64_t j) -> float { return AFF ? (float)(j - lo) : (float)(elem_f64(xs[j]) - xlo); };
   float vmax[D], vmin[D];
@@ -570,9 +582,10 @@ __device__ __forceinline__ void k3s_cand(const LttbArgs& a, const K3sArgs& ka, c
 // Lane l: anchor p = l/2, candidates q in [8(l&1), 8(l&1)+8).
 static __device__ __noinline__ void k3s_table(const LttbArgs& a, const K3sArgs& ka, int64_t b, double x0, double y0,
                                           unsigned char* tab) {
-  constexpr int H = K3S_H;
+  constexpr int H = K3S_H, PL = 32 / H == 2 ? 2 : 1;  // lanes per anchor
+  constexpr int QL = H / PL;                           // candidates per lane
   const int lane = threadIdx.x & 31;
-  const int p = lane >> 1, q0 = (lane & 1) * 8;
+  const int p = lane / PL, q0 = (lane % PL) * QL;
   int na = 1;
   double ax = x0, ay = y0;
   if (b > 0) {
@@ -584,22 +597,22 @@ static __device__ __noinline__ void k3s_table(const LttbArgs& a, const K3sArgs& 
   }
   const int nq = __ldcg(a.cand_cnt + b);
   const double2 c = __ldcg(a.means + b);
-  double2 pts[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) pts[i] = q0 + i < nq ? __ldcg(ka.cpt + b * H + q0 + i) : make_double2(0.0, 0.0);
   long long bk = -2;
   int bq = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
+#pragma unroll 8
+  for (int i = 0; i < QL; ++i) {
     if (q0 + i < nq) {
-      const long long k = lttb_area_key(ax, ay, c.x, c.y, pts[i].x, pts[i].y);
+      const double2 pt = __ldcg(ka.cpt + b * H + q0 + i);
+      const long long k = lttb_area_key(ax, ay, c.x, c.y, pt.x, pt.y);
       if (k > bk) { bk = k; bq = q0 + i; }
     }
   }
-  const long long ok = __shfl_xor_sync(FULL, bk, 1);
-  const int oq = __shfl_xor_sync(FULL, bq, 1);
-  if (ok > bk || (ok == bk && oq < bq)) { bk = ok; bq = oq; }
-  if ((lane & 1) == 0) tab[p] = (unsigned char)(p < na && bk >= -1 ? bq : 0);
+  if (PL == 2) {
+    const long long ok = __shfl_xor_sync(FULL, bk, 1);
+    const int oq = __shfl_xor_sync(FULL, bq, 1);
+    if (ok > bk || (ok == bk && oq < bq)) { bk = ok; bq = oq; }
+  }
+  if (lane % PL == 0) tab[p] = (unsigned char)(p < na && bk >= -1 ? bq : 0);
 }
 
 // ---------------------------------------------------------------- phase 4 --
@@ -918,7 +931,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   const XT* xs = (const XT*)a.x;
   const YT* ys = (const YT*)a.y;
   unsigned char* c_tab = dsm;
-  long long* c_pos = reinterpret_cast<long long*>(dsm + ((int64_t)ka.maxb * 16 + 15) / 16 * 16);
+  long long* c_pos = reinterpret_cast<long long*>(dsm + ((int64_t)ka.maxb * H + 15) / 16 * 16);
   int* c_e = reinterpret_cast<int*>(c_pos + ka.maxb + 1);
   int* fcount = reinterpret_cast<int*>(ka.sync + K3S_FCOUNT);
   auto stamp = [&](int i) {
@@ -932,22 +945,40 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_stats<XT, YT>(a, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), m);
   __syncthreads();
   stamp(1);
-  k3s_grid_sync(ka.sync, 0, G);
+  // candidates of buckets [B0, B1) need the statistics of B0-1 and B1 (the
+  // neighbour CTAs'): wait for those two, not for the whole grid
+  if (t == 0) {
+    __threadfence();
+    st_rel(ka.sync + K3S_FLAGS + c, 1u);
+    if (c > 0) spin_until_set(ka.sync + K3S_FLAGS + c - 1, 1u);
+    if (c + 1 < (int)G) spin_until_set(ka.sync + K3S_FLAGS + c + 1, 1u);
+  }
+  __syncthreads();
   // ---- 2: candidates (L2) ----
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_cand<XT, YT>(a, ka, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1));
   __syncthreads();
   stamp(2);
-  k3s_grid_sync(ka.sync, 1, G);
+  // the tables of [B0, B1) need CTA c-1's last candidate set
+  if (t == 0) {
+    __threadfence();
+    st_rel(ka.sync + K3S_FLAGS + K3S_GMAX + c, 1u);
+    if (c > 0) spin_until_set(ka.sync + K3S_FLAGS + K3S_GMAX + c - 1, 1u);
+  }
+  __syncthreads();
   // ---- 3: tables, aggregate A_c = T_{B1-1} o ... o T_{B0}, chain entry, positions ----
   const double px0 = to_f64(xs, 0), py0 = to_f64(ys, 0);
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_table(a, ka, b, px0, py0, c_tab + (b - B0) * H);
   __syncthreads();
-  typedef PMapN<16> M;
+  typedef PMapN<H> M;
+  constexpr int NV = H / 16;  // uint4 words per map
   if (wid == 0) {
     M acc = M::ident();
     for (int64_t b = B0; b < B1; ++b) acc = M::comp(M::load(c_tab + (b - B0) * H), acc);
-    if (lane == 0)
-      *reinterpret_cast<uint4*>(ka.agg + (int64_t)c * H) = make_uint4(acc.v[0], acc.v[1], acc.v[2], acc.v[3]);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        reinterpret_cast<uint4*>(ka.agg + (int64_t)c * H)[i] = make_uint4(acc.v[4 * i], acc.v[4 * i + 1], acc.v[4 * i + 2], acc.v[4 * i + 3]);
+    }
   }
   k3s_grid_sync(ka.sync, 2, G);
   stamp(3);
@@ -960,9 +991,12 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
       for (int i = 0; i < per; ++i) {
         const int cc = lane * per + i;
         if (cc < c) {
-          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(ka.agg + (int64_t)cc * H));
           M g;
-          g.v[0] = v.x; g.v[1] = v.y; g.v[2] = v.z; g.v[3] = v.w;
+#pragma unroll
+          for (int i2 = 0; i2 < NV; ++i2) {
+            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(ka.agg + (int64_t)cc * H) + i2);
+            g.v[4 * i2] = v.x; g.v[4 * i2 + 1] = v.y; g.v[4 * i2 + 2] = v.z; g.v[4 * i2 + 3] = v.w;
+          }
           r = M::comp(g, r);
         }
       }
@@ -970,7 +1004,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
       for (int o = 1; o < 32; o <<= 1) {
         M other;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) other.v[i] = __shfl_down_sync(FULL, r.v[i], o);
+        for (int i = 0; i < 4 * NV; ++i) other.v[i] = __shfl_down_sync(FULL, r.v[i], o);
         if ((lane & (2 * o - 1)) == 0 && lane + o < 32) r = M::comp(other, r);
       }
       e = __shfl_sync(FULL, r.at0(), 0);

@@ -80,7 +80,7 @@ int launch_k3s(LttbArgs a, void* scratch, cudaStream_t st) {
   if (cudaFuncGetAttributes(&fa, (const void*)kern) != cudaSuccess) return fail(MM_ECUDA, "cudaFuncGetAttributes(k3s)");
   const int64_t G = nsm;
   const int64_t maxb = cdiv(k3, G) + 1;
-  const int64_t dyn = std::max<int64_t>(up(maxb * 16) + (maxb + 1) * 8 + maxb * 4, repair_smem_bytes(k3));
+  const int64_t dyn = std::max<int64_t>(up(maxb * K3S_H) + (maxb + 1) * 8 + maxb * 4, repair_smem_bytes(k3));
   if (dyn + (int64_t)fa.sharedSizeBytes > optin) return MM_ENOTSUP;
   static std::atomic<unsigned long long> attr{0};
   if (int rc = smem_optin(attr, (const void*)kern, (int)(optin - fa.sharedSizeBytes), "k_lttb_k3s")) return rc;
@@ -93,7 +93,7 @@ int launch_k3s(LttbArgs a, void* scratch, cudaStream_t st) {
   ka.sync = (unsigned*)scratch;  // K3S_SYNC_WORDS counters / flags (fcount among them)
   a.fcount = (int*)(ka.sync + K3S_FCOUNT);
   ka.agg = (unsigned char*)scratch + up(K3S_SYNC_WORDS * 4);
-  ka.cpt = (double2*)(ka.agg + up((int64_t)K3S_GMAX * 16));
+  ka.cpt = (double2*)(ka.agg + up((int64_t)K3S_GMAX * K3S_H));
   ka.prof = k3s_prof_buffer();  // tools only (MMLTTB_K3S_PROF=1)
   if (ka.prof) cudaMemsetAsync(ka.prof, 0, (size_t)(K3S_GMAX * 8 + 64) * 8, st);
   if (cudaMemsetAsync(ka.sync, 0, (size_t)K3S_SYNC_WORDS * 4, st) != cudaSuccess) return fail(MM_ECUDA, "memset(k3s)");

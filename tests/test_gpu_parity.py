@@ -574,3 +574,56 @@ def test_batched_validate_row_order():
         mm.minmaxlttb(x, y, 50, minmax_ratio=4, validate=True)
     x2 = torch.arange(n, dtype=torch.int64, device=DEV)[:, None].repeat(1, 3)[:, 0]  # shared x, fine
     mm.minmaxlttb(x2, torch.randn(3, n, device=DEV), 50, minmax_ratio=4, validate=True)
+
+
+K3S_CASE = """
+import sys
+import numpy as np, torch
+sys.path.insert(0, '.')
+import paper_2305_00332_b200 as mm
+from oracle import oracle as O
+rng = np.random.Generator(np.random.PCG64(21))
+n = 700_001
+x = np.arange(n, dtype=np.int64)
+y = np.cumsum(rng.standard_normal(n)) + rng.normal(0, 0.5, n)
+xi = np.cumsum(rng.integers(1, 4, n)).astype(np.int64)
+yd = np.repeat(np.cumsum(rng.standard_normal(n // 2 + 1)), 2)[:n].copy()
+for xx, yy, k in [(x, y, 2000), (xi, y.astype(np.float32), 1500), (x, yd, 1800), (x.astype(np.float64) * 0.25, y, 3001)]:
+    got = mm.lttb(torch.from_numpy(xx).cuda(), torch.from_numpy(yy).cuda(), k).cpu().numpy()
+    if not np.array_equal(got, O.lttb(xx, yy.astype(np.float64), k)):
+        sys.exit('mismatch at n_out=%d' % k)
+print('ok')
+"""
+
+
+@pytest.mark.parametrize("knobs", [{}, {"MMLTTB_K3C_CAND_CAP": "1"}, {"MMLTTB_K3C_CAND_CAP": "2"},
+                                   {"MMLTTB_K3C_CERT_FORCE": "1"}, {"MMLTTB_K3S": "0"}])
+def test_lttb_k3s_single_launch(knobs):
+    """K3s (one cooperative launch for full LTTB over >= 8 x SMs large buckets):
+    arange / irregular integer / duplicated-point / float x, f64 and f32 y, at
+    its default, with the candidate sets cut to 1-2 points (every bucket's pick
+    missed: 4a mismatches, 4b deviation walks and the sequential repair walk
+    all run), with every certification failing (in-order exact means), and the
+    multi-kernel K3c fallback (MMLTTB_K3S=0) -- all index-exact vs the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, **knobs)
+    r = subprocess.run([sys.executable, "-c", K3S_CASE], env=env, capture_output=True, text=True,
+                       cwd=str(GOLD.parent.parent), timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-500:] + r.stderr[-2000:]
+
+
+def test_lttb_k3s_repeatable():
+    """The cross-CTA protocols of the single-launch kernel (neighbour flags,
+    grid barriers, aggregate exchange, last-CTA repair) must be deterministic:
+    30 back-to-back calls give identical indices."""
+    rng = np.random.Generator(np.random.PCG64(5))
+    n = 3_000_000
+    x = torch.arange(n, dtype=torch.int64, device=DEV)
+    y = torch.from_numpy(np.cumsum(rng.standard_normal(n))).to(DEV)
+    first = mm.lttb(x, y, 2500)
+    for _ in range(30):
+        assert torch.equal(mm.lttb(x, y, 2500), first)
+    assert np.array_equal(first.cpu().numpy(), O.lttb(x.cpu().numpy(), y.cpu().numpy(), 2500))
