@@ -75,10 +75,10 @@ void stage_mark(cudaStream_t st, int i) {
 int64_t preselect_ws(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt, bool with_lttb) {
   const int64_t k = (n_out - 2) * (r_ps / 2);
   const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * k, S, ydt, B, true);
+  const ExPlan p = plan_extrema(B * k, S, ydt, B, true, with_lttb && k23_ok(B, k, n_out, r_ps) && dyn_chunk_elems() > 0);
   const int64_t cap = 2 + 2 * k;
   int64_t bytes = ex_ws(B * k, p) + up(B * 8);
-  if (with_lttb) bytes += 3 * up(B * cap * 8) + lttb_ws(B, n_out, r_ps);
+  if (with_lttb) bytes += 3 * up(B * cap * 8) + lttb_ws(B, n_out, r_ps) + k23_ws() + up(4 * (K23_STAT + B * k));
   return bytes;
 }
 
@@ -309,6 +309,46 @@ static int minmaxlttb_entry(const void* x, int x_dtype, int64_t x_ld, const void
   const int64_t k = (n_out - 2) * (r_ps / 2);
   if (k > N - 2) return fail(MM_EINVAL, "sub-buckets exceed interior");
   if (!mul_ok(k, N)) return fail(MM_ERANGE, "k*N overflows int64");
+  const int64_t S = cdiv(N - 2, k);
+  const bool k23 = k23_ok(B, k, n_out, r_ps);
+  const ExPlan p = plan_extrema(B * k, S, y_dtype, B, true, k23 && dyn_chunk_elems() > 0);
+  const int64_t cap = 2 + 2 * k;
+  if (k23) {
+    // one series: K1, then K2 + K3 in one cooperative launch (K23).  The only
+    // zeroing of the call is one memset over K23's barrier words and K1's
+    // arrival counters (adjacent); the status word is written, not ORed.
+    Carve cv{(char*)workspace, workspace_bytes};
+    int* status = cv.take<int>(1);
+    unsigned* zr = cv.take<unsigned>(K23_STAT + B * k);
+    unsigned* k23s = cv.take<unsigned>(k23_ws() / 4);
+    ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
+    carve_ex(cv, B * k, p, ea);
+    int64_t* pre = cv.take<int64_t>(B * cap);
+    double* px = cv.take<double>(B * cap);
+    double* py = cv.take<double>(B * cap);
+    if (!cv.ok) return fail(MM_EWORKSPACE, "workspace too small (%lld bytes)", (long long)workspace_bytes);
+    ea.arrivals = zr + K23_STAT;  // (the carve_ex slot stays unused)
+    ea.arrivals_zeroed = 1;
+    ea.ticket = p.E > 0 && dyn_chunk_elems() > 0 ? zr + 128 : nullptr;  // (zeroed with the rest)
+    if (cudaMemsetAsync(zr, 0, (size_t)(K23_STAT + B * k) * sizeof(unsigned), st) != cudaSuccess)
+      return fail(MM_ECUDA, "memset");
+    stage_mark(st, 0);
+    if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
+    stage_mark(st, 1);
+    K23Args ka{};
+    ka.ext = ea.ext; ka.cnt8 = ea.cnt8; ka.k = k; ka.N = N; ka.n_out = n_out;
+    ka.x = x; ka.y = y; ka.pre = pre; ka.px = px; ka.py = py; ka.out = out; ka.status = status;
+    ka.sync = zr;
+    ka.stat = k23s;
+    if ((rc = launch_k23(ka, x_dtype, y_dtype, r_ps, st))) return rc;
+    stage_mark(st, 2);
+    stage_mark(st, 3);
+    if (out_count) {
+      k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
+      return check_launch("k_fill");
+    }
+    return MM_OK;
+  }
   Carve cv0{(char*)workspace, workspace_bytes};
   int* status = take_status(cv0, st);
   if (!status) return fail(MM_EWORKSPACE, "workspace too small");
@@ -325,9 +365,6 @@ static int minmaxlttb_entry(const void* x, int x_dtype, int64_t x_ld, const void
     }
     return MM_OK;
   }
-  const int64_t S = cdiv(N - 2, k);
-  const ExPlan p = plan_extrema(B * k, S, y_dtype, B, true);
-  const int64_t cap = 2 + 2 * k;
   Carve cv = cv0;
   ExArgs ea{y, y_ld, B, 1, N - 2, k, nullptr, 0, k, p.C, p.chunk};
   carve_ex(cv, B * k, p, ea);

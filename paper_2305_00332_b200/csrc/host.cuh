@@ -19,6 +19,7 @@
 #include "../../include/mmlttb.h"
 #include "kernels.cuh"
 #include "fused.cuh"
+#include "k23.cuh"
 
 using namespace mm;
 
@@ -69,7 +70,14 @@ inline int64_t env_i64(const char* name, int64_t dflt) {
   return e ? atoll(e) : dflt;
 }
 
-inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, int64_t B = 0, bool closed_form = false) {
+inline int64_t dyn_chunk_elems() {
+  // measured and not adopted: 4096 / 8192 / 16384-element chunks made C3 K1 93 / 83 / 84 us vs
+  // 75 us with one range per warp (each new chunk restarts the load pipeline)
+  static const int64_t v = env_i64("MMLTTB_K1_DYN_CHUNK", 0);
+  return v;
+}
+inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, int64_t B = 0, bool closed_form = false,
+                           bool dyn = false) {
   // tuned on B200 (tools/plan_sweep.sh): ~4 waves of 148 SMs x 32 resident
   // warps, chunks of >= 4096 float32 elements
   static const int64_t want = env_i64("MMLTTB_K1_WANT_WARPS", 148LL * 128);
@@ -77,6 +85,9 @@ inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, i
   // flat split: one wave of 148 SMs x 24 resident warps (80 regs), two for
   // very long series (tools/flat_sweep.sh)
   static const int64_t flat_env = env_i64("MMLTTB_K1_FLAT_WARPS", -1);
+  // ticketed flat K1 (when the caller provides a zeroed ticket): chunk length in
+  // float32-equivalent elements (A/B knob MMLTTB_K1_DYN_CHUNK; 0 = one range per warp)
+  const int64_t dyn_chunk = dyn ? dyn_chunk_elems() : 0;
   const int64_t min_chunk = ydt == MM_F32 ? minc32 : minc32 / 2;
   ExPlan p;
   const int64_t nb_ = B > 0 ? buckets_total / B : 0;
@@ -88,6 +99,7 @@ inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, i
     const int64_t nb = nb_;
     p.Ws = std::max<int64_t>(1, flat_warps / B);
     p.E = std::max<int64_t>(min_chunk, cdiv(nb * max_bucket, p.Ws));
+    if (dyn_chunk > 0) p.E = std::min<int64_t>(p.E, dyn_chunk * (ydt == MM_F32 ? 1 : 2) / 2 * 2);  // ticketed chunks
     p.Ws = cdiv(nb * max_bucket, p.E);
     p.CP = cdiv(max_bucket, p.E) + 1;
     p.C = 1;
@@ -169,6 +181,11 @@ int64_t repair_scans_read();
 bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt);
 int launch_fused(const FusedArgs& fa, int xdt, int ydt, cudaStream_t st);
 int sm_count();
+
+// ---- K2 + K3 of one series in one cooperative launch (k23_launch.cu) ----
+bool k23_ok(int64_t B, int64_t k, int64_t n_out, int64_t r_ps);
+int64_t k23_ws();
+int launch_k23(K23Args a, int xdt, int ydt, int64_t r_ps, cudaStream_t st);
 
 // ---- K2 + K3 single-CTA (post_launch.cu) ----
 constexpr int PAIR_NT = 128, PAIR_ITEMS = 2;

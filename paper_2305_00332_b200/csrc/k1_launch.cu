@@ -5,9 +5,9 @@ namespace mmh {
 
 int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
   if (a.E > 0) {  // flat split
-    if (cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
+    if (!a.arrivals_zeroed && cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
-    const int64_t blocks = cdiv(a.B * a.Ws, 8);
+    const int64_t blocks = a.ticket ? std::min<int64_t>(cdiv(a.B * a.Ws, 8), (int64_t)sm_count() * 3) : cdiv(a.B * a.Ws, 8);
     if (ydt == MM_F32) {
 #ifdef MMLTTB_AB  // tuning build only (tools/flat_sweep.sh)
       static const int64_t fv = env_i64("MMLTTB_K1_FLAT_VARIANT", 0);
@@ -46,7 +46,7 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
     return check_launch("k_extrema(small)");
   }
   const int64_t warps = a.B * a.nb * a.C;
-  if (a.C > 1 && cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
+  if (a.C > 1 && !a.arrivals_zeroed && cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
     return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");
   const int64_t blocks = cdiv(warps, 8);
   if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");

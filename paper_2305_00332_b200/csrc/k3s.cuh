@@ -79,7 +79,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void spin_until_set(const unsigned* p, unsigned want) {
   const unsigned long long t0 = gtimer();
   while (ld_acq(p) < want) {
-    __nanosleep(100);
+    __nanosleep(32);
     if (gtimer() - t0 > 2000000000ull) __trap();  // 2 s
   }
 }

@@ -128,6 +128,9 @@ struct ExArgs {
   struct Ext* ext;         // [B][nb]      final (imin, imax) per bucket
   unsigned char* cnt8;     // [B][nb]      1 + (imin != imax): K2's scan input
   int64_t E, Ws, CP;       // flat mode: elements per warp, warps per series, partial stride
+  int arrivals_zeroed;     // the caller zeroed `arrivals` (merged into its own memset)
+  unsigned* ticket;        // flat mode: chunk ticket (zeroed per call) -> persistent warps take
+                           // chunks dynamically; null: one static range per warp
 };
 
 struct Ext {
@@ -297,13 +300,10 @@ __device__ __forceinline__ void publish_partial(const ExArgs& a, int64_t bkt, in
 // does the same work (no last-wave tail); a range spanning bucket edges
 // publishes one partial per intersected bucket (slot = w - first warp of the
 // bucket), combined by the bucket's last-arriving warp.
-template <typename T, int U, int LDV, int MINB = 3>
-__global__ void __launch_bounds__(256, MINB) k_extrema_flat(ExArgs a) {
+template <typename T, int U, int LDV>
+__device__ __forceinline__ void flat_range(const ExArgs& a, int64_t w, int lane) {
   typedef YTr<T> Tr;
   typedef typename Tr::K K;
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= a.B * a.Ws) return;  // warp-uniform
   const int64_t s = w / a.Ws, wl = w % a.Ws;
   const T* y = (const T*)a.y + s * a.y_ld;
   const int64_t E_lo = pbound(a.start, a.len, a.k, a.b0), E_hi = pbound(a.start, a.len, a.k, a.b0 + a.nb);
@@ -327,6 +327,24 @@ __global__ void __launch_bounds__(256, MINB) k_extrema_flat(ExArgs a) {
     if (bhi >= e1) break;
     ++b;
   }
+}
+
+template <typename T, int U, int LDV, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) k_extrema_flat(ExArgs a) {
+  const int lane = threadIdx.x & 31;
+  if (a.ticket) {  // persistent warps take the next range until none is left (no single-wave tail)
+    for (;;) {
+      unsigned w = 0;
+      if (lane == 0) w = atomicAdd(a.ticket, 1u);
+      w = __shfl_sync(FULL, w, 0);
+      if ((int64_t)w >= a.B * a.Ws) break;
+      flat_range<T, U, LDV>(a, (int64_t)w, lane);
+    }
+    return;
+  }
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= a.B * a.Ws) return;  // warp-uniform
+  flat_range<T, U, LDV>(a, w, lane);
 }
 
 // One warp per (series, bucket, chunk).  Lanes stream 16-byte vectors
