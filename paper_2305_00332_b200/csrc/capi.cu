@@ -6,6 +6,7 @@
 // stream.  Nothing here synchronises the host.  The kernel launchers live in
 // k1_launch.cu / lttb_launch.cu / fused_launch.cu / post_launch.cu (host.cuh).
 #include "host.cuh"
+#include "k23.cuh"
 #include "raster.cuh"
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX3: a no-op unless a tool (nsys / ncu) is attached
@@ -596,7 +597,7 @@ int mmlttb_deinterleave_f64(const void* pairs, int64_t n, double* x, double* y, 
   if (!pairs || !x || !y || n < 0) return fail(MM_EINVAL, "bad arguments");
   if (n == 0) return MM_OK;
   if ((uintptr_t)pairs % 16) return fail(MM_EINVAL, "pairs must be 16-byte aligned");
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), (int64_t)sm_count() * 32);
   k_deinterleave_f64<<<blocks, 256, 0, (cudaStream_t)stream>>>((const double2*)pairs, x, y, n);
   return check_launch("k_deinterleave_f64");
 }

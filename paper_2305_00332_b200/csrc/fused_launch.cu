@@ -4,22 +4,29 @@
 namespace mmh {
 
 // ---- fused per-series path (batches of medium series) --------------------
-constexpr int64_t FUSED_MIN_B = 148;
 
 bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt) {
   static const bool off = env_i64("MMLTTB_NO_FUSED", 0) != 0;  // A/B knob
   const int64_t k = (n_out - 2) * (r_ps / 2);
-  return !off && B >= FUSED_MIN_B && r_ps >= 2 && r_ps <= 8 && N < (1LL << 31) &&
+  return !off && B >= sm_count() && r_ps >= 2 && r_ps <= 8 && N < (1LL << 31) &&
          fused_smem(k, n_out - 2, 8, esize(ydt)) <= FUSED_SMEM_MAX;
 }
 
+// SM count of the current device (cached per device; 148, a B200, when none is present)
 int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) { (void)cudaGetLastError(); return 148; }
+  if (dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
   }
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    n = 148;
+  }
+  if (dev < 64) cache[dev].store(n, std::memory_order_relaxed);
   return n;
 }
 

@@ -19,9 +19,9 @@
 #include "../../include/mmlttb.h"
 #include "kernels.cuh"
 #include "fused.cuh"
-#include "k23.cuh"
 
 using namespace mm;
+namespace mm { struct K23Args; }
 
 namespace mmh {
 
@@ -70,6 +70,8 @@ inline int64_t env_i64(const char* name, int64_t dflt) {
   return e ? atoll(e) : dflt;
 }
 
+int sm_count();  // of the current device (148 on B200; 148 when no device is present)
+
 inline int64_t dyn_chunk_elems() {
   // measured and not adopted: 4096 / 8192 / 16384-element chunks made C3 K1 93 / 83 / 84 us vs
   // 75 us with one range per warp (each new chunk restarts the load pipeline)
@@ -80,7 +82,9 @@ inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, i
                            bool dyn = false) {
   // tuned on B200 (tools/plan_sweep.sh): ~4 waves of 148 SMs x 32 resident
   // warps, chunks of >= 4096 float32 elements
-  static const int64_t want = env_i64("MMLTTB_K1_WANT_WARPS", 148LL * 128);
+  const int64_t nsm = sm_count();
+  static const int64_t want_env = env_i64("MMLTTB_K1_WANT_WARPS", -1);
+  const int64_t want = want_env >= 0 ? want_env : nsm * 128;
   static const int64_t minc32 = env_i64("MMLTTB_K1_MIN_CHUNK", 4096);
   // flat split: one wave of 148 SMs x 24 resident warps (80 regs), two for
   // very long series (tools/flat_sweep.sh)
@@ -91,7 +95,7 @@ inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, i
   const int64_t min_chunk = ydt == MM_F32 ? minc32 : minc32 / 2;
   ExPlan p;
   const int64_t nb_ = B > 0 ? buckets_total / B : 0;
-  const int64_t flat_warps = flat_env >= 0 ? flat_env : (nb_ * max_bucket > 400000000LL ? 148LL * 48 : 148LL * 24);
+  const int64_t flat_warps = flat_env >= 0 ? flat_env : (nb_ * max_bucket > 400000000LL ? nsm * 48 : nsm * 24);
   // flat split above this many elements per bucket (A/B knob MMLTTB_K1_FLAT_MIN; measured on
   // C3 r=32, 3,128-point buckets: 8-lane groups 117.6 us vs flat 126.8 us per call)
   static const int64_t flat_min = env_i64("MMLTTB_K1_FLAT_MIN", SMALL_BUCKET);
@@ -170,9 +174,9 @@ inline int smax_for(int64_t s) {
 inline bool use_tables(int64_t s) { return smax_for(s) > 0; }
 inline int64_t tab_ld(int64_t k3, int smax) { return (k3 * smax + 15) / 16 * 16; }
 // K3c flat passes (B == 1): one wave of warps, partial slots per bucket
-constexpr int64_t K3C_FLAT_WARPS = 148 * 24;
+inline int64_t k3c_flat_warps() { return (int64_t)sm_count() * 24; }
 constexpr int64_t K3C_FLAT_PART = 256;  // bytes per (bucket, warp) partial, >= every pass's partial
-inline int64_t flat_cp_max(int64_t k3) { return (K3C_FLAT_WARPS * 65 / 64 + k3 - 1) / k3 + 3; }
+inline int64_t flat_cp_max(int64_t k3) { return (k3c_flat_warps() * 65 / 64 + k3 - 1) / k3 + 3; }
 int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s);
 int launch_lttb(LttbArgs a, int xdt, int ydt, int64_t s, cudaStream_t st);
 int64_t repair_scans_read();
@@ -180,9 +184,8 @@ int64_t repair_scans_read();
 // ---- fused batch kernel (fused_launch.cu) ----
 bool fused_ok(int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int ydt);
 int launch_fused(const FusedArgs& fa, int xdt, int ydt, cudaStream_t st);
-int sm_count();
 
-// ---- K2 + K3 of one series in one cooperative launch (k23_launch.cu) ----
+// ---- K2 + K3 of one series in one cooperative launch (k23.cuh, k23_launch.cu) ----
 bool k23_ok(int64_t B, int64_t k, int64_t n_out, int64_t r_ps);
 int64_t k23_ws();
 int launch_k23(K23Args a, int xdt, int ydt, int64_t r_ps, cudaStream_t st);

@@ -1,6 +1,7 @@
 // k23_launch.cu -- K23 (k23.cuh): compaction + LTTB of one series' preselected
 // points in one cooperative launch; the single-series minmaxlttb tail.
 #include "host.cuh"
+#include "k23.cuh"
 
 namespace mmh {
 

@@ -146,7 +146,7 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
       f.CP = cdiv(cdiv(L, k3), f.E) + 1;
       return f.CP <= flat_cp_max(k3);
     };
-    if (!plan(fl, K3C_FLAT_WARPS) || !plan(fl_c, K3C_FLAT_WARPS * 2 / 3)) return fail(MM_ERANGE, "K3c flat partial slots");
+    if (!plan(fl, k3c_flat_warps()) || !plan(fl_c, k3c_flat_warps() * 2 / 3)) return fail(MM_ERANGE, "K3c flat partial slots");
     // arrival counters of the three passes, the failed-certification count, the
     // flagged-bucket count and the fix/verify2 grid barrier: one memset
     fcnt = cv.take<unsigned>(3 * k3 + 3);
@@ -167,13 +167,19 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   a.cert_force = cforce;
   if (flat) {
     fl.cnt = fcnt;
+#ifdef MMLTTB_AB  // tuning build only: points in flight per lane (4: 43 vs 45 us at 8 on C2)
     if (flat_un(false) == 8) k_lttb_means_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
-    else k_lttb_means_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+    else
+#endif
+    k_lttb_means_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
   } else {
-    static const int64_t mnt = env_i64("MMLTTB_K3C_MEANS_NT", 256);
     const dim3 g((unsigned)k3, (unsigned)a.B);
+#ifdef MMLTTB_AB
+    static const int64_t mnt = env_i64("MMLTTB_K3C_MEANS_NT", 256);
     if (mnt == 128) k_lttb_means_approx<XT, YT, 128, 8><<<g, 128, 0, st>>>(a);
-    else k_lttb_means_approx<XT, YT, 256, 4><<<g, 256, 0, st>>>(a);
+    else
+#endif
+    k_lttb_means_approx<XT, YT, 256, 4><<<g, 256, 0, st>>>(a);
   }
   int rc = check_launch("k_lttb_means");
   if (rc) return rc;
@@ -186,24 +192,29 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
   if ((rc = launch_chain_scan<H>(a, st))) return rc;
   if (!flat && cudaMemsetAsync(a.fcount, 0, (size_t)a.B * sizeof(int), st) != cudaSuccess)
     return fail(MM_ECUDA, "memset");
-  static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);  // A/B knob (64: 30 vs 37.5 us at 256 on C2)
   if (flat) {
     fl.cnt = fcnt + 2 * k3;
+#ifdef MMLTTB_AB  // (8 in flight: 26 vs 29 us at 4 on C2)
     if (flat_un(true) == 4) k_lttb_verify_flat<XT, YT, 4><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
-    else k_lttb_verify_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
+    else
+#endif
+    k_lttb_verify_flat<XT, YT, 8><<<dim3(flat_grid, 1), 256, 0, st>>>(a, fl);
     if ((rc = check_launch("k_lttb_verify_flat"))) return rc;
     k_lttb_verify_fix<XT, YT, 256><<<dim3((unsigned)sm_count(), 1), 256, 0, st>>>(a, fl);
     if ((rc = check_launch("k_lttb_verify_fix"))) return rc;
   } else {
+#ifdef MMLTTB_AB  // (64 threads per bucket: 30 vs 37.5 us at 256 on C2)
+    static const int64_t vnt = env_i64("MMLTTB_K3C_VERIFY_NT", 64);
     if (vnt == 256) k_lttb_verify<XT, YT, 256><<<dim3((unsigned)k3, (unsigned)a.B), 256, 0, st>>>(a);
-    else k_lttb_verify<XT, YT, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
+    else
+#endif
+    k_lttb_verify<XT, YT, 64><<<dim3((unsigned)k3, (unsigned)a.B), 64, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_verify"))) return rc;
   }
   {
     k_lttb_verify2<XT, YT, 256><<<dim3((unsigned)sm_count(), (unsigned)a.B), 256, 0, st>>>(a);
     if ((rc = check_launch("k_lttb_verify2"))) return rc;
   }
-  static const int64_t rp = env_i64("MMLTTB_K3C_REPAIR_NT", 512);  // A/B knob (512: 22.1 vs 24.4 us at 1024 on C2)
   // chain state staged in shared memory when it fits (A/B knob MMLTTB_K3C_REPAIR_SMEM=0: global)
   static const bool rsm = env_i64("MMLTTB_K3C_REPAIR_SMEM", 1) != 0;
   constexpr int64_t RSMEM_MAX = 200 * 1024;
@@ -215,15 +226,20 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
     kern<<<(unsigned)a.B, 512, (size_t)rbytes, st>>>(a);
     return check_launch("k_lttb_repair_smem");
   }
+#ifdef MMLTTB_AB  // (512 threads: 22.1 vs 24.4 us at 1024 on C2)
+  static const int64_t rp = env_i64("MMLTTB_K3C_REPAIR_NT", 512);
   if (rp == 1024) k_lttb_repair<XT, YT, 1024><<<(unsigned)a.B, 1024, 0, st>>>(a);
-  else k_lttb_repair<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
+  else
+#endif
+  k_lttb_repair<XT, YT, 512><<<(unsigned)a.B, 512, 0, st>>>(a);
   return check_launch("k_lttb_repair");
 }
 
+// buckets of <= 64 points (lttb_small_x_*.cu)
 template <typename XT, typename YT>
-int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
+int launch_lttb_small_t(LttbArgs a, int64_t s, cudaStream_t st) {
   if (a.B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
-  if (use_tables(s)) {
+  {
     switch (smax_for(s)) {
       case 4: return launch_tables_jump<XT, YT, 4>(a, st);
       case 8: return launch_tables_jump<XT, YT, 8>(a, st);
@@ -232,13 +248,21 @@ int launch_lttb_t(LttbArgs a, int64_t s, cudaStream_t st) {
       default: return launch_tables_jump<XT, YT, 64>(a, st);
     }
   }
-  return launch_lttb_large<XT, YT, 16>(a, st);
 }
 
 template <typename XT>
-int launch_lttb_x(LttbArgs a, int ydt, int64_t s, cudaStream_t st) {
-  if (ydt == MM_F32) return launch_lttb_t<XT, float>(a, s, st);
-  if (ydt == MM_F64) return launch_lttb_t<XT, double>(a, s, st);
+int launch_lttb_small_x(LttbArgs a, int ydt, int64_t s, cudaStream_t st) {
+  if (ydt == MM_F32) return launch_lttb_small_t<XT, float>(a, s, st);
+  if (ydt == MM_F64) return launch_lttb_small_t<XT, double>(a, s, st);
+  return fail(MM_EINVAL, "y dtype");
+}
+
+// larger buckets: K3s / K3c (lttb_x_*.cu)
+template <typename XT>
+int launch_lttb_large_x(LttbArgs a, int ydt, cudaStream_t st) {
+  if (a.B > 65535) return fail(MM_ERANGE, "batch > 65535 series");
+  if (ydt == MM_F32) return launch_lttb_large<XT, float, 16>(a, st);
+  if (ydt == MM_F64) return launch_lttb_large<XT, double, 16>(a, st);
   return fail(MM_EINVAL, "y dtype");
 }
 

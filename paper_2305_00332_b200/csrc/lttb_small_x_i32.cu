@@ -1,0 +1,9 @@
+// lttb_small_x_i32.cu -- K3a launchers (LTTB buckets <= 64 points) for x = int
+// (a separate translation unit: the build compiles the K3 variants in parallel)
+#include "lttb_impl.cuh"
+
+namespace mmh {
+
+int launch_lttb_small_i32(LttbArgs a, int ydt, int64_t s, cudaStream_t st) { return launch_lttb_small_x<int>(a, ydt, s, st); }
+
+}  // namespace mmh

@@ -1,9 +1,14 @@
-// lttb_x_f64.cu -- K3 launchers for x = double (see lttb_impl.cuh)
+// lttb_x_f64.cu -- K3 launchers for x = double, buckets > 64 points (K3s / K3c; see lttb_impl.cuh)
 #include "lttb_impl.cuh"
 
 namespace mmh {
 
-int launch_lttb_f64(LttbArgs a, int ydt, int64_t s, cudaStream_t st) { return launch_lttb_x<double>(a, ydt, s, st); }
+int launch_lttb_small_f64(LttbArgs a, int ydt, int64_t s, cudaStream_t st);  // lttb_small_x_f64.cu
+
+int launch_lttb_f64(LttbArgs a, int ydt, int64_t s, cudaStream_t st) {
+  if (use_tables(s)) return launch_lttb_small_f64(a, ydt, s, st);
+  return launch_lttb_large_x<double>(a, ydt, st);
+}
 
 // k_lttb_repair's counter is a per-translation-unit device variable
 int64_t repair_scans_f64() {
