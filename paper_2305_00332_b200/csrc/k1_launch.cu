@@ -17,13 +17,19 @@ int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
         case 3: k_extrema_flat<float, 8, 1, 3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
         case 4: k_extrema_flat<float, 12, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
         case 5: k_extrema_flat<float, 16, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+        // register double-buffered rounds (round i+1's loads in flight while round i is reduced):
+        // C3 K1 77.1 us at 2 CTAs / SM, 81.8 us with 4-vector rounds at 3, vs 72.9 us; 1e9 611 / 658 vs 575 us
+        case 6: k_extrema_flat<float, 8, 3, 2, true><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+        case 7: k_extrema_flat<float, 4, 3, 3, true><<<(unsigned)blocks, 256, 0, st>>>(a); break;
         default: k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
       }
 #else
-      k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+      if (a.ticket) k_extrema_flat<float, 8, 3, 3, false, true><<<(unsigned)blocks, 256, 0, st>>>(a);
+      else k_extrema_flat<float, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
 #endif
     } else {
-      k_extrema_flat<double, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+      if (a.ticket) k_extrema_flat<double, 8, 3, 3, false, true><<<(unsigned)blocks, 256, 0, st>>>(a);
+      else k_extrema_flat<double, 8, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
     }
     return check_launch("k_extrema_flat");
   }

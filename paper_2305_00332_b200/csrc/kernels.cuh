@@ -158,7 +158,7 @@ __device__ __forceinline__ int64_t pbound(int64_t start, int64_t len, int64_t k,
 // vector improves the running extreme its raw 16 bytes are kept in
 // registers, so the exact element is recovered without re-reading memory (a
 // re-read would miss L2 on a long stream and cost extra DRAM traffic).
-template <typename T, int U, int LDV, int G, bool KEEPRAW = true>
+template <typename T, int U, int LDV, int G, bool KEEPRAW = true, bool PF = false>
 __device__ __forceinline__ void group_extrema(const T* y, int64_t lo, int64_t hi, int lane, typename YTr<T>::K& mn,
                                               int& omn, typename YTr<T>::K& mx, int& omx) {
   typedef YTr<T> Tr;
@@ -181,13 +181,14 @@ __device__ __forceinline__ void group_extrema(const T* y, int64_t lo, int64_t hi
     }
     const int nvec = (n - head) / Tr::VEC;
     const uint4* vp = reinterpret_cast<const uint4*>(base + head);
-    for (int v0 = 0; v0 < nvec; v0 += G * U) {
-      uint4 r[U];
+    auto ld_round = [&](uint4 (&r)[U], int v0) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * G + lane;
         if (v < nvec) r[u] = ld_stream<LDV>(vp + v);
       }
+    };
+    auto use_round = [&](const uint4 (&r)[U], int v0) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * G + lane;
@@ -200,6 +201,22 @@ __device__ __forceinline__ void group_extrema(const T* y, int64_t lo, int64_t hi
           if (vl < mn) { mn = vl; omn = head + v * Tr::VEC; vmn = true; if (KEEPRAW) rmn = r[u]; }
           if (vh > mx) { mx = vh; omx = head + v * Tr::VEC; vmx = true; if (KEEPRAW) rmx = r[u]; }
         }
+      }
+    };
+    if constexpr (PF) {  // register double buffer: round i+1's loads in flight while round i is reduced
+      uint4 ra[U], rb[U];
+      if (nvec > 0) ld_round(ra, 0);
+      for (int v0 = 0; v0 < nvec; v0 += 2 * G * U) {
+        if (v0 + G * U < nvec) ld_round(rb, v0 + G * U);
+        use_round(ra, v0);
+        if (v0 + 2 * G * U < nvec) ld_round(ra, v0 + 2 * G * U);
+        if (v0 + G * U < nvec) use_round(rb, v0 + G * U);
+      }
+    } else {
+      for (int v0 = 0; v0 < nvec; v0 += G * U) {
+        uint4 r[U];
+        ld_round(r, v0);
+        use_round(r, v0);
       }
     }
     if (!KEEPRAW) {  // short ranges read with normal L2 policy: the vectors are still cached
@@ -300,7 +317,7 @@ __device__ __forceinline__ void publish_partial(const ExArgs& a, int64_t bkt, in
 // does the same work (no last-wave tail); a range spanning bucket edges
 // publishes one partial per intersected bucket (slot = w - first warp of the
 // bucket), combined by the bucket's last-arriving warp.
-template <typename T, int U, int LDV>
+template <typename T, int U, int LDV, bool PF = false>
 __device__ __forceinline__ void flat_range(const ExArgs& a, int64_t w, int lane) {
   typedef YTr<T> Tr;
   typedef typename Tr::K K;
@@ -317,7 +334,7 @@ __device__ __forceinline__ void flat_range(const ExArgs& a, int64_t w, int lane)
     const int64_t lo = max(e0, blo), hi = min(e1, bhi);
     K mn, mx;
     int omn, omx;
-    group_extrema<T, U, LDV, 32>(y, lo, hi, lane, mn, omn, mx, omx);
+    group_extrema<T, U, LDV, 32, true, PF>(y, lo, hi, lane, mn, omn, mx, omx);
     const int64_t pmn = omn == INT_MAX ? INT64_MAX : lo + omn;
     const int64_t pmx = omx == INT_MAX ? INT64_MAX : lo + omx;
     const int64_t wf = (max(blo, E_lo) - E_lo) / a.E;
@@ -329,22 +346,22 @@ __device__ __forceinline__ void flat_range(const ExArgs& a, int64_t w, int lane)
   }
 }
 
-template <typename T, int U, int LDV, int MINB = 3>
+template <typename T, int U, int LDV, int MINB = 3, bool PF = false, bool DYN = false>
 __global__ void __launch_bounds__(256, MINB) k_extrema_flat(ExArgs a) {
   const int lane = threadIdx.x & 31;
-  if (a.ticket) {  // persistent warps take the next range until none is left (no single-wave tail)
+  if constexpr (DYN) {  // persistent warps take the next range until none is left (no single-wave tail)
     for (;;) {
       unsigned w = 0;
       if (lane == 0) w = atomicAdd(a.ticket, 1u);
       w = __shfl_sync(FULL, w, 0);
       if ((int64_t)w >= a.B * a.Ws) break;
-      flat_range<T, U, LDV>(a, (int64_t)w, lane);
+      flat_range<T, U, LDV, PF>(a, (int64_t)w, lane);
     }
     return;
   }
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= a.B * a.Ws) return;  // warp-uniform
-  flat_range<T, U, LDV>(a, w, lane);
+  flat_range<T, U, LDV, PF>(a, w, lane);
 }
 
 // One warp per (series, bucket, chunk).  Lanes stream 16-byte vectors
