@@ -83,17 +83,23 @@ __device__ __forceinline__ void spin_until_set(const unsigned* p, unsigned want)
     if (gtimer() - t0 > 2000000000ull) __trap();  // 2 s
   }
 }
-// grid-wide barrier i over the G co-resident CTAs: the last arriver releases
-// a flag the others poll (counter and flag on different lines)
+// grid-wide barrier i over the G co-resident CTAs: a release add on the
+// counter, then acquire polls of the counter itself (tight; the watchdog clock
+// is read every 1,024 polls).  A/B: MMLTTB_BARRIER_FLAG (host) selects the
+// earlier variant (last arriver releases a flag on another line).
 __device__ __forceinline__ void k3s_grid_sync(unsigned* sync, int i, unsigned G) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    unsigned* ctr = sync + 64 * i;
     __threadfence();
-    if (atomicAdd(sync + 64 * i, 1u) == G - 1) {
-      __threadfence();
-      st_rel(sync + 64 * i + 32, 1u);
-    } else {
-      spin_until_set(sync + 64 * i + 32, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    unsigned long long t0 = 0;
+    for (unsigned it = 1; ld_acq(ctr) < G; ++it) {
+      if ((it & 1023u) == 0) {
+        const unsigned long long t = gtimer();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 2000000000ull) __trap();  // 2 s
+      }
     }
   }
   __syncthreads();
