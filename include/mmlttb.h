@@ -74,6 +74,26 @@ int mmlttb_stage_timer_read(double *ms3, int64_t *calls);
 int mmlttb_trace(int enable);
 int64_t mmlttb_trace_read(char *buf, int64_t len);
 
+/* Deferred status word (non-finite y), for callers that keep their inputs on
+ * the device and do not want a host sync per call.  mmlttb_status_arm()
+ * returns a ticket >= 0 and arms this host thread: its next mmlttb_minmaxlttb
+ * / mmlttb_minmax_preselect / mmlttb_minmax / mmlttb_m4 call stores that
+ * call's status from the device into a pinned, device-mapped host slot (the
+ * single-series K23 launch does it from its own CTA 0; other paths add one
+ * 1-thread kernel after their last launch).  mmlttb_status_poll(ticket,
+ * block) returns 2 while the slot is not yet written (block = 0; block = 1
+ * synchronises the device first), else 1 if that call saw NaN/inf in y (the
+ * reference's NonFiniteValue, core.py:80-94) or 0 if not; MM_EINVAL if the
+ * armed call failed or the ticket was overwritten (the ring has 1024 slots).
+ * A call made while its stream is capturing a graph does not deliver a
+ * status (the slot then reads as clean).  mmlttb_status_ring()
+ * exposes the 1024-slot ring (host view) for callers that poll it directly:
+ * slot ticket % 1024 holds ((ticket + 1) << 3) | 4 * failed | 2 * captured | status bit
+ * once written. */
+int64_t mmlttb_status_arm(void);
+const volatile unsigned long long *mmlttb_status_ring(void);
+int mmlttb_status_poll(int64_t ticket, int block);
+
 /* Bytes of device workspace an operation needs for B series of N points. */
 int64_t mmlttb_workspace_bytes(int op, int64_t B, int64_t N, int64_t n_out, int64_t r_ps, int y_dtype);
 

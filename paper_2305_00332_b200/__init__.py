@@ -14,6 +14,7 @@ from .raster import Canvas, RasterImage, fit_canvas, rasterize, read_pgm, write_
 from .seriesio import read_series, write_series
 from .downsamplers import (
     Batch,
+    check_deferred,
     downsample,
     every_nth,
     lttb,
@@ -30,6 +31,7 @@ __all__ = [
     "Algorithm",
     "Batch",
     "Canvas",
+    "check_deferred",
     "ConvMask",
     "RasterImage",
     "conv_mask",

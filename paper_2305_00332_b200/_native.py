@@ -41,6 +41,9 @@ _SIGS = {
     "mmlttb_stage_timer_read": (_i32, [_p, _p]),
     "mmlttb_trace": (_i32, [_i32]),
     "mmlttb_trace_read": (_i64, [_p, _i64]),
+    "mmlttb_status_arm": (_i64, []),
+    "mmlttb_status_ring": (_p, []),
+    "mmlttb_status_poll": (_i32, [_i64, _i32]),
     "mmlttb_workspace_bytes": (_i64, [_i32, _i64, _i64, _i64, _i64, _i32]),
     "mmlttb_minmaxlttb": (_i32, [_p, _i32, _i64, _p, _i32, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _i64, _p]),
     "mmlttb_minmax_preselect": (_i32, [_p, _i32, _i64, _i64, _i64, _i64, _i64, _p, _i64, _p, _p, _i64, _p]),

@@ -145,6 +145,63 @@ int check_common(const void* y, int ydt, int64_t B, int64_t N, int64_t n_out) {
   return MM_OK;
 }
 
+// Deferred status: device-input callers learn of non-finite y (the
+// reference's NonFiniteValue) without a host sync.  mmlttb_status_arm()
+// hands out a slot of a pinned, device-mapped ring; the next status-producing
+// call of this host thread stores (tag | status bit) there from the device:
+// K23 (the single-series path) from its CTA 0 as part of the launch, every
+// other path with one 1-thread kernel after its last launch.
+constexpr int64_t STATUS_SLOTS = 1024;
+struct StatusRing {
+  std::mutex mu;
+  volatile unsigned long long* host = nullptr;
+};
+StatusRing g_status;
+struct StatusArm {
+  unsigned long long* slot = nullptr;  // device view of the armed slot
+  volatile unsigned long long* hslot = nullptr;  // host view
+  unsigned long long tag = 0;
+  bool consumed = false;
+};
+thread_local StatusArm g_arm;
+constexpr unsigned long long TAG_FAILED = 4;  // host-written: the armed call failed
+
+__global__ void k_status_mirror(const int* status, unsigned long long* slot, unsigned long long tag) {
+  *(volatile unsigned long long*)slot = tag | (unsigned long long)(*status & 1);
+}
+
+inline unsigned long long ticket_tag(int64_t t) { return (unsigned long long)(t + 1) << 3; }
+
+// Runs one status-producing entry; delivers the armed slot afterwards.
+constexpr unsigned long long TAG_SKIPPED = 2;  // host-written: the armed call was captured into a graph
+template <class F>
+int with_status_slot(const void* workspace, void* stream, F&& f) {
+  if (g_arm.slot) {  // a captured launch must not bake the slot into the graph
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      *g_arm.hslot = g_arm.tag | TAG_SKIPPED;
+      g_arm = StatusArm{};
+    }
+  }
+  int rc = f();
+  StatusArm a = g_arm;
+  g_arm = StatusArm{};
+  if (!a.slot) return rc;
+  if (rc == MM_OK && !a.consumed) {
+    k_status_mirror<<<1, 1, 0, (cudaStream_t)stream>>>((const int*)workspace, a.slot, a.tag);
+    rc = check_launch("k_status_mirror");
+  }
+  if (rc != MM_OK) *a.hslot = a.tag | TAG_FAILED;
+  return rc;
+}
+unsigned long long* status_slot_take(unsigned long long* tag) {
+  if (!g_arm.slot || g_arm.consumed) return nullptr;
+  g_arm.consumed = true;
+  *tag = g_arm.tag;
+  return g_arm.slot;
+}
+
 }  // namespace mmh
 
 
@@ -173,6 +230,52 @@ int64_t mmlttb_trace_read(char* buf, int64_t len) {
   }
   g_trace.clear();
   return n;
+}
+
+const volatile unsigned long long* mmlttb_status_ring(void) {
+  std::lock_guard<std::mutex> lk(g_status.mu);
+  if (!g_status.host) {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, STATUS_SLOTS * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) !=
+        cudaSuccess) {
+      fail(MM_ECUDA, "status ring: cudaHostAlloc");
+      return nullptr;
+    }
+    memset(h, 0, STATUS_SLOTS * sizeof(unsigned long long));
+    g_status.host = (volatile unsigned long long*)h;
+  }
+  return g_status.host;
+}
+
+int64_t mmlttb_status_arm(void) {
+  static std::atomic<int64_t> next{0};
+  if (!g_status.host && !mmlttb_status_ring()) return MM_ECUDA;
+  const int64_t t = next.fetch_add(1);
+  const int64_t s = t % STATUS_SLOTS;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, (void*)(g_status.host + s), 0) != cudaSuccess)
+    return fail(MM_ECUDA, "status_arm: cudaHostGetDevicePointer");
+  g_status.host[s] = 0;
+  g_arm = StatusArm{(unsigned long long*)d, g_status.host + s, ticket_tag(t), false};
+  return t;
+}
+
+int mmlttb_status_poll(int64_t ticket, int block) {
+  if (ticket < 0 || !g_status.host) return fail(MM_EINVAL, "bad status ticket");
+  const unsigned long long tag = ticket_tag(ticket);
+  volatile unsigned long long* p = g_status.host + ticket % STATUS_SLOTS;
+  unsigned long long v = *p;
+  if ((v & ~7ull) != tag && block) {  // the slot is written by the call's last kernel
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(MM_ECUDA, "status_poll: %s",
+                                                            cudaGetErrorString(cudaGetLastError()));
+    v = *p;
+  }
+  if ((v & ~7ull) != tag) {
+    if (v != 0 && (v & ~7ull) > tag) return fail(MM_EINVAL, "expired status ticket");
+    return block ? fail(MM_EINVAL, "status ticket never delivered") : 2;
+  }
+  if (v & TAG_FAILED) return fail(MM_EINVAL, "the armed call failed");
+  return (int)(v & 1);  // (TAG_SKIPPED: no status, reads as 0)
 }
 
 int mmlttb_stage_timer(int enable) {
@@ -281,17 +384,21 @@ static int minmax_impl(const void* y, int ydt, int64_t y_ld, int64_t B, int64_t 
 
 int mmlttb_minmax(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int64_t* out,
                   int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream) {
-  return batch_chunks(B, [&](int64_t s0, int64_t b) {
-    return minmax_impl(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, 0, 0, out + s0 * n_out,
-                       out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, (cudaStream_t)stream);
+  return with_status_slot(workspace, stream, [&] {
+    return batch_chunks(B, [&](int64_t s0, int64_t b) {
+      return minmax_impl(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, 0, 0, out + s0 * n_out,
+                         out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, (cudaStream_t)stream);
+    });
   });
 }
 
 int mmlttb_m4(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out, int64_t* out,
               int64_t* out_count, void* workspace, int64_t workspace_bytes, void* stream) {
-  return batch_chunks(B, [&](int64_t s0, int64_t b) {
-    return minmax_impl(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, 1, 0, out + s0 * n_out,
-                       out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, (cudaStream_t)stream);
+  return with_status_slot(workspace, stream, [&] {
+    return batch_chunks(B, [&](int64_t s0, int64_t b) {
+      return minmax_impl(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, 1, 0, out + s0 * n_out,
+                         out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, (cudaStream_t)stream);
+    });
   });
 }
 
@@ -339,6 +446,7 @@ static int minmaxlttb_entry(const void* x, int x_dtype, int64_t x_ld, const void
     K23Args ka{};
     ka.ext = ea.ext; ka.cnt8 = ea.cnt8; ka.k = k; ka.N = N; ka.n_out = n_out;
     ka.x = x; ka.y = y; ka.pre = pre; ka.px = px; ka.py = py; ka.out = out; ka.status = status;
+    ka.mirror = status_slot_take(&ka.mtag);
     ka.sync = zr;
     ka.stat = k23s;
     if ((rc = launch_k23(ka, x_dtype, y_dtype, r_ps, st))) return rc;
@@ -432,19 +540,23 @@ static int lttb_entry(const void* x, int x_dtype, int64_t x_ld, const void* y, i
 int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B, int64_t N, int64_t n_out,
                             int64_t r_ps, int64_t* out, int64_t out_ld, int64_t* out_count, void* workspace,
                             int64_t workspace_bytes, void* stream) {
-  return batch_chunks(B, [&](int64_t s0, int64_t b) {
-    return preselect_entry(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, r_ps, out + s0 * out_ld,
-                           out_ld, out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, stream);
+  return with_status_slot(workspace, stream, [&] {
+    return batch_chunks(B, [&](int64_t s0, int64_t b) {
+      return preselect_entry(elem_off(y, y_dtype, s0 * y_ld), y_dtype, y_ld, b, N, n_out, r_ps, out + s0 * out_ld,
+                             out_ld, out_count ? out_count + s0 : nullptr, workspace, workspace_bytes, stream);
+    });
   });
 }
 
 int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
                       int64_t N, int64_t n_out, int64_t r_ps, int64_t* out, int64_t* out_count, void* workspace,
                       int64_t workspace_bytes, void* stream) {
-  return batch_chunks(B, [&](int64_t s0, int64_t b) {
-    return minmaxlttb_entry(elem_off(x, x_dtype, s0 * x_ld), x_dtype, x_ld, elem_off(y, y_dtype, s0 * y_ld), y_dtype,
-                            y_ld, b, N, n_out, r_ps, out + s0 * n_out, out_count ? out_count + s0 : nullptr,
-                            workspace, workspace_bytes, stream);
+  return with_status_slot(workspace, stream, [&] {
+    return batch_chunks(B, [&](int64_t s0, int64_t b) {
+      return minmaxlttb_entry(elem_off(x, x_dtype, s0 * x_ld), x_dtype, x_ld, elem_off(y, y_dtype, s0 * y_ld), y_dtype,
+                              y_ld, b, N, n_out, r_ps, out + s0 * n_out, out_count ? out_count + s0 : nullptr,
+                              workspace, workspace_bytes, stream);
+    });
   });
 }
 

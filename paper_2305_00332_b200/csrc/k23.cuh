@@ -37,6 +37,8 @@ struct K23Args {
   int64_t* pre; double* px; double* py;  // preselected set (global index, x, y as f64)
   int64_t* out;
   int* status;                // bit 0: non-finite y seen (overwritten, not ORed: no zeroing needed)
+  unsigned long long* mirror; // optional mapped-host slot: gets mtag | status (mmlttb_status_arm)
+  unsigned long long mtag;
   unsigned* sync;             // K23_STAT words: barriers 0, 1 (K3S layout: counter 64 i, flag 64 i + 32), zeroed per call
   unsigned* stat;             // [G] per-CTA status bits (written every call)
   unsigned char* agg;         // [G][32] aggregate maps
@@ -258,7 +260,10 @@ __global__ void __launch_bounds__(K23_NT) k_k23(K23Args a) {
     unsigned st = 0;
     for (int q = lane; q < (int)G; q += 32) st |= __ldcg(a.stat + q);
     st = __reduce_or_sync(FULL, st);
-    if (lane == 0) *a.status = (int)st;
+    if (lane == 0) {
+      *a.status = (int)st;
+      if (a.mirror) *(volatile unsigned long long*)a.mirror = a.mtag | (st & 1u);
+    }
   }
   // ---------------- B: LTTB tables of buckets [B0, B1) ----------------
   const int64_t B0 = (int64_t)c * k3 / G, B1 = (int64_t)(c + 1) * k3 / G;

@@ -20,7 +20,10 @@ is always bucket-parallel and byte-identical to the sequential reference.
 """
 from __future__ import annotations
 
+import collections
 import contextlib
+import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -40,8 +43,67 @@ from .errors import (
 
 __all__ = [
     "every_nth", "minmax", "m4", "lttb", "minmax_preselect", "minmaxlttb", "run_parallel", "downsample",
-    "Batch",
+    "Batch", "check_deferred",
 ]
+
+
+# ----------------------------------------------- deferred status words ------
+# Device-input calls (validate=None) do not sync: their status word (bit 0 =
+# non-finite y) is stored by the device into a pinned host slot armed before
+# the call (mmlttb_status_arm) and checked by later calls or check_deferred().
+_DEFERRED: collections.deque = collections.deque()
+_DEFERRED_LOCK = threading.Lock()
+_DEFERRED_MAX = 512  # the C ring holds 1024 outstanding tickets
+
+
+_RING = None  # numpy view of the library's pinned status ring (mmlttb_status_ring)
+_RING_SLOTS = 1024
+
+
+def _ring():
+    global _RING
+    if _RING is None:
+        p = N.lib().mmlttb_status_ring()
+        if not p:
+            N.check(N.MM_ECUDA, "status_ring")
+        _RING = np.ctypeslib.as_array((ctypes.c_uint64 * _RING_SLOTS).from_address(p))
+    return _RING
+
+
+def _poll_landed(block: bool) -> None:
+    """Retire the deferred tickets whose slots the device has written, in order."""
+    ring = _ring()
+    with _DEFERRED_LOCK:
+        while _DEFERRED:
+            t, what = _DEFERRED[0]
+            v = int(ring[t % _RING_SLOTS])
+            if (v >> 3) != t + 1:
+                if not block:
+                    return
+                rc = N.lib().mmlttb_status_poll(t, 1)  # synchronises the device
+                if rc < 0:
+                    _DEFERRED.popleft()
+                    N.check(rc, "status_poll")
+                v = rc
+            _DEFERRED.popleft()
+            if v & 1:
+                raise NonFiniteValue(f"series contains NaN or infinite values (in an earlier {what} call on device "
+                                     "inputs; pass validate=True to check before returning)")
+
+
+def check_deferred(block: bool = True) -> None:
+    """Raise ``NonFiniteValue`` if an earlier device-input call saw NaN/inf in ``y``.
+
+    The reference rejects non-finite values when the series is built
+    (core.py:80-94).  Calls on CUDA tensors with ``validate=None`` do not
+    synchronise for that check; the device writes their status word into a
+    pinned host slot, every later call polls the slots already written
+    (non-blocking) and raises for the oldest failing call.
+    ``check_deferred()`` synchronises the device for the outstanding slots
+    (``block=True``) and raises the same way.
+    """
+    if _DEFERRED:
+        _poll_landed(block)
 
 
 # --------------------------------------------------------------- inputs ----
@@ -73,6 +135,8 @@ class Batch:
     def ready(self):
         if self._ready:
             return self
+        if _DEFERRED:
+            _poll_landed(False)
         y, x = self._y_in, self._x_in
         dev = N.require_cuda(y.device if not self.host else self._dev_in)
         yt = torch.as_tensor(y) if not isinstance(y, torch.Tensor) else y
@@ -124,9 +188,30 @@ class Batch:
             raise NonFiniteValue("series contains NaN or infinite values")
         raise NonMonotonicX("xs must be sorted in non-decreasing order")
 
-    def post_check(self, ws: torch.Tensor) -> None:
-        """Raise the reference's NonFiniteValue from the kernels' status word."""
-        if self.validate is False or (self.validate is None and not self.host):
+    def arm(self) -> int | None:
+        """Device inputs with validate=None: arm a deferred status slot for the
+        next library call (mmlttb_status_arm); None when the check is synchronous
+        (host inputs, validate=True) or skipped (validate=False).  A call under
+        graph capture delivers no status (the library checks)."""
+        if self.validate is not None or self.host:
+            return None
+        t = N.lib().mmlttb_status_arm()
+        if t < 0:
+            N.check(t, "status_arm")
+        return t
+
+    def post_check(self, ws: torch.Tensor, what: str, ticket: int | None) -> None:
+        """Raise the reference's NonFiniteValue from the kernels' status word.
+
+        Host inputs (and validate=True) read it now; device inputs with
+        validate=None get it back through the armed slot (``check_deferred``),
+        so the call stays free of host syncs; validate=False skips it."""
+        if ticket is not None:
+            _DEFERRED.append((ticket, what))  # (deque.append is atomic)
+            if len(_DEFERRED) > _DEFERRED_MAX:
+                check_deferred(block=True)
+            return
+        if self.validate is False or not (self.host or self.validate):
             return
         if int(ws[:4].view(torch.int32)[0].item()) & 1:
             raise NonFiniteValue("series contains NaN or infinite values")
@@ -245,6 +330,7 @@ def _minmax_like(b, n_out, op: str, force: bool = False):
     cnt = torch.empty(b.B, dtype=torch.int64, device=b.device)
     with _ctx(b):
         st = N.stream_ptr(b.device)
+        ticket = b.arm()
         if force:  # r_ps == 1 through the fused entry (downsamplers.py:164-179)
             wsb = N.lib().mmlttb_workspace_bytes(N.OP_MINMAXLTTB, b.B, b.n, n_out, 1, ydt)
             ws = N.workspace(wsb, b.device, b.n)
@@ -256,7 +342,7 @@ def _minmax_like(b, n_out, op: str, force: bool = False):
             ws = N.workspace(wsb, b.device, b.n)
             N.check(fn(b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out, out.data_ptr(), cnt.data_ptr(), ws.data_ptr(),
                        wsb, st), op, b.n)
-    b.post_check(ws)
+    b.post_check(ws, "minmaxlttb" if force else op, ticket)
     return _counted(b, out, cnt)
 
 
@@ -341,10 +427,11 @@ def minmax_preselect(series, n_out, r_ps, parallel=False, *args, **kw):
     with _ctx(b):
         wsb = N.lib().mmlttb_workspace_bytes(N.OP_PRESELECT, b.B, b.n, n_out, r_ps, ydt)
         ws = N.workspace(wsb, b.device, b.n)
+        ticket = b.arm()
         N.check(N.lib().mmlttb_minmax_preselect(b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out, r_ps, out.data_ptr(),
                                                 cap, cnt.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(b.device)),
                 "minmax_preselect", b.n)
-    b.post_check(ws)
+    b.post_check(ws, "minmax_preselect", ticket)
     return _counted(b, out, cnt)
 
 
@@ -356,10 +443,11 @@ def _minmaxlttb_batch(b, n_out: int, r_ps: int):
         st = N.stream_ptr(b.device)
         wsb = N.workspace_bytes(N.OP_MINMAXLTTB, b.B, b.n, n_out, r_ps, ydt)
         ws = N.stream_workspace(wsb, b.device, st, b.n)
+        ticket = b.arm()
         N.check(N.lib().mmlttb_minmaxlttb(N.ptr(b.x), xdt, b.x_ld, b.y.data_ptr(), ydt, b.n, b.B, b.n, n_out,
                                           r_ps, out.data_ptr(), None, ws.data_ptr(), wsb, st),
                 "minmaxlttb", b.n)
-    b.post_check(ws)
+    b.post_check(ws, "minmaxlttb", ticket)
     return b.ret(out)
 
 

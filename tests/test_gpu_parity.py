@@ -4,6 +4,7 @@ Index-exact equality everywhere (integer/index work; LTTB fp64 parity is
 bit-exact by construction, so the tolerance is zero).  Inputs are the
 seeded recipes of tests/recipes.py and tests/fuzzgen.py.
 """
+import ctypes
 import gzip
 import json
 import os
@@ -455,8 +456,8 @@ def test_fused_batch_path(r, ydt, xkind):
 
 def test_flat_api_nonfinite_parity():
     """The reference rejects NaN/inf at TimeSeries construction (core.py:89-90);
-    the flat form detects it for free from the K1 keys (host inputs) or on
-    request (validate=True for device inputs)."""
+    the flat form detects it for free from the K1 keys: at once for host inputs
+    and validate=True, deferred (no host sync) for device inputs."""
     n = 50_000
     x = np.arange(n, dtype=np.int64)
     for ydt in (np.float32, np.float64):
@@ -479,9 +480,36 @@ def test_flat_api_nonfinite_parity():
     xd[100] = 5
     with pytest.raises(errors.NonMonotonicX):
         mm.minmaxlttb(xd, torch.randn(n, device=DEV), 100, minmax_ratio=4, validate=True)
-    # device inputs without validate: no sync, no raise (garbage in, indices out)
-    out = mm.minmaxlttb(torch.from_numpy(x).to(DEV), yb, 100, minmax_ratio=4)
+    # device inputs without validate: no host sync in the call; the status
+    # word comes back asynchronously and the error surfaces at check_deferred()
+    mm.check_deferred()
+    xd = torch.from_numpy(x).to(DEV)
+    out = mm.minmaxlttb(xd, yb, 100, minmax_ratio=4)
     assert out.shape == (4, 100)
+    with pytest.raises(errors.NonFiniteValue, match="earlier minmaxlttb call"):
+        mm.check_deferred()
+    mm.check_deferred()  # reported once
+    # ... or at the next call, once the copy has landed
+    for fn, args in ((mm.minmaxlttb, (100,)), (mm.minmax, (100,)), (mm.m4, (100,)), (mm.minmax_preselect, (100, 4))):
+        fn(xd, yb, *args)
+        torch.cuda.synchronize()
+        with pytest.raises(errors.NonFiniteValue):
+            mm.minmaxlttb(xd, torch.randn(n, device=DEV), 100, minmax_ratio=4)
+        mm.check_deferred()
+    # clean device calls, validate=False and graph-free streams never raise
+    for _ in range(3):
+        mm.minmaxlttb(xd, torch.randn(4, n, device=DEV), 100, minmax_ratio=4)
+    mm.minmaxlttb(xd, yb, 100, minmax_ratio=4, validate=False)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        mm.minmaxlttb(xd, torch.randn(n, device=DEV), 100, minmax_ratio=4)
+    mm.check_deferred()
+    # the 1e8-class single-series path (K23 / cooperative) reports it too
+    yl = torch.randn(3_000_000, device=DEV)
+    yl[2_999_999] = float("inf")
+    mm.minmaxlttb(torch.arange(3_000_000, device=DEV), yl, 2000, minmax_ratio=4)
+    with pytest.raises(errors.NonFiniteValue):
+        mm.check_deferred()
 
 
 def test_plan_graph_replay():
@@ -514,6 +542,83 @@ def _minmaxlttb_abi(x, y2d, n, n_out, r, y_ld):
     NN.check(L.mmlttb_minmaxlttb(x.data_ptr(), NN.DTYPE_CODE[x.dtype], 0, y2d.data_ptr(), ydt, y_ld, B, n, n_out, r,
                                  out.data_ptr(), None, ws.data_ptr(), wsb, NN.stream_ptr(DEV)), "minmaxlttb", n)
     return out.cpu().numpy()
+
+
+def test_status_arm_abi():
+    """mmlttb_status_arm / _poll through the C ABI: every status-producing path
+    (K23 single series, fused batch, per-stage batch, preselect, minmax/m4)
+    delivers its NaN bit to the armed slot; a failed call and a captured call
+    are reported as such; unarmed calls leave the ring alone."""
+    from paper_2305_00332_b200 import _native as NN
+    L = NN.lib()
+    st = NN.stream_ptr(DEV)
+
+    def run(op, y, n_out, r=4, B=1, n=None):
+        n = n or y.shape[-1]
+        x = torch.arange(n, device=DEV)
+        ydt = NN.DTYPE_CODE[y.dtype]
+        code = {"mml": NN.OP_MINMAXLTTB, "pre": NN.OP_PRESELECT, "mm": NN.OP_MINMAX, "m4": NN.OP_M4}[op]
+        wsb = L.mmlttb_workspace_bytes(code, B, n, n_out, r if op in ("mml", "pre") else 0, ydt)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=DEV)
+        cap = 2 + 2 * (n_out - 2) * (r // 2)
+        out = torch.empty((B, max(n_out, cap)), dtype=torch.int64, device=DEV)
+        cnt = torch.empty(B, dtype=torch.int64, device=DEV)
+        if op == "mml":
+            return L.mmlttb_minmaxlttb(x.data_ptr(), NN.DTYPE_CODE[x.dtype], 0, y.data_ptr(), ydt, n, B, n, n_out, r,
+                                       out.data_ptr(), None, ws.data_ptr(), wsb, st)
+        if op == "pre":
+            return L.mmlttb_minmax_preselect(y.data_ptr(), ydt, n, B, n, n_out, r, out.data_ptr(), out.shape[1],
+                                             cnt.data_ptr(), ws.data_ptr(), wsb, st)
+        fn = L.mmlttb_minmax if op == "mm" else L.mmlttb_m4
+        return fn(y.data_ptr(), ydt, n, B, n, n_out, out.data_ptr(), cnt.data_ptr(), ws.data_ptr(), wsb, st)
+
+    cases = [("mml", 1, 3_000_000, 2000), ("mml", 1, 200_000, 1000), ("mml", 200, 20_000, 100),
+             ("mml", 3, 400_000, 40), ("pre", 2, 100_000, 100), ("mm", 2, 100_000, 100), ("m4", 2, 100_000, 100)]
+    for op, B, n, n_out in cases:
+        for bad in (False, True):
+            y = torch.randn(B, n, device=DEV)
+            if bad:
+                y[B - 1, n // 3] = float("nan")
+            t = L.mmlttb_status_arm()
+            assert t >= 0
+            assert run(op, y, n_out, B=B, n=n) == 0
+            assert L.mmlttb_status_poll(t, 1) == int(bad), (op, B, n, bad)
+    # a failing call marks its slot failed
+    t = L.mmlttb_status_arm()
+    y = torch.randn(1, 1000, device=DEV)
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=DEV)
+    assert L.mmlttb_minmaxlttb(None, 2, 0, y.data_ptr(), 9, 1000, 1, 1000, 100, 4, ws.data_ptr(), None,
+                               ws.data_ptr(), 1 << 20, st) != 0  # bad y dtype
+    assert L.mmlttb_status_poll(t, 0) < 0
+    # unarmed calls do not write the ring
+    ring = np.ctypeslib.as_array((ctypes.c_uint64 * 1024).from_address(L.mmlttb_status_ring()))
+    before = ring.copy()
+    run("mml", torch.randn(1, 3_000_000, device=DEV), 2000)
+    torch.cuda.synchronize()
+    assert np.array_equal(ring, before)
+    # a captured call delivers "no status" and its graph never touches the slot
+    y = torch.randn(1, 200_000, device=DEV)
+    y[0, 5] = float("inf")
+    run("mml", y, 1000)  # warm the workspace paths before capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x = torch.arange(200_000, device=DEV)
+        wsb = L.mmlttb_workspace_bytes(NN.OP_MINMAXLTTB, 1, 200_000, 1000, 4, 0)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=DEV)
+        out = torch.empty((1, 1000), dtype=torch.int64, device=DEV)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            t = L.mmlttb_status_arm()
+            rc = L.mmlttb_minmaxlttb(x.data_ptr(), NN.DTYPE_CODE[x.dtype], 0, y.data_ptr(), 0, 200_000, 1, 200_000,
+                                     1000, 4, out.data_ptr(), None, ws.data_ptr(), wsb, s.cuda_stream)
+    assert rc == 0
+    assert L.mmlttb_status_poll(t, 1) == 0
+    slot = int(ring[t % 1024])
+    g.replay()
+    torch.cuda.synchronize()
+    assert int(ring[t % 1024]) == slot
 
 
 @pytest.mark.parametrize("ydt,n,pad,r,n_out", [(np.float32, 20_000, 0, 4, 257), (np.float32, 20_003, 1, 2, 300),
