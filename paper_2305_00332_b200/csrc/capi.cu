@@ -6,6 +6,7 @@
 // stream.  Nothing here synchronises the host.  The kernel launchers live in
 // k1_launch.cu / lttb_launch.cu / fused_launch.cu / post_launch.cu (host.cuh).
 #include "host.cuh"
+#include <chrono>
 #include "k23.cuh"
 #include "raster.cuh"
 
@@ -42,6 +43,21 @@ int check_launch(const char* what) {
   if (e != cudaSuccess) return fail(MM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   return MM_OK;
 }
+
+// Host-path profiler (tuning builds only: -DMMLTTB_HOSTPROF via MMLTTB_NVCC_EXTRA):
+// cumulative host time between marks of the single-series minmaxlttb path.
+#ifdef MMLTTB_HOSTPROF
+thread_local double g_hp_acc[16];
+thread_local std::chrono::high_resolution_clock::time_point g_hp_t;
+#define HP_MARK(i)                                                                              \
+  do {                                                                                          \
+    auto _n = std::chrono::high_resolution_clock::now();                                        \
+    if (i > 0) g_hp_acc[i] += std::chrono::duration<double, std::micro>(_n - g_hp_t).count();  \
+    g_hp_t = _n;                                                                                \
+  } while (0)
+#else
+#define HP_MARK(i) do {} while (0)
+#endif
 
 // Stage timer: events recorded on the caller's stream at K1|K2|K3 boundaries
 // of the fused entries (bench.py reads per-kernel device time from these).
@@ -421,6 +437,7 @@ static int minmaxlttb_entry(const void* x, int x_dtype, int64_t x_ld, const void
   const bool k23 = k23_ok(B, k, n_out, r_ps);
   const ExPlan p = plan_extrema(B * k, S, y_dtype, B, true, k23 && dyn_chunk_elems() > 0);
   const int64_t cap = 2 + 2 * k;
+  HP_MARK(2);
   if (k23) {
     // one series: K1, then K2 + K3 in one cooperative launch (K23).  The only
     // zeroing of the call is one memset over K23's barrier words and K1's
@@ -438,10 +455,14 @@ static int minmaxlttb_entry(const void* x, int x_dtype, int64_t x_ld, const void
     ea.arrivals = zr + K23_STAT;  // (the carve_ex slot stays unused)
     ea.arrivals_zeroed = 1;
     ea.ticket = p.E > 0 && dyn_chunk_elems() > 0 ? zr + 128 : nullptr;  // (zeroed with the rest)
+    HP_MARK(3);
     if (cudaMemsetAsync(zr, 0, (size_t)(K23_STAT + B * k) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "memset");
+    HP_MARK(4);
     stage_mark(st, 0);
+    HP_MARK(5);
     if ((rc = launch_extrema(ea, y_dtype, st))) return rc;
+    HP_MARK(6);
     stage_mark(st, 1);
     K23Args ka{};
     ka.ext = ea.ext; ka.cnt8 = ea.cnt8; ka.k = k; ka.N = N; ka.n_out = n_out;
@@ -449,9 +470,12 @@ static int minmaxlttb_entry(const void* x, int x_dtype, int64_t x_ld, const void
     ka.mirror = status_slot_take(&ka.mtag);
     ka.sync = zr;
     ka.stat = k23s;
+    HP_MARK(7);
     if ((rc = launch_k23(ka, x_dtype, y_dtype, r_ps, st))) return rc;
+    HP_MARK(8);
     stage_mark(st, 2);
     stage_mark(st, 3);
+    HP_MARK(9);
     if (out_count) {
       k_fill<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(out_count, B, n_out);
       return check_launch("k_fill");
@@ -548,10 +572,19 @@ int mmlttb_minmax_preselect(const void* y, int y_dtype, int64_t y_ld, int64_t B,
   });
 }
 
+#ifdef MMLTTB_HOSTPROF
+int mmlttb_hostprof_read(double* acc) {
+  for (int i = 0; i < 16; ++i) { acc[i] = g_hp_acc[i]; g_hp_acc[i] = 0; }
+  return MM_OK;
+}
+#endif
+
 int mmlttb_minmaxlttb(const void* x, int x_dtype, int64_t x_ld, const void* y, int y_dtype, int64_t y_ld, int64_t B,
                       int64_t N, int64_t n_out, int64_t r_ps, int64_t* out, int64_t* out_count, void* workspace,
                       int64_t workspace_bytes, void* stream) {
+  HP_MARK(0);
   return with_status_slot(workspace, stream, [&] {
+    HP_MARK(1);
     return batch_chunks(B, [&](int64_t s0, int64_t b) {
       return minmaxlttb_entry(elem_off(x, x_dtype, s0 * x_ld), x_dtype, x_ld, elem_off(y, y_dtype, s0 * y_ld), y_dtype,
                               y_ld, b, N, n_out, r_ps, out + s0 * n_out, out_count ? out_count + s0 : nullptr,

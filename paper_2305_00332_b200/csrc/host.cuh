@@ -58,6 +58,7 @@ struct Carve {
 struct ExPlan {
   int64_t C, chunk, Cmax;
   int64_t E = 0, Ws = 0, CP = 0;  // flat mode (E > 0): elements/warp, warps/series, partial stride
+  int64_t nt = 0;                 // tile mode (nt > 0): tile CTAs per series, partial stride CP
 };
 
 // Chunks per bucket: enough warps for ~4 waves over 148 SMs x 32 resident
@@ -100,6 +101,24 @@ inline ExPlan plan_extrema(int64_t buckets_total, int64_t max_bucket, int ydt, i
   // flat split above this many elements per bucket (A/B knob MMLTTB_K1_FLAT_MIN; measured on
   // C3 r=32, 3,128-point buckets: 8-lane groups 117.6 us vs flat 126.8 us per call)
   static const int64_t flat_min = env_i64("MMLTTB_K1_FLAT_MIN", SMALL_BUCKET);
+#ifdef MMLTTB_AB
+  // tile mode (k1_tiles.cuh, tuning build only): 32 KB tile CTAs, sub-buckets of >= one
+  // warp's elements (1,024 float32 / 512 float64); knobs MMLTTB_K1_TILES=1,
+  // MMLTTB_K1_TILES_MIN (smallest sub-bucket, elements).  Measured and not adopted:
+  // C3 K1 124 vs 72 us, 1e9 1.10 vs 0.58 ms -- issue-bound (profiles/r02/k1_tiles.md)
+  static const bool tiles_on = env_i64("MMLTTB_K1_TILES", 0) != 0;
+  static const int64_t tiles_min = env_i64("MMLTTB_K1_TILES_MIN", SMALL_BUCKET);
+  const int64_t vec = ydt == MM_F32 ? 4 : 2, tile_el = 2048 * vec;
+  if (closed_form && B > 0 && tiles_on && max_bucket - 1 >= std::max<int64_t>(tiles_min, 256 * vec)) {
+    const int64_t nb = nb_;
+    p.nt = std::max<int64_t>(1, cdiv(nb * max_bucket / vec, 2048));
+    p.CP = cdiv(max_bucket, tile_el) + 2;
+    p.C = 1;
+    p.chunk = max_bucket;
+    p.Cmax = p.CP;
+    return p;
+  }
+#endif
   if (closed_form && B > 0 && max_bucket > flat_min && flat_warps > 0) {
     const int64_t nb = nb_;
     p.Ws = std::max<int64_t>(1, flat_warps / B);
@@ -129,6 +148,7 @@ inline bool carve_ex(Carve& cv, int64_t nbt, const ExPlan& p, ExArgs& a) {
   a.E = p.E;
   a.Ws = p.Ws;
   a.CP = p.CP;
+  a.nt = p.nt;
   a.ext = cv.take<Ext>(nbt);
   a.cnt8 = cv.take<unsigned char>(nbt);
   a.part = nullptr;

@@ -1,9 +1,42 @@
 // k1_launch.cu -- K1 (sub-bucket extrema) launch: kernel variant dispatch.
 #include "host.cuh"
+#ifdef MMLTTB_AB
+#include "k1_tiles.cuh"
+#endif
 
 namespace mmh {
 
 int launch_extrema(const ExArgs& a, int ydt, cudaStream_t st) {
+#ifdef MMLTTB_AB
+  if (a.nt > 0) {  // tile mode (k1_tiles.cuh; tuning build only)
+    const int64_t blocks = a.B * a.nt;
+    if (blocks > 0x7fffffffLL) return fail(MM_ERANGE, "extrema grid too large");
+    ExArgs t = a;
+    t.e_lo = t.start + (t.b0 * t.len) / t.k;  // pbound (core.py:173)
+    t.e_hi = t.start + ((t.b0 + t.nb) * t.len) / t.k;
+    t.rlen = 1.0 / (double)t.len;
+    t.rk = 1.0 / (double)t.k;
+    if (ydt == MM_F32)
+      k_extrema_tiles<float><<<(unsigned)blocks, K1T_NT, 0, st>>>(t);
+    else
+      k_extrema_tiles<double><<<(unsigned)blocks, K1T_NT, 0, st>>>(t);
+    if (int rc = check_launch("k_extrema_tiles")) return rc;
+    // the multi-tile sub-buckets' partials: a programmatic dependent launch
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)cdiv(a.B * a.nb, 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = ydt == MM_F32 ? cudaLaunchKernelEx(&cfg, k_extrema_tiles_combine<float>, t)
+                                        : cudaLaunchKernelEx(&cfg, k_extrema_tiles_combine<double>, t);
+    if (e != cudaSuccess) { (void)cudaGetLastError(); return fail(MM_ECUDA, "k_extrema_tiles_combine: %s", cudaGetErrorString(e)); }
+    return check_launch("k_extrema_tiles_combine");
+  }
+#endif
   if (a.E > 0) {  // flat split
     if (!a.arrivals_zeroed && cudaMemsetAsync(a.arrivals, 0, (size_t)(a.B * a.nb) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "cudaMemsetAsync(arrivals)");

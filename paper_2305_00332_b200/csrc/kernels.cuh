@@ -131,6 +131,10 @@ struct ExArgs {
   int arrivals_zeroed;     // the caller zeroed `arrivals` (merged into its own memset)
   unsigned* ticket;        // flat mode: chunk ticket (zeroed per call) -> persistent warps take
                            // chunks dynamically; null: one static range per warp
+  int64_t nt;              // tile mode (k1_tiles.cuh, nt > 0): tile CTAs per series (an upper
+                           // bound), partial stride CP
+  int64_t e_lo, e_hi;      // tile mode: [pbound(b0), pbound(b0 + nb)) (set by the launcher)
+  double rlen, rk;         // tile mode: 1/len, 1/k (division-free bucket arithmetic)
 };
 
 struct Ext {

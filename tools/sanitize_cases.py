@@ -208,6 +208,34 @@ def case_p2p():
             _eq(S.lttb_merged(oi, ox, oy, om, n_out, r), want, f"p2p epoch {epoch} rank {g}")
 
 
+def _k3s(seed, n=1_600_000, n_out=1400):
+    # >= 8 x SMs large buckets: the one-launch K3s path (grid barrier, neighbour flags,
+    # aggregate maps, deviation walks)
+    x = np.arange(n, dtype=np.int64)
+    y = _rw(n, seed, np.float64)
+    got = mm.lttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out)
+    _eq(got, O.lttb(x, y, n_out), "k3s")
+
+
+def case_k3s():
+    _k3s(16)
+
+
+def case_k3s_miss():
+    os.environ["MMLTTB_K3C_CAND_CAP"] = "1"  # every candidate set misses: 4a/4b walks + repair walk
+    _k3s(17)
+
+
+def case_k23():
+    # one series, cooperative K2+K3a (grid barriers, per-CTA status slots), C1 and C3 shapes
+    for n, n_out, r, dt in ((1_000_000, 1000, 4, np.float64), (4_000_000, 2000, 4, np.float32),
+                            (4_000_000, 2000, 32, np.float32)):
+        x = np.arange(n, dtype=np.int64)
+        y = _rw(n, 18, dt)
+        got = mm.minmaxlttb(torch.from_numpy(x).to(DEV), torch.from_numpy(y).to(DEV), n_out, minmax_ratio=r)
+        _eq(got, O.minmaxlttb(x, y.astype(np.float64), n_out, r), f"k23 n={n} r={r}")
+
+
 def case_raster():
     n = 5_000
     x = np.arange(n, dtype=np.float64)
