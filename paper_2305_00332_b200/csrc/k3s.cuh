@@ -47,6 +47,14 @@ constexpr int K3S_D = K3S_DIRS;
 constexpr int K3S_H = K3S_D <= 8 ? 16 : 32;  // candidate slots per bucket (table width: 16 or 32)
 constexpr int K3S_U = 8;             // loads in flight per lane per array
 constexpr int K3S_GMAX = 1024;       // CTA bound for the workspace
+// Group summaries (round 2, "pruned" phases 2 and 4a): phase 1 also publishes the
+// y range of every GROUP of a bucket -- 2^s consecutive warp-wide 16-byte vector
+// loads (64 f64 / 128 f32 points for s = 0; s grows so that a bucket has at most
+// K3S_GCAP groups).  The candidate search and the verification then bound each
+// group's best value from its (y range) x (index range) box and only scan the
+// few groups that can matter: on C2 ~5 of 79 groups per bucket for the
+// candidates and ~1.1 for the verification (a random walk without spikes: 5.1 / 1.14).
+constexpr int K3S_GCAP = 128;
 
 struct K3sArgs {
   int G;                 // CTAs, all co-resident (cooperative launch)
@@ -55,6 +63,7 @@ struct K3sArgs {
   unsigned char* agg;    // [G][16] aggregate maps
   double2* cpt;          // [k3][16] candidate points (x, y)
   unsigned long long* prof;  // optional [G][8] %globaltimer stamps per phase (tools), or null
+  int2* gmeta;           // [k3][K3S_GCAP] per-group (min, max) y keys written by phase 1, or null (no pruning)
 };
 // sync words: barrier i = counter at 64 i, release flag at 64 i + 32 (separate
 // 128-byte lines: the pollers never delay the arrivals); done counter, fcount
@@ -103,6 +112,22 @@ __device__ __forceinline__ void k3s_grid_sync(unsigned* sync, int i, unsigned G)
     }
   }
   __syncthreads();
+}
+
+// tool counters (prof mode): [0] verify calls, [1] violations, [2] shared high word, [3] cert fails,
+// [4] full-path picks, [5] flagged buckets, [6] 4b picks, [7] repair picks, [8] pruned candidate searches,
+// [9] their surviving groups, [10] plain candidate searches, [11] pruned verifications, [12] their
+// surviving groups, [13] plain verifications (one warp)
+__device__ unsigned long long* g_k3s_cnt;
+__device__ __forceinline__ void k3s_count(int i) {
+  if (g_k3s_cnt && (threadIdx.x & 31) == 0 && ((threadIdx.x >> 5) == 0 || i < 0)) atomicAdd(g_k3s_cnt + (i < 0 ? -i : i), 1ull);
+}
+// tool timeline of one warp (CTA 70, warp 0): slots 32..63
+__device__ __forceinline__ void k3s_dbg(int i) {
+  if (g_k3s_cnt && blockIdx.x == 70 && threadIdx.x == 0) g_k3s_cnt[32 + i] = gtimer();
+}
+__device__ __forceinline__ void k3s_cnt_add(int i, int v) {  // (every warp's lane 0)
+  if (g_k3s_cnt && (threadIdx.x & 31) == 0) atomicAdd(g_k3s_cnt + i, (unsigned long long)v);
 }
 
 // float -> int32 key with the same order (IEEE total order)
@@ -168,6 +193,16 @@ __device__ __forceinline__ VWin vwin(int64_t lo, int64_t hi) {
   if (w.vf * EV >= hi) w.nt = 0;  // no full vector: the head covers everything
   return w;
 }
+// group geometry of a window: nl warp-loads (32 vectors each), 2^s warp-loads per group, ng groups
+struct GGeo { int s, ng; int64_t nl; };
+__device__ __forceinline__ GGeo ggeo(const VWin& w) {
+  GGeo g;
+  g.nl = (w.vl - w.vf + 31) >> 5;
+  g.s = 0;
+  while (((g.nl + (1LL << g.s) - 1) >> g.s) > K3S_GCAP) ++g.s;
+  g.ng = (int)((g.nl + (1LL << g.s) - 1) >> g.s);
+  return g;
+}
 // element index handled by `lane` in the head / tail step (or -1)
 __device__ __forceinline__ int64_t vwin_edge(const VWin& w, int64_t lo, int lane) {
   if (lane < w.nh) return lo + lane;
@@ -179,8 +214,11 @@ __device__ __forceinline__ int64_t vwin_edge(const VWin& w, int64_t lo, int lane
 // this lane's UV vectors of round g (r[u] = vector v0 + 32u) of which the
 // first cnt are in range (cnt == UV in every round but the last, which the
 // compiler specialises; out-of-range slots repeat vector v0).
-template <int UV, bool STREAM, bool PREFETCH, typename F>
-__device__ __forceinline__ void vrounds(const uint4* base, const VWin& w, int L, int NL, F&& body) {
+// ALLTAIL: every lane runs the body of the last (partial) round, with cnt = 0
+// where it has no vector left (bodies with warp-wide operations).
+struct NoMid { __device__ __forceinline__ void operator()() const {} };
+template <int UV, bool STREAM, bool PREFETCH, bool ALLTAIL = false, typename F, typename MID = NoMid>
+__device__ __forceinline__ void vrounds(const uint4* base, const VWin& w, int L, int NL, F&& body, MID&& mid = NoMid{}) {
   const int64_t nfull = (w.vl - w.vf) / ((int64_t)NL * UV);
   int64_t v0 = w.vf + L;
   const uint4* p = base + v0;
@@ -194,6 +232,7 @@ __device__ __forceinline__ void vrounds(const uint4* base, const VWin& w, int L,
     for (; g < nfull; ++g, v0 += step, p += step) {
       uint4 r[UV];
       ld(r, p);
+      mid();  // (work that overlaps the loads' latency)
       body(r, v0, UV, g);
     }
   } else {
@@ -215,11 +254,13 @@ __device__ __forceinline__ void vrounds(const uint4* base, const VWin& w, int L,
       p += step;
     }
   }
-  if (v0 < w.vl) {
-    const int cnt = (int)((w.vl - v0 + NL - 1) / NL);
+  if (ALLTAIL ? (v0 - L < w.vl) : (v0 < w.vl)) {
+    const int cnt = v0 < w.vl ? (int)((w.vl - v0 + NL - 1) / NL) : 0;
+    if (ALLTAIL && cnt == 0) p = base + w.vf;  // (a valid address; the values are not used)
     uint4 r[UV];
 #pragma unroll
     for (int u = 0; u < UV; ++u) r[u] = STREAM ? __ldcs(p + (u < cnt ? NL * u : 0)) : p[u < cnt ? NL * u : 0];
+    mid();
     body(r, v0, cnt, g);
   }
 }
@@ -228,9 +269,9 @@ __device__ __forceinline__ void vrounds(const uint4* base, const VWin& w, int L,
 // One warp: statistics of bucket b = [lo, hi), published for every later phase.
 template <typename XT, typename YT>
 __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const YT* ys, int64_t b, int64_t lo,
-                                          int64_t hi, int64_t m) {
+                                          int64_t hi, int64_t m, int2* gm) {
   constexpr int EY = Vec<YT>::EV, EX = Vec<XT>::EV;
-  constexpr int UY = 16 / EY, UX = 16 / EX;  // 16 elements per lane per round
+  constexpr int UY = 8, UX = 16 / EX;  // y: 8 vectors per lane per round (quad mapping below); x: 16 elements
   const int lane = threadIdx.x & 31;
   const int64_t k3 = a.n_out - 2;
   const int n = (int)(hi - lo);
@@ -258,41 +299,87 @@ __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const
       return hy ^ ((hy >> 31) & 0x7fffffff);
     }
   };
-  auto yel = [&](YT y) {
-    sy = __dadd_rn(sy, (double)y);
-    const int k = ykey(y);
-    kmn = min(kmn, k);
-    kmx = max(kmx, k);
-  };
+  // The y pass uses a QUAD mapping: in a round of 32 UY vectors, the LS = 32 / UY
+  // lanes of set bi = lane / LS load the 32 consecutive vectors of block bi
+  // (instruction u: vector 4u + lane % 4 of the lane's 4 UY-vector quad --
+  // 64 contiguous bytes per 4 lanes, whole sectors), so a block's (min, max) keys
+  // are a lane-local reduction plus log2(LS) shuffle steps per round: the
+  // group summaries (2^s blocks per group) cost no warp-wide reduction per load.
+  const VWin wy = vwin<YT>(lo, hi);
+  const GGeo gg = ggeo(wy);
   {
-    const VWin w = vwin<YT>(lo, hi);
-    const int64_t e = vwin_edge(w, lo, lane);
+    const int64_t e = vwin_edge(wy, lo, lane);
     if (e >= 0) {
-      yel(ys[e]);
-      if (try_y) ly = min(ly, lsb_exp((double)ys[e]));
+      const YT y = ys[e];
+      sy = __dadd_rn(sy, (double)y);
+      const int k = ykey(y);
+      kmn = min(kmn, k);
+      kmx = max(kmx, k);
+      if (try_y) ly = min(ly, lsb_exp((double)y));
     }
-    auto body = [&](const uint4 (&r)[UY], int64_t, int cnt, int) {
+    constexpr int LS = 32 / UY;              // lanes per block: 4 (f64) / 8 (f32)
+    constexpr int LGU = UY == 8 ? 3 : 2;     // log2(UY)
+    const uint4* yv = reinterpret_cast<const uint4*>(ys);
+    const int64_t voff = (int64_t)(lane >> 2) * (4 * UY) + (lane & 3);
+    int amn = INT_MAX, amx = INT_MIN;        // groups spanning rounds (s > LGU)
+    auto run = [&](auto lsb_tag) {
+      constexpr bool LSB = decltype(lsb_tag)::value;
+      int g = 0;
+      for (int64_t vr = wy.vf; vr < wy.vl; vr += 32 * UY, ++g) {  // (warp-uniform)
+        const int64_t v0 = vr + voff;
+        uint4 r[UY];
+        const bool full = vr + 32 * UY <= wy.vl;
+        if (full) {
 #pragma unroll
-      for (int u = 0; u < UY; ++u)
-        if (u < cnt) {
+          for (int u = 0; u < UY; ++u) r[u] = yv[v0 + 4 * u];
+        } else {
 #pragma unroll
-          for (int q = 0; q < EY; ++q) yel(Vec<YT>::get(r[u], q));
+          for (int u = 0; u < UY; ++u) r[u] = v0 + 4 * u < wy.vl ? yv[v0 + 4 * u] : make_uint4(0, 0, 0, 0);
         }
-    };
-    auto body_lsb = [&](const uint4 (&r)[UY], int64_t, int cnt, int) {
+        int vmn = INT_MAX, vmx = INT_MIN;
 #pragma unroll
-      for (int u = 0; u < UY; ++u)
-        if (u < cnt) {
+        for (int u = 0; u < UY; ++u) {
+          if (full || v0 + 4 * u < wy.vl) {
 #pragma unroll
-          for (int q = 0; q < EY; ++q) {
-            const YT y = Vec<YT>::get(r[u], q);
-            yel(y);
-            ly = min(ly, lsb_exp((double)y));
+            for (int q = 0; q < EY; ++q) {
+              const YT y = Vec<YT>::get(r[u], q);
+              sy = __dadd_rn(sy, (double)y);
+              const int k = ykey(y);
+              vmn = min(vmn, k);
+              vmx = max(vmx, k);
+              if (LSB) ly = min(ly, lsb_exp((double)y));
+            }
           }
         }
+        kmn = min(kmn, vmn);
+        kmx = max(kmx, vmx);
+        if (gm) {
+          // block (LS lanes), then the group's 2^s blocks (or the whole round)
+          const int steps = 5 - LGU + min(gg.s, LGU);  // shuffle steps: 1 << i, i < steps
+#pragma unroll
+          for (int i = 0; i < 5; ++i) {
+            if (i < steps) {
+              vmn = min(vmn, __shfl_xor_sync(FULL, vmn, 1 << i));
+              vmx = max(vmx, __shfl_xor_sync(FULL, vmx, 1 << i));
+            }
+          }
+          if (gg.s <= LGU) {
+            const int gi = (int)(((int64_t)g * UY + lane / LS) >> gg.s);
+            if ((lane & ((LS << gg.s) - 1)) == 0 && gi < gg.ng) gm[gi] = make_int2(vmn, vmx);
+          } else {
+            amn = min(amn, vmn);
+            amx = max(amx, vmx);
+            const int64_t nblk = (int64_t)(g + 1) * UY;  // blocks so far
+            if ((nblk & ((1LL << gg.s) - 1)) == 0 || vr + 32 * UY >= wy.vl) {
+              if (lane == 0) gm[(int)((nblk - 1) >> gg.s)] = make_int2(amn, amx);
+              amn = INT_MAX; amx = INT_MIN;
+            }
+          }
+        }
+      }
     };
-    if (try_y) vrounds<UY, false, false>(reinterpret_cast<const uint4*>(ys), w, lane, 32, body_lsb);
-    else vrounds<UY, false, false>(reinterpret_cast<const uint4*>(ys), w, lane, 32, body);
+    if (try_y) run(std::true_type{});
+    else run(std::false_type{});
   }
   // ---- x: affine test (integral: XOR-accumulated difference from the formula),
   // float x: bit compare + sum, keys, lowest bits
@@ -400,7 +487,74 @@ __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const
   }
 }
 
+// (min, max) y keys of a group (phase 1) -> rigorous bounds y0 <= every y <= y1 of
+// the group (f32: exact; f64: the high words' granules); NaN keys give NaN bounds
+template <typename YT>
+__device__ __forceinline__ void gkey_bounds(int2 k, double& y0, double& y1) {
+  if constexpr (sizeof(YT) == 4) {
+    y0 = (double)__int_as_float(k.x ^ ((k.x >> 31) & 0x7fffffff));
+    y1 = (double)__int_as_float(k.y ^ ((k.y >> 31) & 0x7fffffff));
+  } else {
+    y0 = dkey_inv((long long)k.x * 4294967296LL);
+    y1 = dkey_inv((long long)k.y * 4294967296LL + 4294967295LL);
+  }
+}
+__device__ __forceinline__ int hw_abs(double v) { return (int)((__double_as_longlong(v) >> 32) & 0x7fffffff); }
+
 // ---------------------------------------------------------------- phase 2 --
+// winner lane + group of each of the 2D extremes (warp REDUX on order keys):
+// lane e < 2D keeps extreme e's winner
+__device__ __forceinline__ void k3s_winners(const float (&vmax)[K3S_D], const float (&vmin)[K3S_D], const int (&gmax)[K3S_D],
+                                            const int (&gmin)[K3S_D], int& my_g, int& my_l, int& my_key) {
+  constexpr int D = K3S_D;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int e = 0; e < 2 * D; ++e) {
+    const int k = e >> 1;
+    const int key = (e & 1) ? fkey(-vmin[k]) : fkey(vmax[k]);
+    const int wk = __reduce_max_sync(FULL, key);
+    const int wl = __ffs(__ballot_sync(FULL, key == wk)) - 1;
+    const int wg = __shfl_sync(FULL, (e & 1) ? gmin[k] : gmax[k], wl);
+    if (lane == e) { my_g = wg; my_l = wl; my_key = wk; }
+  }
+}
+
+// lanes' resolved candidate positions `off` (or -1) -> bucket b's sorted,
+// de-duplicated candidate set (positions + points)
+template <typename XT, typename YT>
+__device__ __forceinline__ void k3s_cand_finish(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
+                                                int64_t lo, int64_t off) {
+  constexpr int H = K3S_H;
+  const int lane = threadIdx.x & 31;
+  int o32 = off < 0 ? INT_MAX : (int)(off - lo);
+  // sort the <= 2D offsets across the warp (bitonic), de-duplicate, cap
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int o = __shfl_xor_sync(FULL, o32, j);
+      const bool up = ((lane & k) == 0);
+      const bool lower = (lane & j) == 0;
+      o32 = (lower == up) ? min(o32, o) : max(o32, o);
+    }
+  }
+  const int prev = __shfl_up_sync(FULL, o32, 1);
+  const bool keep = o32 != INT_MAX && (lane == 0 || prev != o32);
+  const unsigned km = __ballot_sync(FULL, keep);
+  const int rank = __popc(km & ((1u << lane) - 1));
+  const int cap = a.cand_cap > 0 && a.cand_cap < H ? a.cand_cap : H;
+  const int cw = max(1, min(__popc(km), cap));
+  if (keep && rank < cap) {
+    const int64_t p = lo + o32;
+    a.cand[b * H + rank] = p;
+    ka.cpt[b * H + rank] = make_double2(to_f64(xs, p), to_f64(ys, p));
+  }
+  if (lane == 0) {
+    if (km == 0) { a.cand[b * H] = lo; ka.cpt[b * H] = make_double2(to_f64(xs, lo), to_f64(ys, lo)); }
+    a.cand_cnt[b] = cw;
+  }
+}
+
 // One warp: direction candidates of bucket b = [lo, hi).  D slopes lambda over
 // the anchor box (bucket b-1's ranges, or point 0) and the mean c = means[b];
 // per slope the argmax and argmin of Y + lambda*T (T: index offset for affine
@@ -471,17 +625,8 @@ __device__ __forceinline__ void k3s_cand_t(const LttbArgs& a, const K3sArgs& ka,
       if (val < vmin[k]) { vmin[k] = val; gmin[k] = ng; }
     }
   }
-  // winner lane + group of each of the 2D extremes (warp REDUX on order keys)
   int my_g = -1, my_l = 0, my_key = 0;  // lane e < 2D keeps extreme e's winner
-#pragma unroll
-  for (int e = 0; e < 2 * D; ++e) {
-    const int k = e >> 1;
-    const int key = (e & 1) ? fkey(-vmin[k]) : fkey(vmax[k]);
-    const int wk = __reduce_max_sync(FULL, key);
-    const int wl = __ffs(__ballot_sync(FULL, key == wk)) - 1;
-    const int wg = __shfl_sync(FULL, (e & 1) ? gmin[k] : gmax[k], wl);
-    if (lane == e) { my_g = wg; my_l = wl; my_key = wk; }
-  }
+  k3s_winners(vmax, vmin, gmax, gmin, my_g, my_l, my_key);
   // lanes 0..2D-1 resolve their extreme's group to its first point (parallel re-reads)
   int64_t off = -1;
   if (lane < 2 * D && my_g >= 0) {
@@ -513,39 +658,184 @@ __device__ __forceinline__ void k3s_cand_t(const LttbArgs& a, const K3sArgs& ka,
       }
     }
   }
-  int o32 = off < 0 ? INT_MAX : (int)(off - lo);
-  // sort the <= 2D offsets across the warp (bitonic), de-duplicate, cap
+  k3s_cand_finish<XT, YT>(a, ka, xs, ys, b, lo, off);
+}
+
+// Pruned candidates (affine x; group summaries of phase 1).  For slope lambda
+// a group with y range [ymn, ymx] and index offsets [t0, t1] holds a value of
+// Y + lambda T of at least ymx + min(lambda t0, lambda t1) and none above
+// ymx + max(lambda t0, lambda t1): only groups whose upper bound reaches the
+// best lower bound of any group (likewise for the minima) can hold the
+// slope's extreme.  The union of those groups over the D slopes (C2: ~5 of 79)
+// is staged in shared memory as (Y, T) pairs, and lane l searches slope l % 16
+// over half of the staged points (both extremes), so no winner resolution is
+// needed: T is the exact index offset (buckets below 2^24 points).  Compact
+// code on purpose (rolled loops): a warp runs this once per bucket, and
+// straight-line code of that length is bound by instruction fetch.  A heuristic
+// like the plain search (phase 4 makes the result exact); returns false when
+// the plain search should run instead.
+constexpr int K3S_STAGE = 512;  // staged points per warp and chunk (float2 each)
+template <typename XT, typename YT>
+__device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
+                                             int64_t lo, int64_t hi, float lmin, float lmax, unsigned char* slist,
+                                             float2* stage) {
+  constexpr int D = K3S_D, NI = K3S_GCAP / 32;
+  constexpr int EV = Vec<YT>::EV, CW = K3S_STAGE / (32 * EV);  // warp-loads per chunk
+  static_assert(D == 16, "lane l searches slope l % 16");
+  const int lane = threadIdx.x & 31;
+  k3s_dbg(1);
+  const VWin w = vwin<YT>(lo, hi);
+  if (hi - lo >= (1 << 24)) return false;  // (T must be exact in f32)
+  const GGeo gg = ggeo(w);
+  if (gg.ng == 0) return false;
+  const int2* gm = ka.gmeta + b * K3S_GCAP;
+  const uint4* yv = reinterpret_cast<const uint4*>(ys);
+  // this lane's groups: y bounds (outer and inner) and index offsets
+  float yxh[NI], yxl[NI], ynh[NI], ynl[NI], t0[NI], t1[NI];
 #pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const int o = __shfl_xor_sync(FULL, o32, j);
-      const bool up = ((lane & k) == 0);
-      const bool lower = (lane & j) == 0;
-      o32 = (lower == up) ? min(o32, o) : max(o32, o);
+  for (int i = 0; i < NI; ++i) {
+    const int gi = lane + 32 * i;
+    yxh[i] = yxl[i] = -INFINITY; ynh[i] = ynl[i] = INFINITY; t0[i] = t1[i] = 0.f;
+    if (gi < gg.ng) {
+      const int2 k = __ldcg(gm + gi);
+      if constexpr (sizeof(YT) == 4) {
+        yxh[i] = yxl[i] = __int_as_float(k.y ^ ((k.y >> 31) & 0x7fffffff));
+        ynh[i] = ynl[i] = __int_as_float(k.x ^ ((k.x >> 31) & 0x7fffffff));
+      } else {
+        yxh[i] = __double2float_ru(dkey_inv((long long)k.y * 4294967296LL + 4294967295LL));
+        yxl[i] = __double2float_rd(dkey_inv((long long)k.y * 4294967296LL));
+        ynl[i] = __double2float_rd(dkey_inv((long long)k.x * 4294967296LL));
+        ynh[i] = __double2float_ru(dkey_inv((long long)k.x * 4294967296LL + 4294967295LL));
+      }
+      const int64_t v0g = w.vf + ((int64_t)gi << (gg.s + 5)), v1g = min((int64_t)w.vl, (int64_t)(v0g + (32LL << gg.s)));
+      t0[i] = (float)(v0g * EV - lo);
+      t1[i] = (float)(v1g * EV - 1 - lo);
     }
   }
-  const int prev = __shfl_up_sync(FULL, o32, 1);
-  const bool keep = o32 != INT_MAX && (lane == 0 || prev != o32);
-  const unsigned km = __ballot_sync(FULL, keep);
-  const int rank = __popc(km & ((1u << lane) - 1));
-  const int cap = a.cand_cap > 0 && a.cand_cap < H ? a.cand_cap : H;
-  const int cw = max(1, min(__popc(km), cap));
-  if (keep && rank < cap) {
-    const int64_t p = lo + o32;
-    a.cand[b * H + rank] = p;
-    ka.cpt[b * H + rank] = make_double2(to_f64(xs, p), to_f64(ys, p));
+  k3s_dbg(2);
+  const float tspan = (float)(hi - lo), dl = (lmax - lmin) * (1.f / (float)(D - 1));
+  bool sv[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) sv[i] = false;
+#pragma unroll 2
+  for (int k = 0; k < D; ++k) {
+    const float l = fmaf(dl, (float)k, lmin);
+    float bl = -INFINITY, bs = INFINITY;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const float p0 = l * t0[i], p1 = l * t1[i];
+      bl = fmaxf(bl, yxl[i] + fminf(p0, p1));   // a value of at least this exists
+      bs = fminf(bs, ynh[i] + fmaxf(p0, p1));   // a value of at most this exists
+    }
+    const int kx = __reduce_max_sync(FULL, fkey(bl)), kn = __reduce_max_sync(FULL, fkey(-bs));
+    const float tx = __int_as_float(kx ^ ((kx >> 31) & 0x7fffffff)), tn = -__int_as_float(kn ^ ((kn >> 31) & 0x7fffffff));
+    const float sl = 2e-6f * (fabsf(l) * tspan);
+    const float thx = tx - (sl + 2e-6f * fabsf(tx)), thn = tn + (sl + 2e-6f * fabsf(tn));
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const float p0 = l * t0[i], p1 = l * t1[i];
+      sv[i] = sv[i] || (yxh[i] + fmaxf(p0, p1) >= thx) || (ynl[i] + fminf(p0, p1) <= thn);
+    }
   }
-  if (lane == 0) {
-    if (km == 0) { a.cand[b * H] = lo; ka.cpt[b * H] = make_double2(to_f64(xs, lo), to_f64(ys, lo)); }
-    a.cand_cnt[b] = cw;
+  k3s_dbg(3);
+  int nsurv = 0;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const unsigned wd = __ballot_sync(FULL, sv[i]);
+    if (sv[i]) slist[nsurv + __popc(wd & ((1u << lane) - 1u))] = (unsigned char)(lane + 32 * i);
+    nsurv += __popc(wd);
   }
+  __syncwarp();
+  const int64_t nun = (int64_t)nsurv << gg.s;  // warp-loads to scan
+  if (nsurv == 0 || nun * 2 > gg.nl) return false;
+  k3s_cnt_add(8, 1);
+  k3s_cnt_add(9, nsurv);
+  // lane l: the 4 slopes 4 (l % 4) .. + 3 (8 independent running extremes)
+  // over the staged float4s (2 points each) l / 4, l / 4 + 8, ...
+  const int sq = lane & 3, ps = lane >> 2;
+  float lk[4], bmax[4], bmin[4], tmax[4], tmin[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    lk[j] = fmaf(dl, (float)(4 * sq + j), lmin);
+    bmax[j] = -INFINITY; bmin[j] = INFINITY; tmax[j] = -1.f; tmin[j] = -1.f;
+  }
+  auto search = [&](int np) {  // np: staged points, a multiple of 2
+    __syncwarp();
+    const float4* s4 = reinterpret_cast<const float4*>(stage);
+#pragma unroll 1
+    for (int i = ps; i < np / 2; i += 8) {
+      const float4 v = s4[i];  // two (Y, T) points
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float a0 = fmaf(lk[j], v.y, v.x), a1 = fmaf(lk[j], v.w, v.z);
+        if (a0 > bmax[j]) { bmax[j] = a0; tmax[j] = v.y; }
+        if (a0 < bmin[j]) { bmin[j] = a0; tmin[j] = v.y; }
+        if (a1 > bmax[j]) { bmax[j] = a1; tmax[j] = v.w; }
+        if (a1 < bmin[j]) { bmin[j] = a1; tmin[j] = v.w; }
+      }
+    }
+    __syncwarp();
+  };
+  {  // head / tail elements (NaN: an empty slot, never wins)
+    const int64_t ej = vwin_edge(w, lo, lane);
+    stage[lane] = ej >= 0 ? make_float2((float)ys[ej], (float)(ej - lo)) : make_float2(NAN, 0.f);
+    if (__any_sync(FULL, ej >= 0)) search(32);
+  }
+  k3s_dbg(4);
+  const int smask = (1 << gg.s) - 1;
+#pragma unroll 1
+  for (int64_t q0 = 0; q0 < nun; q0 += CW) {
+    uint4 r[CW];
+    int64_t vs[CW];
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
+      vs[u] = -1;
+      if (q0 + u < nun) {
+        const int64_t q = q0 + u;
+        const int64_t v = w.vf + 32 * ((((int64_t)slist[q >> gg.s]) << gg.s) + (q & smask)) + lane;
+        if (v < w.vl) vs[u] = v;
+      }
+      r[u] = vs[u] >= 0 ? yv[vs[u]] : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
+      const float tb = (float)(vs[u] * EV - lo);
+#pragma unroll
+      for (int e = 0; e < EV; ++e)
+        stage[(u * 32 + lane) * EV + e] = vs[u] >= 0 ? make_float2((float)Vec<YT>::get(r[u], e), tb + (float)e) : make_float2(NAN, 0.f);
+    }
+    search((int)min((int64_t)CW, nun - q0) * 32 * EV);
+  }
+  k3s_dbg(5);
+  // merge the 8 point subsets (lanes with equal l % 4); lane l then reports
+  // extreme l / 4 of its 4 slopes x 2 sides
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float obx = __shfl_xor_sync(FULL, bmax[j], o), otx = __shfl_xor_sync(FULL, tmax[j], o);
+      const float obn = __shfl_xor_sync(FULL, bmin[j], o), otn = __shfl_xor_sync(FULL, tmin[j], o);
+      if (obx > bmax[j]) { bmax[j] = obx; tmax[j] = otx; }
+      if (obn < bmin[j]) { bmin[j] = obn; tmin[j] = otn; }
+    }
+  }
+  float tw = tmax[0];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    tw = ps == 2 * j ? tmax[j] : tw;
+    tw = ps == 2 * j + 1 ? tmin[j] : tw;
+  }
+  const int64_t off = tw >= 0.f ? lo + (int64_t)tw : -1;
+  k3s_cand_finish<XT, YT>(a, ka, xs, ys, b, lo, off);
+  k3s_dbg(6);
+  return true;
 }
 
 template <typename XT, typename YT>
 __device__ __forceinline__ void k3s_cand(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
-                                         int64_t lo, int64_t hi) {
+                                         int64_t lo, int64_t hi, unsigned char* slist, float2* stage) {
   constexpr int D = K3S_D;
+  k3s_dbg(0);
   double bx0, bx1, by0, by1;
   if (b == 0) {
     bx0 = bx1 = to_f64(xs, 0);
@@ -575,9 +865,11 @@ __device__ __forceinline__ void k3s_cand(const LttbArgs& a, const K3sArgs& ka, c
     lmin = fmin(lmin, l);
     lmax = fmax(lmax, l);
   }
+  if (aff && ka.gmeta && k3s_cand_pruned<XT, YT>(a, ka, xs, ys, b, lo, hi, (float)lmin, (float)lmax, slist, stage)) return;
   float lam[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) lam[k] = (float)(lmin + (lmax - lmin) * ((double)k / (double)(D - 1)));
+  k3s_cnt_add(10, 1);
   if (aff) k3s_cand_t<XT, YT, true>(a, ka, xs, ys, b, lo, hi, lam, 0.0);
   else k3s_cand_t<XT, YT, false>(a, ka, xs, ys, b, lo, hi, lam, elem_f64(xs[lo]));
 }
@@ -591,6 +883,7 @@ static __device__ __noinline__ void k3s_table(const LttbArgs& a, const K3sArgs& 
   constexpr int H = K3S_H, PL = 32 / H == 2 ? 2 : 1;  // lanes per anchor
   constexpr int QL = H / PL;                           // candidates per lane
   const int lane = threadIdx.x & 31;
+  k3s_dbg(8);
   const int p = lane / PL, q0 = (lane % PL) * QL;
   int na = 1;
   double ax = x0, ay = y0;
@@ -619,6 +912,7 @@ static __device__ __noinline__ void k3s_table(const LttbArgs& a, const K3sArgs& 
     if (ok > bk || (ok == bk && oq < bq)) { bk = ok; bq = oq; }
   }
   if (lane % PL == 0) tab[p] = (unsigned char)(p < na && bk >= -1 ? bq : 0);
+  k3s_dbg(9);
 }
 
 // ---------------------------------------------------------------- phase 4 --
@@ -752,12 +1046,6 @@ __device__ __noinline__ int64_t warp_pick(const LttbArgs& a, const XT* xs, const
 // also the next guess (*alt) when r is wrong.  Returns false when anything is
 // off (violation, inf / NaN, failed certification).
 struct GrpRed { int v, m1, m2, j1; };
-// tool counters (prof mode): [0] verify calls, [1] violations, [2] shared high word, [3] cert fails,
-// [4] full-path picks, [5] flagged buckets, [6] 4b picks, [7] repair picks
-__device__ unsigned long long* g_k3s_cnt;
-__device__ __forceinline__ void k3s_count(int i) {
-  if (g_k3s_cnt && (threadIdx.x & 31) == 0 && ((threadIdx.x >> 5) == 0 || i < 0)) atomicAdd(g_k3s_cnt + (i < 0 ? -i : i), 1ull);
-}
 __device__ __forceinline__ void top2_merge(int& m1, int& m2, int& j1, int om1, int om2, int oj1) {
   m2 = max(max(m2, om2), min(m1, om1));
   j1 = om1 > m1 ? oj1 : (om1 < m1 ? j1 : min(j1, oj1));
@@ -766,12 +1054,13 @@ __device__ __forceinline__ void top2_merge(int& m1, int& m2, int& j1, int om1, i
 
 template <int NWG, typename XT, typename YT>
 __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b, int64_t prev,
-                           int64_t r, int64_t* alt, GrpRed* sh) {
+                           int64_t r, int64_t* alt, GrpRed* sh, const int2* gm) {
   constexpr int EV = Vec<YT>::EV, UV = 8 / EV, NL = 32 * NWG;
   const int lane = threadIdx.x & 31, wg = NWG == 1 ? 0 : (int)(threadIdx.x >> 5);
   const int L = wg * 32 + lane;
   const int64_t lo = lbound(a, m, b), hi = lbound(a, m, b + 1);
   if (alt) *alt = -1;
+  if (NWG == 1) k3s_dbg(16);
   if (r < lo || r >= hi) return false;
   const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
   const double2 c = __ldcg(a.means + b);
@@ -842,8 +1131,91 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
       }
     });
   };
-  if (afi) run(std::true_type{});
-  else run(std::false_type{});
+  // Pruned scan (one warp, group summaries of phase 1): every fp operation of
+  // the area is monotone in its operands, so over a group's box [xa, xb] x [y0, y1]
+  // the rounded value tt lies in [fl(Mmin - Nmax), fl(Mmax - Nmin)] with
+  // M = fl(P fl(y - ay)) and N = fl(fl(ax - x) S) taken at the box edges -- no
+  // error term.  A group whose bound's high word is below r's cannot hold the
+  // pick nor share r's high word and is skipped (its bound still feeds the
+  // runner-up m2 of the certification); non-finite products keep the group.
+  bool scanned = false;
+  int mB = -1;
+  if (NWG == 1) k3s_dbg(17);
+  if constexpr (NWG == 1) {
+    if (gm) {
+      const GGeo gg = ggeo(w);
+      const bool xexact = f.ok && (!XForm<XT>::integral || (fabs((double)f.di) * (double)(hi - lo) < 4.0e15 &&
+                                                             fmax(fabs(xr.x), fabs(xr.y)) < 4.0e15));
+      unsigned words[K3S_GCAP / 32];
+      int nsurv = 0, mBl = -1;
+#pragma unroll
+      for (int i = 0; i < K3S_GCAP / 32; ++i) {
+        const int gi = lane + 32 * i;
+        bool sv = false;
+        if (gi < gg.ng) {
+          double y0, y1;
+          gkey_bounds<YT>(__ldcg(gm + gi), y0, y1);
+          const int64_t v0g = w.vf + ((int64_t)gi << (gg.s + 5)), v1g = min((int64_t)w.vl, (int64_t)(v0g + (32LL << gg.s)));
+          double xa = xr.x, xb = xr.y;
+          if (xexact) {
+            xa = XForm<XT>::at(f, v0g * EV - lo);
+            xb = XForm<XT>::at(f, v1g * EV - 1 - lo);
+            if (xb < xa) { const double tt = xa; xa = xb; xb = tt; }
+          }
+          const double M0 = __dmul_rn(P, __dsub_rn(y0, ay)), M1 = __dmul_rn(P, __dsub_rn(y1, ay));
+          const double N0 = __dmul_rn(__dsub_rn(ax, xa), S), N1 = __dmul_rn(__dsub_rn(ax, xb), S);
+          const int kfin = max(max(hw_abs(M0), hw_abs(M1)), max(hw_abs(N0), hw_abs(N1)));
+          const double tlo = __dsub_rn(fmin(M0, M1), fmax(N0, N1)), thi = __dsub_rn(fmax(M0, M1), fmin(N0, N1));
+          const int hb = max(hw_abs(tlo), hw_abs(thi));
+          sv = kfin >= 0x7ff00000 || hb >= hr;
+          if (!sv) mBl = max(mBl, hb);
+        }
+        words[i] = __ballot_sync(FULL, sv);
+        nsurv += __popc(words[i]);
+      }
+      if ((((int64_t)nsurv << gg.s) << 1) <= gg.nl) {  // else: the plain scan is cheaper
+        scanned = true;
+        k3s_cnt_add(11, 1);
+        k3s_cnt_add(12, nsurv);
+        mB = __reduce_max_sync(FULL, mBl);
+        const uint4* yv = reinterpret_cast<const uint4*>(ys);
+        const int nsub = 1 << gg.s;
+        static_assert(K3S_GCAP == 128, "four ballot words");
+#pragma unroll 1
+        for (int i = 0; i < K3S_GCAP / 32; ++i) {
+          for (unsigned wd = i == 0 ? words[0] : i == 1 ? words[1] : i == 2 ? words[2] : words[3]; wd; wd &= wd - 1) {
+            const int gi = 32 * i + __ffs(wd) - 1;
+            const int64_t vb = w.vf + ((int64_t)gi << (gg.s + 5)) + lane;
+            for (int sub = 0; sub < nsub; sub += 4) {
+              uint4 rr[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int64_t v = vb + 32LL * (sub + u);
+                rr[u] = (sub + u < nsub && v < w.vl) ? yv[v] : make_uint4(0, 0, 0, 0);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int64_t v = vb + 32LL * (sub + u);
+                if (sub + u < nsub && v < w.vl) {
+#pragma unroll
+                  for (int q = 0; q < EV; ++q) {
+                    const int64_t j = v * EV + q;
+                    el(__dsub_rn(ax, xat(j)), (double)Vec<YT>::get(rr[u], q), (int)(j - lo));
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  if (NWG == 1) k3s_dbg(18);
+  if (!scanned) {
+    if (NWG == 1) k3s_cnt_add(13, 1);
+    if (afi) run(std::true_type{});
+    else run(std::false_type{});
+  }
   // group reduction
 #pragma unroll
   for (int o = 16; o; o >>= 1)
@@ -858,6 +1230,8 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
       top2_merge(m1, m2, j1, g.m1, g.m2, g.j1);
     }
   }
+  if (NWG == 1) k3s_dbg(19);
+  m2 = max(m2, mB);  // skipped groups: every key's high word <= mB < hr
   if (NWG == 1) k3s_count(-0); else k3s_count(0);
   if (m1 > hr) {  // a point beats r: where the exact pick most likely is
     if (alt && m1 < 0x7ff00000 && j1 != INT_MAX) *alt = lo + j1;
@@ -887,10 +1261,10 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
 // CTA: block_bucket_argmax_cert, never storing means back).
 template <int NWG, typename XT, typename YT>
 __device__ int64_t grp_pick(const LttbArgs& a, const XT* xs, const YT* ys, int64_t m, int64_t b, int64_t prev,
-                            int64_t guess, GrpRed* sh, double* s_a, long long* s_i) {
+                            int64_t guess, GrpRed* sh, double* s_a, long long* s_i, const int2* gm = nullptr) {
   int64_t alt = -1;
-  if (grp_verify<NWG, XT, YT>(a, xs, ys, m, b, prev, guess, &alt, sh)) return guess;
-  if (alt >= 0 && alt != guess && grp_verify<NWG, XT, YT>(a, xs, ys, m, b, prev, alt, nullptr, sh)) return alt;
+  if (grp_verify<NWG, XT, YT>(a, xs, ys, m, b, prev, guess, &alt, sh, gm)) return guess;
+  if (alt >= 0 && alt != guess && grp_verify<NWG, XT, YT>(a, xs, ys, m, b, prev, alt, nullptr, sh, gm)) return alt;
   if (NWG == 1) k3s_count(-4); else k3s_count(4);
   if constexpr (NWG == 1) return warp_pick<XT, YT>(a, xs, ys, m, b, prev);
   else return block_bucket_argmax_cert<XT, YT, 32 * NWG>(a, 0, m, xs, ys, b, prev, s_a, s_i, false);
@@ -929,6 +1303,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   extern __shared__ __align__(16) unsigned char dsm[];  // tables [maxb][16] | pos [maxb+1] | entry [maxb]; repair state
   __shared__ int s_e;
   __shared__ int s_last;
+  __shared__ unsigned char s_glist[K3S_NW][K3S_GCAP];  // phase 2: surviving groups per warp
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int64_t k3 = a.n_out - 2, m = a.n;
   const int c = blockIdx.x;
@@ -948,7 +1323,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   stamp(0);
 
   // ---- 1: statistics (HBM) ----
-  for (int64_t b = B0 + wid; b < B1; b += NW) k3s_stats<XT, YT>(a, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), m);
+  for (int64_t b = B0 + wid; b < B1; b += NW) k3s_stats<XT, YT>(a, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), m, ka.gmeta ? ka.gmeta + b * K3S_GCAP : nullptr);
   __syncthreads();
   stamp(1);
   // candidates of buckets [B0, B1) need the statistics of B0-1 and B1 (the
@@ -960,8 +1335,10 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
     if (c + 1 < (int)G) spin_until_set(ka.sync + K3S_FLAGS + c + 1, 1u);
   }
   __syncthreads();
+  k3s_dbg(10);
   // ---- 2: candidates (L2) ----
-  for (int64_t b = B0 + wid; b < B1; b += NW) k3s_cand<XT, YT>(a, ka, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1));
+  for (int64_t b = B0 + wid; b < B1; b += NW) k3s_cand<XT, YT>(a, ka, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), s_glist[wid],
+                                                         reinterpret_cast<float2*>(dsm) + wid * K3S_STAGE);  // (dsm: free until phase 3)
   __syncthreads();
   stamp(2);
   // the tables of [B0, B1) need CTA c-1's last candidate set
@@ -971,10 +1348,12 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
     if (c > 0) spin_until_set(ka.sync + K3S_FLAGS + K3S_GMAX + c - 1, 1u);
   }
   __syncthreads();
+  k3s_dbg(11);
   // ---- 3: tables, aggregate A_c = T_{B1-1} o ... o T_{B0}, chain entry, positions ----
   const double px0 = to_f64(xs, 0), py0 = to_f64(ys, 0);
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_table(a, ka, b, px0, py0, c_tab + (b - B0) * H);
   __syncthreads();
+  k3s_dbg(12);
   typedef PMapN<H> M;
   constexpr int NV = H / 16;  // uint4 words per map
   if (wid == 0) {
@@ -986,8 +1365,10 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
         reinterpret_cast<uint4*>(ka.agg + (int64_t)c * H)[i] = make_uint4(acc.v[4 * i], acc.v[4 * i + 1], acc.v[4 * i + 2], acc.v[4 * i + 3]);
     }
   }
+  k3s_dbg(13);
   k3s_grid_sync(ka.sync, 2, G);
   stamp(3);
+  k3s_dbg(14);
   if (wid == 0) {
     // entry = (A_{c-1} o ... o A_0)(0): lane l composes a contiguous run, then an ordered tree
     int e = 0;
@@ -1047,7 +1428,8 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   if (t == 0 && B1 == k3) out[k3 + 1] = omap(m - 1);
   for (int64_t b = B0 + wid; b < B1; b += NW) {
     const int64_t chain = c_pos[b - B0 + 1];
-    const int64_t r = grp_pick<1, XT, YT>(a, xs, ys, m, b, c_pos[b - B0], chain, nullptr, nullptr, nullptr);
+    const int64_t r = grp_pick<1, XT, YT>(a, xs, ys, m, b, c_pos[b - B0], chain, nullptr, nullptr, nullptr,
+                                          ka.gmeta ? ka.gmeta + b * K3S_GCAP : nullptr);
     if (lane == 0) {
       const bool fg = r != chain;
       a.best[b] = r;
@@ -1057,7 +1439,9 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
     if (r != chain) k3s_count(-5);
   }
   stamp(5);
+  k3s_dbg(20);
   k3s_grid_sync(ka.sync, 3, G);
+  k3s_dbg(21);
   // ---- 4b: one CTA per mismatch f: the true pick of bucket f is best[f]; walk
   // on with exact whole-CTA picks (guessed from the candidate sets) until the
   // chain is re-joined, patching the output.  A walk that meets another
@@ -1097,6 +1481,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
     s_last = atomicAdd(ka.sync + K3S_DONE, 1u) == G - 1;
   }
   __syncthreads();
+  k3s_dbg(22);
   if (!s_last) return;
   __threadfence();
   stamp(6);

@@ -65,7 +65,7 @@ int launch_tables_jump(LttbArgs a, cudaStream_t st) {
 unsigned long long* k3s_prof_buffer();
 
 template <typename XT, typename YT>
-int launch_k3s(LttbArgs a, void* scratch, cudaStream_t st) {
+int launch_k3s(LttbArgs a, void* scratch, int2* gmeta, cudaStream_t st) {
   static const bool on = env_i64("MMLTTB_K3S", 1) != 0;
   if (!on) return MM_ENOTSUP;
   const int64_t k3 = a.n_out - 2;
@@ -80,7 +80,8 @@ int launch_k3s(LttbArgs a, void* scratch, cudaStream_t st) {
   if (cudaFuncGetAttributes(&fa, (const void*)kern) != cudaSuccess) return fail(MM_ECUDA, "cudaFuncGetAttributes(k3s)");
   const int64_t G = nsm;
   const int64_t maxb = cdiv(k3, G) + 1;
-  const int64_t dyn = std::max<int64_t>(up(maxb * K3S_H) + (maxb + 1) * 8 + maxb * 4, repair_smem_bytes(k3));
+  const int64_t dyn = std::max<int64_t>(std::max<int64_t>(up(maxb * K3S_H) + (maxb + 1) * 8 + maxb * 4, repair_smem_bytes(k3)),
+                                        (int64_t)K3S_NW * K3S_STAGE * 8);  // phase 2 stages candidates in the same bytes
   if (dyn + (int64_t)fa.sharedSizeBytes > optin) return MM_ENOTSUP;
   static std::atomic<unsigned long long> attr{0};
   if (int rc = smem_optin(attr, (const void*)kern, (int)(optin - fa.sharedSizeBytes), "k_lttb_k3s")) return rc;
@@ -94,6 +95,9 @@ int launch_k3s(LttbArgs a, void* scratch, cudaStream_t st) {
   a.fcount = (int*)(ka.sync + K3S_FCOUNT);
   ka.agg = (unsigned char*)scratch + up(K3S_SYNC_WORDS * 4);
   ka.cpt = (double2*)(ka.agg + up((int64_t)K3S_GMAX * K3S_H));
+  // group summaries for the pruned candidate search / verification (A/B knob MMLTTB_K3S_PRUNE=0)
+  static const bool prune = env_i64("MMLTTB_K3S_PRUNE", 1) != 0;
+  ka.gmeta = prune ? gmeta : nullptr;
   ka.prof = k3s_prof_buffer();  // tools only (MMLTTB_K3S_PROF=1)
   if (ka.prof) cudaMemsetAsync(ka.prof, 0, (size_t)(K3S_GMAX * 8 + 64) * 8, st);
   if (cudaMemsetAsync(ka.sync, 0, (size_t)K3S_SYNC_WORDS * 4, st) != cudaSuccess) return fail(MM_ECUDA, "memset(k3s)");
@@ -155,7 +159,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
     fl.part = cv.take<unsigned char>(k3 * flat_cp_max(k3) * K3C_FLAT_PART);
     fl.ulist = cv.take<int>(k3);
     fl_c.part = fl.part;
-    const int rk = launch_k3s<XT, YT>(a, fl.part, st);
+    int2* gmeta = cv.take<int2>(k3 * K3S_GCAP);
+    const int rk = launch_k3s<XT, YT>(a, fl.part, gmeta, st);
     if (rk != MM_ENOTSUP) return rk;  // otherwise: the multi-kernel K3c below
     if (cudaMemsetAsync(fcnt, 0, (size_t)(3 * k3 + 3) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "memset");

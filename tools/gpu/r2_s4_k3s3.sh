@@ -1,0 +1,5 @@
+set -x
+O=gpurun_out/s4
+mkdir -p $O
+MMLTTB_K3S_PROF=1 timeout 900 python tools/k3s_check.py --time --prof c2 c2_f32y big_buckets_f32 > $O/k3s_prune3.log 2>&1; echo "rc=$?" >> $O/k3s_prune3.log
+timeout 900 python tools/k3s_check.py --time > $O/k3s_prune3_noprof.log 2>&1

@@ -34,7 +34,31 @@ CASES = [
     ("f64x_arange", 2_000_000, 600, "f64", np.float32),
     ("few_buckets", 500_000, 120, "i64", np.float64),
     ("ties", 1_000_000, 400, "i64tie", np.float64),
+    # group pruning: 2^s warp-loads per group (s > 0), other data shapes
+    ("big_buckets", 20_000_000, 1190, "i64", np.float64, "walk"),
+    ("big_buckets_f32", 40_000_000, 1200, "i64", np.float32, "walk"),
+    ("huge_buckets", 60_000_000, 1186, "i32", np.float32, "c2"),
+    ("smooth", 6_000_000, 1500, "i64", np.float64, "sin"),
+    ("const", 4_000_000, 1300, "i64", np.float64, "const"),
+    ("steps", 6_000_000, 1400, "f64", np.float64, "steps"),
+    ("neg_dx", 5_000_000, 1250, "f64neg", np.float64, "walk"),
 ]
+
+
+def make_y(kind, n, ydt):
+    rng = np.random.Generator(np.random.PCG64(11))
+    if kind == "c2":
+        return c2_y(n, 2, ydt)
+    if kind == "walk":
+        return np.cumsum(rng.standard_normal(n)).astype(ydt)
+    if kind == "sin":
+        i = np.arange(n, dtype=np.float64)
+        return (np.sin(i / 3000.0) * 100 + np.sin(i / 17.0)).astype(ydt)
+    if kind == "const":
+        return np.full(n, 3.25, dtype=ydt)
+    if kind == "steps":  # long flat runs: whole groups tie
+        return np.repeat(rng.integers(-5, 5, n // 1000 + 1), 1000)[:n].astype(ydt)
+    raise ValueError(kind)
 
 
 def make_x(kind, n, seed):
@@ -48,6 +72,8 @@ def make_x(kind, n, seed):
         return np.cumsum(np.random.Generator(np.random.PCG64(seed)).exponential(1.0, n))
     if kind == "i64tie":
         return np.arange(n, dtype=np.int64)
+    if kind == "f64neg":
+        return -0.25 * np.arange(n, dtype=np.float64)[::-1].copy() - 7.0
     raise ValueError(kind)
 
 
@@ -55,11 +81,11 @@ def main():
     timing = "--time" in sys.argv
     only = [a for a in sys.argv[1:] if not a.startswith("--")]
     ok_all = True
-    for name, n, n_out, xk, ydt in CASES:
+    for name, n, n_out, xk, ydt, *yk in CASES:
         if only and name not in only:
             continue
         x = make_x(xk, n, 7)
-        y = c2_y(n, 2, ydt)
+        y = make_y(yk[0] if yk else "c2", n, ydt)
         if xk == "i64tie":  # duplicated values: exact area ties everywhere
             y = np.repeat(y[: n // 2], 2)[:n].copy()
         want = O.lttb(x, y.astype(np.float64), n_out)
@@ -96,6 +122,12 @@ def main():
                 allv = np.array(buf, dtype=np.float64)
                 cn = allv[1024 * 8:1024 * 8 + 8].astype(np.int64)
                 print("   counters: verify calls %d, violations %d, shared-hi %d, cert fails %d, full picks %d, flagged %d, 4b picks %d, repair picks %d" % tuple(cn))
+                pc = allv[1024 * 8 + 8:1024 * 8 + 14].astype(np.int64)
+                print("   pruning: cand pruned %d (groups %d), cand plain %d; verify pruned %d (groups %d), verify plain %d" % tuple(pc))
+                tl = allv[1024 * 8 + 32:1024 * 8 + 64]
+                if tl.max() > 0:
+                    t00 = allv[70 * 8]
+                    print("   CTA 70 warp 0 timeline (us):", " ".join(f"{i}:{(v - t00) / 1e3:.1f}" for i, v in enumerate(tl) if v > 0))
                 dv = allv[1024 * 8 + 16:1024 * 8 + 32].reshape(4, 4)
                 for st in dv:
                     if st[0] > 0:
