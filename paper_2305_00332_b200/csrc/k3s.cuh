@@ -271,7 +271,8 @@ template <typename XT, typename YT>
 __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const YT* ys, int64_t b, int64_t lo,
                                           int64_t hi, int64_t m, int2* gm) {
   constexpr int EY = Vec<YT>::EV, EX = Vec<XT>::EV;
-  constexpr int UY = 8, UX = 16 / EX;  // y: 8 vectors per lane per round (quad mapping below); x: 16 elements
+  // elements per lane per round: the same for x and y (they finish together), 8 vectors of the wider type
+  constexpr int EPR = 8 * (EX < EY ? EX : EY), UY = EPR / EY;
   const int lane = threadIdx.x & 31;
   const int64_t k3 = a.n_out - 2;
   const int n = (int)(hi - lo);
@@ -299,7 +300,33 @@ __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const
       return hy ^ ((hy >> 31) & 0x7fffffff);
     }
   };
-  // The y pass uses a QUAD mapping: in a round of 32 UY vectors, the LS = 32 / UY
+  // ---- x: affine test (integral: XOR-accumulated difference from the formula),
+  // float x: bit compare + sum, keys, lowest bits
+  double sx = 0.0;
+  int lx = XForm<XT>::integral ? 0 : 4096, aff = 1;
+  long long kxm = LLONG_MAX, kxM = LLONG_MIN;
+  unsigned long long dacc = 0;  // integral x: OR of (x ^ formula) over the bucket
+  auto xel = [&](XT x, long long xe) {  // xe: integral: the formula's value here; float: the offset j - lo
+    if constexpr (XForm<XT>::integral) {
+      dacc |= (unsigned long long)((long long)x ^ xe);
+    } else {
+      const double vx = (double)x;
+      aff &= __double_as_longlong(vx) == __double_as_longlong(XForm<XT>::at(f, xe));
+      sx = __dadd_rn(sx, vx);
+      const long long kk = dkey(vx);
+      kxm = min(kxm, kk);
+      kxM = max(kxM, kk);
+      if (try_x) lx = min(lx, lsb_exp(vx));
+    }
+  };
+  auto xexp = [&](int64_t j) -> long long {
+    if constexpr (XForm<XT>::integral) return (long long)((unsigned long long)f.x0i + (unsigned long long)(j - lo) * (unsigned long long)f.di);
+    else return (long long)(j - lo);
+  };
+  const long long xstep = XForm<XT>::integral ? f.di : 1;
+  // One merged loop streams y and x: a round's 8 + 8 vector loads per lane are
+  // issued together (the pass is bound by rounds x DRAM latency, not by issue).
+  // The y loads use a QUAD mapping: in a round of 32 UY vectors, the LS = 32 / UY
   // lanes of set bi = lane / LS load the 32 consecutive vectors of block bi
   // (instruction u: vector 4u + lane % 4 of the lane's 4 UY-vector quad --
   // 64 contiguous bytes per 4 lanes, whole sectors), so a block's (min, max) keys
@@ -322,20 +349,49 @@ __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const
     const uint4* yv = reinterpret_cast<const uint4*>(ys);
     const int64_t voff = (int64_t)(lane >> 2) * (4 * UY) + (lane & 3);
     int amn = INT_MAX, amx = INT_MIN;        // groups spanning rounds (s > LGU)
+    constexpr int UXR = EPR / EX;            // x: lane-strided vectors per lane per round (evict-first)
+    const VWin wx = vwin<XT>(lo, hi);
+    const uint4* xv = reinterpret_cast<const uint4*>(xs);
+    {
+      const int64_t ex = vwin_edge(wx, lo, lane);
+      if (ex >= 0) xel(xs[ex], xexp(ex));
+    }
+    const long long vstep = (long long)((unsigned long long)xstep * (unsigned long long)(32 * EX));
     auto run = [&](auto lsb_tag) {
       constexpr bool LSB = decltype(lsb_tag)::value;
-      int g = 0;
-      for (int64_t vr = wy.vf; vr < wy.vl; vr += 32 * UY, ++g) {  // (warp-uniform)
-        const int64_t v0 = vr + voff;
-        uint4 r[UY];
-        const bool full = vr + 32 * UY <= wy.vl;
+      const int nry = (int)((wy.vl - wy.vf + 32 * UY - 1) / (32 * UY)), nrx = (int)((wx.vl - wx.vf + 32 * UXR - 1) / (32 * UXR));
+      for (int g = 0; g < max(nry, nrx); ++g) {  // (warp-uniform)
+        const int64_t vr = wy.vf + (int64_t)g * (32 * UY), v0 = vr + voff;
+        const int64_t x0v = wx.vf + (int64_t)g * (32 * UXR) + lane;
+        uint4 r[UY], rx[UXR];
+        const bool full = vr + 32 * UY <= wy.vl, fullx = x0v - lane + 32 * UXR <= wx.vl;
         if (full) {
 #pragma unroll
           for (int u = 0; u < UY; ++u) r[u] = yv[v0 + 4 * u];
-        } else {
+        } else if (g < nry) {
 #pragma unroll
           for (int u = 0; u < UY; ++u) r[u] = v0 + 4 * u < wy.vl ? yv[v0 + 4 * u] : make_uint4(0, 0, 0, 0);
         }
+        if (fullx) {
+#pragma unroll
+          for (int u = 0; u < UXR; ++u) rx[u] = __ldcs(xv + x0v + 32 * u);
+        } else if (g < nrx) {
+#pragma unroll
+          for (int u = 0; u < UXR; ++u) rx[u] = x0v + 32 * u < wx.vl ? __ldcs(xv + x0v + 32 * u) : make_uint4(0, 0, 0, 0);
+        }
+        if (g < nrx) {
+          long long xe = xexp(x0v * EX);
+#pragma unroll
+          for (int u = 0; u < UXR; ++u) {
+            if (fullx || x0v + 32 * u < wx.vl) {
+#pragma unroll
+              for (int q = 0; q < EX; ++q)
+                xel(Vec<XT>::get(rx[u], q), (long long)((unsigned long long)xe + (unsigned long long)(q * xstep)));
+            }
+            xe = (long long)((unsigned long long)xe + (unsigned long long)vstep);
+          }
+        }
+        if (g >= nry) continue;
         int vmn = INT_MAX, vmx = INT_MIN;
 #pragma unroll
         for (int u = 0; u < UY; ++u) {
@@ -380,48 +436,6 @@ __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const
     };
     if (try_y) run(std::true_type{});
     else run(std::false_type{});
-  }
-  // ---- x: affine test (integral: XOR-accumulated difference from the formula),
-  // float x: bit compare + sum, keys, lowest bits
-  double sx = 0.0;
-  int lx = XForm<XT>::integral ? 0 : 4096, aff = 1;
-  long long kxm = LLONG_MAX, kxM = LLONG_MIN;
-  unsigned long long dacc = 0;  // integral x: OR of (x ^ formula) over the bucket
-  auto xel = [&](XT x, long long xe) {  // xe: integral: the formula's value here; float: the offset j - lo
-    if constexpr (XForm<XT>::integral) {
-      dacc |= (unsigned long long)((long long)x ^ xe);
-    } else {
-      const double vx = (double)x;
-      aff &= __double_as_longlong(vx) == __double_as_longlong(XForm<XT>::at(f, xe));
-      sx = __dadd_rn(sx, vx);
-      const long long kk = dkey(vx);
-      kxm = min(kxm, kk);
-      kxM = max(kxM, kk);
-      if (try_x) lx = min(lx, lsb_exp(vx));
-    }
-  };
-  auto xexp = [&](int64_t j) -> long long {
-    if constexpr (XForm<XT>::integral) return (long long)((unsigned long long)f.x0i + (unsigned long long)(j - lo) * (unsigned long long)f.di);
-    else return (long long)(j - lo);
-  };
-  const long long xstep = XForm<XT>::integral ? f.di : 1;
-  {
-    const VWin w = vwin<XT>(lo, hi);
-    const int64_t e = vwin_edge(w, lo, lane);
-    if (e >= 0) xel(xs[e], xexp(e));
-    const long long vstep = (long long)((unsigned long long)xstep * (unsigned long long)(32 * EX));
-    vrounds<UX, true, false>(reinterpret_cast<const uint4*>(xs), w, lane, 32, [&](const uint4 (&r)[UX], int64_t v0, int cnt, int) {
-      long long xe = xexp(v0 * EX);
-#pragma unroll
-      for (int u = 0; u < UX; ++u) {
-        if (u < cnt) {
-#pragma unroll
-          for (int q = 0; q < EX; ++q)
-            xel(Vec<XT>::get(r[u], q), (long long)((unsigned long long)xe + (unsigned long long)(q * xstep)));
-        }
-        xe = (long long)((unsigned long long)xe + (unsigned long long)vstep);
-      }
-    });
   }
   if constexpr (XForm<XT>::integral) aff = dacc == 0;
   aff = __all_sync(FULL, aff);
@@ -1369,34 +1383,33 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   k3s_grid_sync(ka.sync, 2, G);
   stamp(3);
   k3s_dbg(14);
+  // entry = (A_{c-1} o ... o A_0)(0).  The predecessors' aggregate maps are staged
+  // in shared memory (one L2 round trip); lane l of warp 0 composes its run of
+  // maps by byte lookups (32 independent chains), lane 0 then walks the <= 32
+  // run maps and the CTA's own tables.
+  unsigned char* s_agg = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(c_e + ka.maxb) + 15) & ~(uintptr_t)15);
+  unsigned char* s_chk = s_agg + (int64_t)G * H;
+  for (int i = t; i < c * (H / 16); i += NT)
+    reinterpret_cast<uint4*>(s_agg)[i] = __ldcg(reinterpret_cast<const uint4*>(ka.agg) + i);
+  __syncthreads();
   if (wid == 0) {
-    // entry = (A_{c-1} o ... o A_0)(0): lane l composes a contiguous run, then an ordered tree
-    int e = 0;
-    if (c > 0) {
-      const int per = (c + 31) / 32;
-      M r = M::ident();
-      for (int i = 0; i < per; ++i) {
-        const int cc = lane * per + i;
-        if (cc < c) {
-          M g;
+    const int per = (c + 31) / 32;
+    const int c0 = lane * per, c1 = min(c, c0 + per);
+    if (c0 < c1) {
+      unsigned char st[H];
 #pragma unroll
-          for (int i2 = 0; i2 < NV; ++i2) {
-            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(ka.agg + (int64_t)cc * H) + i2);
-            g.v[4 * i2] = v.x; g.v[4 * i2 + 1] = v.y; g.v[4 * i2 + 2] = v.z; g.v[4 * i2 + 3] = v.w;
-          }
-          r = M::comp(g, r);
-        }
+      for (int p = 0; p < H; ++p) st[p] = (unsigned char)p;
+      for (int cc = c0; cc < c1; ++cc) {
+#pragma unroll
+        for (int p = 0; p < H; ++p) st[p] = s_agg[cc * H + st[p]];
       }
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        M other;
-#pragma unroll
-        for (int i = 0; i < 4 * NV; ++i) other.v[i] = __shfl_down_sync(FULL, r.v[i], o);
-        if ((lane & (2 * o - 1)) == 0 && lane + o < 32) r = M::comp(other, r);
-      }
-      e = __shfl_sync(FULL, r.at0(), 0);
+      for (int p = 0; p < H; ++p) s_chk[lane * H + p] = st[p];
     }
+    __syncwarp();
     if (lane == 0) {
+      int e = 0;
+      for (int l = 0; l * per < c; ++l) e = s_chk[l * H + e];
       s_e = e;
       int ee = e;
       for (int64_t b = B0; b < B1; ++b) {

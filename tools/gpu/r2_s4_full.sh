@@ -1,0 +1,6 @@
+set -x
+O=gpurun_out/s4
+mkdir -p $O
+timeout 900 python tools/k3s_check.py --time > $O/k3s_v5.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -x -p no:randomly > $O/pytest_gpu2.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu2.log
+timeout 600 python bench.py --workload c2 --steps 50 --warmup 5 > $O/bench_c2_v5.log 2>&1
