@@ -64,6 +64,8 @@ struct K3sArgs {
   double2* cpt;          // [k3][16] candidate points (x, y)
   unsigned long long* prof;  // optional [G][8] %globaltimer stamps per phase (tools), or null
   int2* gmeta;           // [k3][K3S_GCAP] per-group (min, max) y keys written by phase 1, or null (no pruning)
+  int* chg;              // [k3] re-verification pass in which a bucket's anchor last changed (phase 4j)
+  int jmin, jmax;        // phase 4j runs while more than jmin buckets are flagged, for at most jmax passes
 };
 // sync words: barrier i = counter at 64 i, release flag at 64 i + 32 (separate
 // 128-byte lines: the pollers never delay the arrivals); done counter, fcount
@@ -118,6 +120,10 @@ __device__ __forceinline__ void k3s_grid_sync(unsigned* sync, int i, unsigned G)
 // [4] full-path picks, [5] flagged buckets, [6] 4b picks, [7] repair picks, [8] pruned candidate searches,
 // [9] their surviving groups, [10] plain candidate searches, [11] pruned verifications, [12] their
 // surviving groups, [13] plain verifications (one warp)
+// Compiled in only with -DK3S_PROF (tools; MMLTTB_NVCC_EXTRA): each call reads a
+// global pointer the warp then branches on, i.e. an exposed load on the
+// latency-bound phases (the phase stamps of `ka.prof` stay: a constant-bank test).
+#ifdef K3S_PROF
 __device__ unsigned long long* g_k3s_cnt;
 __device__ __forceinline__ void k3s_count(int i) {
   if (g_k3s_cnt && (threadIdx.x & 31) == 0 && ((threadIdx.x >> 5) == 0 || i < 0)) atomicAdd(g_k3s_cnt + (i < 0 ? -i : i), 1ull);
@@ -128,6 +134,30 @@ __device__ __forceinline__ void k3s_dbg(int i) {
 }
 __device__ __forceinline__ void k3s_cnt_add(int i, int v) {  // (every warp's lane 0)
   if (g_k3s_cnt && (threadIdx.x & 31) == 0) atomicAdd(g_k3s_cnt + i, (unsigned long long)v);
+}
+#else
+__device__ __forceinline__ void k3s_count(int) {}
+__device__ __forceinline__ void k3s_dbg(int) {}
+__device__ __forceinline__ void k3s_cnt_add(int, int) {}
+#endif
+
+// reusable grid barrier: the n-th use of counter i waits for n G arrivals
+__device__ __forceinline__ void k3s_grid_sync_n(unsigned* sync, int i, unsigned G, unsigned n) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* ctr = sync + 64 * i;
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    unsigned long long t0 = 0;
+    for (unsigned it = 1; ld_acq(ctr) < G * n; ++it) {
+      if ((it & 1023u) == 0) {
+        const unsigned long long t = gtimer();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 2000000000ull) __trap();  // 2 s
+      }
+    }
+  }
+  __syncthreads();
 }
 
 // float -> int32 key with the same order (IEEE total order)
@@ -1332,10 +1362,13 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   auto stamp = [&](int i) {
     if (ka.prof && t == 0) ka.prof[c * 8 + i] = gtimer();
   };
+#ifdef K3S_PROF
   if (t == 0) g_k3s_cnt = ka.prof ? ka.prof + K3S_GMAX * 8 : nullptr;  // (every CTA: same value)
+#endif
   __syncthreads();
   stamp(0);
 
+  for (int64_t i = t; i < B1 - B0; i += NT) ka.chg[B0 + i] = 0;
   // ---- 1: statistics (HBM) ----
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_stats<XT, YT>(a, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), m, ka.gmeta ? ka.gmeta + b * K3S_GCAP : nullptr);
   __syncthreads();
@@ -1439,22 +1472,66 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   for (int64_t i = t; i < B1 - B0; i += NT) out[B0 + i + 1] = omap(c_pos[i + 1]);
   if (t == 0 && B0 == 0) out[0] = omap(0);
   if (t == 0 && B1 == k3) out[k3 + 1] = omap(m - 1);
-  for (int64_t b = B0 + wid; b < B1; b += NW) {
-    const int64_t chain = c_pos[b - B0 + 1];
-    const int64_t r = grp_pick<1, XT, YT>(a, xs, ys, m, b, c_pos[b - B0], chain, nullptr, nullptr, nullptr,
-                                          ka.gmeta ? ka.gmeta + b * K3S_GCAP : nullptr);
-    if (lane == 0) {
-      const bool fg = r != chain;
-      a.best[b] = r;
-      a.flag[b] = fg;
-      if (fg) a.flist[atomicAdd(fcount, 1)] = (int)b;
+  // 4a + 4j.  Pass 0 verifies every bucket.  When many buckets mismatch (smooth
+  // data: the pick moves a little with the anchor, so a candidate chain is off
+  // almost everywhere), parallel fixed-point passes replace the walks: a pass
+  // moves every flagged bucket's exact pick into the chain (pos[b+1] = best[b])
+  // and re-verifies -- all at once, pruned -- the buckets whose anchor moved.
+  // The invariant best[b] = pick(b | pos[b]), flag[b] = (best[b] != pos[b+1])
+  // holds after every pass, so the loop can stop anywhere: no flags left means
+  // the chain is the reference's (induction from bucket 0, exact after pass 0;
+  // bucket i after pass i at the latest), a few flags left go to 4b, and jmax
+  // passes without convergence leave the rest to 4b / the sequential walk.
+  {
+    int* const fc0 = fcount;
+    for (int it = 0;; ++it) {
+      for (int64_t b = B0 + wid; b < B1; b += NW) {
+        bool fg = false;
+        if (it == 0 || __ldcg(ka.chg + b) == it) {
+          const int64_t cur = c_pos[b - B0 + 1];
+          const int64_t r = grp_pick<1, XT, YT>(a, xs, ys, m, b, c_pos[b - B0], cur, nullptr, nullptr, nullptr,
+                                                ka.gmeta ? ka.gmeta + b * K3S_GCAP : nullptr);
+          fg = r != cur;
+          if (lane == 0) {
+            a.best[b] = r;
+            if (fg) a.flist[atomicAdd(fcount, 1)] = (int)b;
+          }
+          if (fg) k3s_count(-5);
+          if (it) k3s_cnt_add(14, 1);
+        }
+        if (lane == 0) a.flag[b] = fg;
+      }
+      if (it == 0) {
+        stamp(5);
+        k3s_dbg(20);
+        k3s_grid_sync(ka.sync, 3, G);
+        k3s_dbg(21);
+      } else {
+        k3s_grid_sync_n(ka.sync, 1, G, 2 * it);
+        if (t == 0 && c == 0) k3s_cnt_add(15, 1);
+      }
+      const int nf = *(volatile int*)fcount;
+#ifdef K3S_NO_4J  // (A/B build: no fixed-point passes)
+      break;
+#endif
+      if (nf <= ka.jmin || it >= ka.jmax) break;
+      for (int64_t i = t; i < B1 - B0; i += NT) {
+        const int64_t b = B0 + i;
+        if (__ldcg(a.flag + b)) {
+          const int64_t p = __ldcg(a.best + b);
+          c_pos[i + 1] = p;
+          a.pos[b + 1] = p;
+          out[b + 1] = omap(p);
+          if (b + 1 < k3) ka.chg[b + 1] = it + 1;
+        }
+      }
+      fcount = fc0 + ((it + 1) & 1);
+      if (c == 0 && t == 0) *fcount = 0;
+      k3s_grid_sync_n(ka.sync, 1, G, 2 * it + 1);
+      if (t == 0 && B0 > 0) c_pos[0] = __ldcg(a.pos + B0);
+      __syncthreads();
     }
-    if (r != chain) k3s_count(-5);
   }
-  stamp(5);
-  k3s_dbg(20);
-  k3s_grid_sync(ka.sync, 3, G);
-  k3s_dbg(21);
   // ---- 4b: one CTA per mismatch f: the true pick of bucket f is best[f]; walk
   // on with exact whole-CTA picks (guessed from the candidate sets) until the
   // chain is re-joined, patching the output.  A walk that meets another

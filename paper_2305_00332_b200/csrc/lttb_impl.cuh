@@ -95,6 +95,11 @@ int launch_k3s(LttbArgs a, void* scratch, int2* gmeta, cudaStream_t st) {
   a.fcount = (int*)(ka.sync + K3S_FCOUNT);
   ka.agg = (unsigned char*)scratch + up(K3S_SYNC_WORDS * 4);
   ka.cpt = (double2*)(ka.agg + up((int64_t)K3S_GMAX * K3S_H));
+  ka.chg = (int*)((unsigned char*)ka.cpt + up(k3 * K3S_H * (int64_t)sizeof(double2)));
+  // fixed-point re-verification passes (A/B knobs: MMLTTB_K3S_JMIN / _JMAX; JMAX=0: walks only)
+  static const int jmin = (int)env_i64("MMLTTB_K3S_JMIN", 8), jmax = (int)env_i64("MMLTTB_K3S_JMAX", 32);
+  ka.jmin = jmin;
+  ka.jmax = jmax;
   // group summaries for the pruned candidate search / verification (A/B knob MMLTTB_K3S_PRUNE=0)
   static const bool prune = env_i64("MMLTTB_K3S_PRUNE", 1) != 0;
   ka.gmeta = prune ? gmeta : nullptr;

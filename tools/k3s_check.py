@@ -122,8 +122,8 @@ def main():
                 allv = np.array(buf, dtype=np.float64)
                 cn = allv[1024 * 8:1024 * 8 + 8].astype(np.int64)
                 print("   counters: verify calls %d, violations %d, shared-hi %d, cert fails %d, full picks %d, flagged %d, 4b picks %d, repair picks %d" % tuple(cn))
-                pc = allv[1024 * 8 + 8:1024 * 8 + 14].astype(np.int64)
-                print("   pruning: cand pruned %d (groups %d), cand plain %d; verify pruned %d (groups %d), verify plain %d" % tuple(pc))
+                pc = allv[1024 * 8 + 8:1024 * 8 + 16].astype(np.int64)
+                print("   pruning: cand pruned %d (groups %d), cand plain %d; verify pruned %d (groups %d), verify plain %d; 4j re-verified %d in %d passes" % tuple(pc))
                 tl = allv[1024 * 8 + 32:1024 * 8 + 64]
                 if tl.max() > 0:
                     t00 = allv[70 * 8]
