@@ -718,11 +718,12 @@ __device__ __forceinline__ void k3s_cand_t(const LttbArgs& a, const K3sArgs& ka,
 // straight-line code of that length is bound by instruction fetch.  A heuristic
 // like the plain search (phase 4 makes the result exact); returns false when
 // the plain search should run instead.
-constexpr int K3S_STAGE = 512;  // staged points per warp and chunk (float2 each)
+constexpr int K3S_STAGE = 512;  // staged points per warp and chunk (float2 each; + 32 head / tail slots)
+constexpr int K3S_STAGE_LD = K3S_STAGE + 32;
 template <typename XT, typename YT>
 __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& ka, const XT* xs, const YT* ys, int64_t b,
                                              int64_t lo, int64_t hi, float lmin, float lmax, unsigned char* slist,
-                                             float2* stage) {
+                                             float2* stage, int2 gk0, int2 gk1, int2 gk2, int2 gk3) {
   constexpr int D = K3S_D, NI = K3S_GCAP / 32;
   constexpr int EV = Vec<YT>::EV, CW = K3S_STAGE / (32 * EV);  // warp-loads per chunk
   static_assert(D == 16, "lane l searches slope l % 16");
@@ -732,16 +733,18 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
   if (hi - lo >= (1 << 24)) return false;  // (T must be exact in f32)
   const GGeo gg = ggeo(w);
   if (gg.ng == 0) return false;
-  const int2* gm = ka.gmeta + b * K3S_GCAP;
   const uint4* yv = reinterpret_cast<const uint4*>(ys);
-  // this lane's groups: y bounds (outer and inner) and index offsets
+  // this lane's groups (summaries loaded by the caller, ahead of its own loads):
+  // y bounds (outer and inner) and index offsets
+  const int2 gk[NI] = {gk0, gk1, gk2, gk3};
+  static_assert(NI == 4, "four summaries per lane");
   float yxh[NI], yxl[NI], ynh[NI], ynl[NI], t0[NI], t1[NI];
 #pragma unroll
   for (int i = 0; i < NI; ++i) {
     const int gi = lane + 32 * i;
     yxh[i] = yxl[i] = -INFINITY; ynh[i] = ynl[i] = INFINITY; t0[i] = t1[i] = 0.f;
     if (gi < gg.ng) {
-      const int2 k = __ldcg(gm + gi);
+      const int2 k = gk[i];
       if constexpr (sizeof(YT) == 4) {
         yxh[i] = yxl[i] = __int_as_float(k.y ^ ((k.y >> 31) & 0x7fffffff));
         ynh[i] = ynl[i] = __int_as_float(k.x ^ ((k.x >> 31) & 0x7fffffff));
@@ -761,7 +764,7 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
   bool sv[NI];
 #pragma unroll
   for (int i = 0; i < NI; ++i) sv[i] = false;
-#pragma unroll 2
+#pragma unroll 4
   for (int k = 0; k < D; ++k) {
     const float l = fmaf(dl, (float)k, lmin);
     float bl = -INFINITY, bs = INFINITY;
@@ -820,11 +823,6 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
     }
     __syncwarp();
   };
-  {  // head / tail elements (NaN: an empty slot, never wins)
-    const int64_t ej = vwin_edge(w, lo, lane);
-    stage[lane] = ej >= 0 ? make_float2((float)ys[ej], (float)(ej - lo)) : make_float2(NAN, 0.f);
-    if (__any_sync(FULL, ej >= 0)) search(32);
-  }
   k3s_dbg(4);
   const int smask = (1 << gg.s) - 1;
 #pragma unroll 1
@@ -848,7 +846,13 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
       for (int e = 0; e < EV; ++e)
         stage[(u * 32 + lane) * EV + e] = vs[u] >= 0 ? make_float2((float)Vec<YT>::get(r[u], e), tb + (float)e) : make_float2(NAN, 0.f);
     }
-    search((int)min((int64_t)CW, nun - q0) * 32 * EV);
+    int np = (int)min((int64_t)CW, nun - q0) * 32 * EV;
+    if (q0 == 0) {  // head / tail elements ride along (NaN: an empty slot, never wins)
+      const int64_t ej = vwin_edge(w, lo, lane);
+      stage[np + lane] = ej >= 0 ? make_float2((float)ys[ej], (float)(ej - lo)) : make_float2(NAN, 0.f);
+      np += 32;
+    }
+    search(np);
   }
   k3s_dbg(5);
   // merge the 8 point subsets (lanes with equal l % 4); lane l then reports
@@ -880,6 +884,11 @@ __device__ __forceinline__ void k3s_cand(const LttbArgs& a, const K3sArgs& ka, c
                                          int64_t lo, int64_t hi, unsigned char* slist, float2* stage) {
   constexpr int D = K3S_D;
   k3s_dbg(0);
+  int2 gk[4] = {};
+  if (ka.gmeta) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) gk[i] = __ldcg(ka.gmeta + b * K3S_GCAP + (threadIdx.x & 31) + 32 * i);
+  }
   double bx0, bx1, by0, by1;
   if (b == 0) {
     bx0 = bx1 = to_f64(xs, 0);
@@ -909,7 +918,7 @@ __device__ __forceinline__ void k3s_cand(const LttbArgs& a, const K3sArgs& ka, c
     lmin = fmin(lmin, l);
     lmax = fmax(lmax, l);
   }
-  if (aff && ka.gmeta && k3s_cand_pruned<XT, YT>(a, ka, xs, ys, b, lo, hi, (float)lmin, (float)lmax, slist, stage)) return;
+  if (aff && ka.gmeta && k3s_cand_pruned<XT, YT>(a, ka, xs, ys, b, lo, hi, (float)lmin, (float)lmax, slist, stage, gk[0], gk[1], gk[2], gk[3])) return;
   float lam[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) lam[k] = (float)(lmin + (lmax - lmin) * ((double)k / (double)(D - 1)));
@@ -1385,7 +1394,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   k3s_dbg(10);
   // ---- 2: candidates (L2) ----
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_cand<XT, YT>(a, ka, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), s_glist[wid],
-                                                         reinterpret_cast<float2*>(dsm) + wid * K3S_STAGE);  // (dsm: free until phase 3)
+                                                         reinterpret_cast<float2*>(dsm) + wid * K3S_STAGE_LD);  // (dsm: free until phase 3)
   __syncthreads();
   stamp(2);
   // the tables of [B0, B1) need CTA c-1's last candidate set

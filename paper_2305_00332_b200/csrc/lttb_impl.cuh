@@ -81,7 +81,7 @@ int launch_k3s(LttbArgs a, void* scratch, int2* gmeta, cudaStream_t st) {
   const int64_t G = nsm;
   const int64_t maxb = cdiv(k3, G) + 1;
   const int64_t dyn = std::max<int64_t>(std::max<int64_t>(up(maxb * K3S_H) + (maxb + 1) * 8 + maxb * 4 + 32 + (G + 32) * K3S_H, repair_smem_bytes(k3)),
-                                        (int64_t)K3S_NW * K3S_STAGE * 8);  // phase 2 stages candidates in the same bytes
+                                        (int64_t)K3S_NW * K3S_STAGE_LD * 8);  // phase 2 stages candidates in the same bytes
   if (dyn + (int64_t)fa.sharedSizeBytes > optin) return MM_ENOTSUP;
   static std::atomic<unsigned long long> attr{0};
   if (int rc = smem_optin(attr, (const void*)kern, (int)(optin - fa.sharedSizeBytes), "k_lttb_k3s")) return rc;

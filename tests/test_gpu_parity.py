@@ -693,23 +693,42 @@ x = np.arange(n, dtype=np.int64)
 y = np.cumsum(rng.standard_normal(n)) + rng.normal(0, 0.5, n)
 xi = np.cumsum(rng.integers(1, 4, n)).astype(np.int64)
 yd = np.repeat(np.cumsum(rng.standard_normal(n // 2 + 1)), 2)[:n].copy()
-for xx, yy, k in [(x, y, 2000), (xi, y.astype(np.float32), 1500), (x, yd, 1800), (x.astype(np.float64) * 0.25, y, 3001)]:
+cases = [(x, y, 2000), (xi, y.astype(np.float32), 1500), (x, yd, 1800), (x.astype(np.float64) * 0.25, y, 3001)]
+# group pruning / fixed-point passes: smooth, constant and stepped data (many
+# mismatches or whole-group ties), decreasing-magnitude negative float x, and
+# buckets of > 8192 points (groups of 2^s warp-loads, s > 0) in f64 and f32
+i = np.arange(n, dtype=np.float64)
+cases += [(x, np.sin(i / 3000.0) * 100 + np.sin(i / 17.0), 1400), (x, np.full(n, 3.25), 1300),
+          (x, np.repeat(rng.integers(-5, 5, n // 1000 + 1), 1000)[:n].astype(np.float64), 1250),
+          (-0.25 * i[::-1].copy() - 7.0, y, 1300)]
+nb = 12_000_011
+yb = np.cumsum(rng.standard_normal(nb))
+cases += [(np.arange(nb, dtype=np.int64), yb, 1186), (np.arange(nb, dtype=np.int32), yb.astype(np.float32), 1190)]
+for xx, yy, k in cases:
     got = mm.lttb(torch.from_numpy(xx).cuda(), torch.from_numpy(yy).cuda(), k).cpu().numpy()
     if not np.array_equal(got, O.lttb(xx, yy.astype(np.float64), k)):
-        sys.exit('mismatch at n_out=%d' % k)
+        sys.exit('mismatch at n=%d n_out=%d' % (len(xx), k))
 print('ok')
 """
 
 
 @pytest.mark.parametrize("knobs", [{}, {"MMLTTB_K3C_CAND_CAP": "1"}, {"MMLTTB_K3C_CAND_CAP": "2"},
-                                   {"MMLTTB_K3C_CERT_FORCE": "1"}, {"MMLTTB_K3S": "0"}])
+                                   {"MMLTTB_K3C_CERT_FORCE": "1"}, {"MMLTTB_K3S": "0"},
+                                   {"MMLTTB_K3S_PRUNE": "0"}, {"MMLTTB_K3S_JMAX": "0"},
+                                   {"MMLTTB_K3S_JMIN": "0", "MMLTTB_K3S_JMAX": "2"},
+                                   {"MMLTTB_K3C_CAND_CAP": "1", "MMLTTB_K3S_JMAX": "0"},
+                                   {"MMLTTB_K3C_CERT_FORCE": "1", "MMLTTB_K3S_JMIN": "0"}])
 def test_lttb_k3s_single_launch(knobs):
     """K3s (one cooperative launch for full LTTB over >= 8 x SMs large buckets):
-    arange / irregular integer / duplicated-point / float x, f64 and f32 y, at
-    its default, with the candidate sets cut to 1-2 points (every bucket's pick
-    missed: 4a mismatches, 4b deviation walks and the sequential repair walk
-    all run), with every certification failing (in-order exact means), and the
-    multi-kernel K3c fallback (MMLTTB_K3S=0) -- all index-exact vs the oracle."""
+    arange / irregular integer / duplicated-point / float x, f64 and f32 y,
+    smooth / constant / stepped data and buckets beyond one group size, at
+    its default (group-pruned candidate search and verification, fixed-point
+    passes when many buckets mismatch), with the candidate sets cut to 1-2 points
+    (every bucket's pick missed: mismatches, fixed-point passes, 4b deviation
+    walks and the sequential repair walk all run), with every certification
+    failing (in-order exact means), without pruning, with the fixed-point passes
+    off (walks only) or cut short after 2 passes, and the multi-kernel K3c
+    fallback (MMLTTB_K3S=0) -- all index-exact vs the oracle."""
     import os
     import subprocess
     import sys
