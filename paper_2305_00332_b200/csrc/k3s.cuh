@@ -1195,10 +1195,12 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
   int mB = -1;
   if (NWG == 1) k3s_dbg(17);
   if constexpr (NWG == 1) {
-    if (gm) {
+    // (affine integer x: the bucket's x range comes from the formula's end points,
+    // which bound every value only when the formula cannot wrap: else no pruning)
+    const bool xnowrap = fabs((double)f.di) * (double)(hi - lo) < 4.0e15 && fmax(fabs(xr.x), fabs(xr.y)) < 4.0e15;
+    if (gm && (!f.ok || !XForm<XT>::integral || xnowrap)) {
       const GGeo gg = ggeo(w);
-      const bool xexact = f.ok && (!XForm<XT>::integral || (fabs((double)f.di) * (double)(hi - lo) < 4.0e15 &&
-                                                             fmax(fabs(xr.x), fabs(xr.y)) < 4.0e15));
+      const bool xexact = f.ok;
       unsigned words[K3S_GCAP / 32];
       int nsurv = 0, mBl = -1;
 #pragma unroll
