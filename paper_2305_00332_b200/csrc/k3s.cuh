@@ -141,6 +141,17 @@ __device__ __forceinline__ void k3s_dbg(int) {}
 __device__ __forceinline__ void k3s_cnt_add(int, int) {}
 #endif
 
+// -DK3S_CHECKED (tools/k3s_check.py under a checked build; compute-sanitizer is
+// closed on the GPU pool): every index into the round-2 arrays (group
+// summaries, survivor lists, the staging buffer, the re-verification stamps)
+// and every vector the pruned phases load is range-checked; a violation traps
+// (the launch fails).  Compiled out by default.
+#ifdef K3S_CHECKED
+#define K3S_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define K3S_ASSERT(c) do { } while (0)
+#endif
+
 // reusable grid barrier: the n-th use of counter i waits for n G arrivals
 __device__ __forceinline__ void k3s_grid_sync_n(unsigned* sync, int i, unsigned G, unsigned n) {
   __syncthreads();
@@ -451,12 +462,14 @@ __device__ __forceinline__ void k3s_stats(const LttbArgs& a, const XT* xs, const
           }
           if (gg.s <= LGU) {
             const int gi = (int)(((int64_t)g * UY + lane / LS) >> gg.s);
+            K3S_ASSERT(gg.ng <= K3S_GCAP);
             if ((lane & ((LS << gg.s) - 1)) == 0 && gi < gg.ng) gm[gi] = make_int2(vmn, vmx);
           } else {
             amn = min(amn, vmn);
             amx = max(amx, vmx);
             const int64_t nblk = (int64_t)(g + 1) * UY;  // blocks so far
             if ((nblk & ((1LL << gg.s) - 1)) == 0 || vr + 32 * UY >= wy.vl) {
+              K3S_ASSERT(((nblk - 1) >> gg.s) < gg.ng && gg.ng <= K3S_GCAP);
               if (lane == 0) gm[(int)((nblk - 1) >> gg.s)] = make_int2(amn, amx);
               amn = INT_MAX; amx = INT_MIN;
             }
@@ -789,6 +802,7 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
 #pragma unroll
   for (int i = 0; i < NI; ++i) {
     const unsigned wd = __ballot_sync(FULL, sv[i]);
+    K3S_ASSERT(!sv[i] || (nsurv + __popc(wd & ((1u << lane) - 1u)) < K3S_GCAP && lane + 32 * i < gg.ng));
     if (sv[i]) slist[nsurv + __popc(wd & ((1u << lane) - 1u))] = (unsigned char)(lane + 32 * i);
     nsurv += __popc(wd);
   }
@@ -834,7 +848,9 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
       vs[u] = -1;
       if (q0 + u < nun) {
         const int64_t q = q0 + u;
+        K3S_ASSERT((q >> gg.s) < nsurv && slist[q >> gg.s] < gg.ng);
         const int64_t v = w.vf + 32 * ((((int64_t)slist[q >> gg.s]) << gg.s) + (q & smask)) + lane;
+        K3S_ASSERT(v >= w.vf);
         if (v < w.vl) vs[u] = v;
       }
       r[u] = vs[u] >= 0 ? yv[vs[u]] : make_uint4(0, 0, 0, 0);
@@ -843,12 +859,15 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
     for (int u = 0; u < CW; ++u) {
       const float tb = (float)(vs[u] * EV - lo);
 #pragma unroll
-      for (int e = 0; e < EV; ++e)
+      for (int e = 0; e < EV; ++e) {
+        K3S_ASSERT((u * 32 + lane) * EV + e < K3S_STAGE);
         stage[(u * 32 + lane) * EV + e] = vs[u] >= 0 ? make_float2((float)Vec<YT>::get(r[u], e), tb + (float)e) : make_float2(NAN, 0.f);
+      }
     }
     int np = (int)min((int64_t)CW, nun - q0) * 32 * EV;
     if (q0 == 0) {  // head / tail elements ride along (NaN: an empty slot, never wins)
       const int64_t ej = vwin_edge(w, lo, lane);
+      K3S_ASSERT(np + lane < K3S_STAGE_LD && (ej < 0 || (ej >= lo && ej < hi)));
       stage[np + lane] = ej >= 0 ? make_float2((float)ys[ej], (float)(ej - lo)) : make_float2(NAN, 0.f);
       np += 32;
     }
@@ -1246,6 +1265,7 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int64_t v = vb + 32LL * (sub + u);
+                K3S_ASSERT(v >= w.vf && gi < gg.ng);
                 rr[u] = (sub + u < nsub && v < w.vl) ? yv[v] : make_uint4(0, 0, 0, 0);
               }
 #pragma unroll
@@ -1503,6 +1523,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
           const int64_t r = grp_pick<1, XT, YT>(a, xs, ys, m, b, c_pos[b - B0], cur, nullptr, nullptr, nullptr,
                                                 ka.gmeta ? ka.gmeta + b * K3S_GCAP : nullptr);
           fg = r != cur;
+          K3S_ASSERT(r >= lbound(a, m, b) && r < lbound(a, m, b + 1));
           if (lane == 0) {
             a.best[b] = r;
             if (fg) a.flist[atomicAdd(fcount, 1)] = (int)b;
@@ -1533,6 +1554,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
           c_pos[i + 1] = p;
           a.pos[b + 1] = p;
           out[b + 1] = omap(p);
+          K3S_ASSERT(b >= 0 && b < k3);
           if (b + 1 < k3) ka.chg[b + 1] = it + 1;
         }
       }

@@ -135,6 +135,16 @@ def main():
                 a = allv[:1024 * 8].reshape(1024, 8)
                 a = a[a[:, 0] > 0]
                 t0 = a[:, 0].min()
+                if "--ctas" in sys.argv:  # per-CTA statistics-done times: buckets per CTA vs finish time
+                    G = a.shape[0]
+                    k3 = n_out - 2
+                    nbk = np.array([(c + 1) * k3 // G - c * k3 // G for c in range(G)])
+                    sd = (a[:, 1] - t0) / 1e3
+                    order = np.argsort(sd)
+                    print("   stats done by buckets/CTA:", {int(k): (round(float(sd[nbk == k].mean()), 1), round(float(sd[nbk == k].max()), 1)) for k in np.unique(nbk)})
+                    print("   slowest CTAs (id, buckets, us):", [(int(c), int(nbk[c]), round(float(sd[c]), 1)) for c in order[-12:]])
+                    print("   fastest CTAs (id, buckets, us):", [(int(c), int(nbk[c]), round(float(sd[c]), 1)) for c in order[:6]])
+                    print("   start skew (us): max", round(float((a[:, 0].max() - t0) / 1e3), 2))
                 names = ["start", "stats", "cand", "tab+agg", "chain", "verify", "verify2+", "repair"]
                 for i in range(1, 8):
                     col = a[:, i]
