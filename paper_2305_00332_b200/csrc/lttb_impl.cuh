@@ -73,12 +73,19 @@ int launch_k3s(LttbArgs a, void* scratch, int2* gmeta, cudaStream_t st) {
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(MM_ECUDA, "cudaGetDevice");
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (nsm < 1 || nsm > K3S_GMAX || k3 < 8LL * nsm) return MM_ENOTSUP;
+  // One warp streams a whole bucket, so with fewer than 8 buckets per SM K3s needs
+  // narrow buckets: measured on one box (tools/k3s_check.py, 1e7 points): 10,020-point
+  // buckets 109 vs 153 us for the K3c kernels, 33,500-point buckets 205 vs 169 us,
+  // 100,000-point buckets 389 vs 240 us (A/B knobs MMLTTB_K3S_MINB4: buckets per SM x 4
+  // from which the bucket width is not looked at; MMLTTB_K3S_WIDE: widest such bucket)
+  static const int64_t minb4 = env_i64("MMLTTB_K3S_MINB4", 32), wide = env_i64("MMLTTB_K3S_WIDE", 16384);
+  if (nsm < 1 || nsm > K3S_GMAX || k3 < 2) return MM_ENOTSUP;
+  if (4 * k3 < minb4 * nsm && (a.n - 2) / k3 > wide) return MM_ENOTSUP;
   if (((uintptr_t)a.x & 15) || ((uintptr_t)a.y & 15)) return MM_ENOTSUP;  // 16-byte vector loads  // < 8 busy warps per SM: K3c's flat passes win
   auto kern = k_lttb_k3s<XT, YT>;
   cudaFuncAttributes fa{};
   if (cudaFuncGetAttributes(&fa, (const void*)kern) != cudaSuccess) return fail(MM_ECUDA, "cudaFuncGetAttributes(k3s)");
-  const int64_t G = nsm;
+  const int64_t G = std::min<int64_t>(nsm, k3);
   const int64_t maxb = cdiv(k3, G) + 1;
   const int64_t dyn = std::max<int64_t>(std::max<int64_t>(up(maxb * K3S_H) + (maxb + 1) * 8 + maxb * 4 + 32 + (G + 32) * K3S_H, repair_smem_bytes(k3)),
                                         (int64_t)K3S_NW * K3S_STAGE_LD * 8);  // phase 2 stages candidates in the same bytes

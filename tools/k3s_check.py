@@ -42,6 +42,16 @@ CASES = [
     ("const", 4_000_000, 1300, "i64", np.float64, "const"),
     ("steps", 6_000_000, 1400, "f64", np.float64, "steps"),
     ("neg_dx", 5_000_000, 1250, "f64neg", np.float64, "walk"),
+    # few, wide buckets (K3s below 8 buckets per SM: one warp streams a whole bucket)
+    ("wide_300", 10_000_000, 300, "i64", np.float64, "walk"),
+    ("wide_1000", 10_000_000, 1000, "i64", np.float64, "walk"),
+    ("wide_100", 10_000_000, 100, "i64", np.float32, "walk"),
+    ("wide_30", 3_000_000, 30, "i64", np.float64, "walk"),
+    ("tiny_k3", 200_000, 4, "i64", np.float64, "walk"),
+    # many narrow buckets (several buckets per warp and phase)
+    ("many_100pt", 1_000_000, 10_000, "i64", np.float64, "walk"),
+    ("many_500pt", 4_000_000, 8_000, "i64", np.float64, "walk"),
+    ("many_1500pt", 6_000_000, 4_000, "i64", np.float32, "walk"),
 ]
 
 
