@@ -55,6 +55,9 @@ constexpr int K3S_GMAX = 1024;       // CTA bound for the workspace
 // few groups that can matter: on C2 ~5 of 79 groups per bucket for the
 // candidates and ~1.1 for the verification (a random walk without spikes: 5.1 / 1.14).
 constexpr int K3S_GCAP = 128;
+// buckets of fewer groups are scanned whole: bounding 12 groups costs what scanning
+// them does (6e6 f32 points / n_out 4000, 1,500-point buckets: 122 vs 114 us)
+constexpr int K3S_PRUNE_MIN_GROUPS = 24;
 
 struct K3sArgs {
   int G;                 // CTAs, all co-resident (cooperative launch)
@@ -745,7 +748,7 @@ __device__ __noinline__ bool k3s_cand_pruned(const LttbArgs& a, const K3sArgs& k
   const VWin w = vwin<YT>(lo, hi);
   if (hi - lo >= (1 << 24)) return false;  // (T must be exact in f32)
   const GGeo gg = ggeo(w);
-  if (gg.ng == 0) return false;
+  if (gg.ng < K3S_PRUNE_MIN_GROUPS) return false;
   const uint4* yv = reinterpret_cast<const uint4*>(ys);
   // this lane's groups (summaries loaded by the caller, ahead of its own loads):
   // y bounds (outer and inner) and index offsets
@@ -1217,8 +1220,8 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
     // (affine integer x: the bucket's x range comes from the formula's end points,
     // which bound every value only when the formula cannot wrap: else no pruning)
     const bool xnowrap = fabs((double)f.di) * (double)(hi - lo) < 4.0e15 && fmax(fabs(xr.x), fabs(xr.y)) < 4.0e15;
-    if (gm && (!f.ok || !XForm<XT>::integral || xnowrap)) {
-      const GGeo gg = ggeo(w);
+    const GGeo gg = ggeo(w);
+    if (gm && gg.ng >= K3S_PRUNE_MIN_GROUPS && (!f.ok || !XForm<XT>::integral || xnowrap)) {
       const bool xexact = f.ok;
       unsigned words[K3S_GCAP / 32];
       int nsurv = 0, mBl = -1;

@@ -186,7 +186,9 @@ def test_batch_equals_per_series():
             assert np.array_equal(lt[i], O.lttb(x, y[i].astype(dt), 200))
 
 
-@pytest.mark.parametrize("n,n_out", [(10, 3), (100, 98), (1000, 500), (65_537, 40), (300_000, 3)])
+@pytest.mark.parametrize("n,n_out", [(10, 3), (100, 98), (1000, 500), (65_537, 40), (300_000, 3),
+                                     # K3s below one bucket per SM (G = k3 CTAs) / K3c for wide buckets
+                                     (20_000, 4), (50_000, 5), (200_000, 60), (1_000_000, 150), (2_000_000, 40)])
 def test_lttb_shapes(n, n_out):
     rng = np.random.Generator(np.random.PCG64(n))
     x = np.cumsum(rng.exponential(1.0, n))
