@@ -973,13 +973,17 @@ static __device__ __noinline__ void k3s_table(const LttbArgs& a, const K3sArgs& 
   const double2 c = __ldcg(a.means + b);
   long long bk = -2;
   int bq = 0;
-#pragma unroll 8
+  // one coalesced load of the bucket's candidate points, then warp broadcasts
+  // (a load per candidate was four dependent L2 round trips)
+  double2 mine = make_double2(0.0, 0.0);
+  if (lane < nq) mine = __ldcg(ka.cpt + b * H + lane);
+  const int nqw = __reduce_max_sync(FULL, nq - q0);  // (warp-uniform trip count)
+#pragma unroll 4
   for (int i = 0; i < QL; ++i) {
-    if (q0 + i < nq) {
-      const double2 pt = __ldcg(ka.cpt + b * H + q0 + i);
-      const long long k = lttb_area_key(ax, ay, c.x, c.y, pt.x, pt.y);
-      if (k > bk) { bk = k; bq = q0 + i; }
-    }
+    if (i >= nqw) break;
+    const double px = __shfl_sync(FULL, mine.x, q0 + i), py = __shfl_sync(FULL, mine.y, q0 + i);
+    const long long k = lttb_area_key(ax, ay, c.x, c.y, px, py);
+    if (q0 + i < nq && k > bk) { bk = k; bq = q0 + i; }
   }
   if (PL == 2) {
     const long long ok = __shfl_xor_sync(FULL, bk, 1);
@@ -1435,16 +1439,10 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_table(a, ka, b, px0, py0, c_tab + (b - B0) * H);
   __syncthreads();
   k3s_dbg(12);
-  typedef PMapN<H> M;
-  constexpr int NV = H / 16;  // uint4 words per map
-  if (wid == 0) {
-    M acc = M::ident();
-    for (int64_t b = B0; b < B1; ++b) acc = M::comp(M::load(c_tab + (b - B0) * H), acc);
-    if (lane == 0) {
-#pragma unroll
-      for (int i = 0; i < NV; ++i)
-        reinterpret_cast<uint4*>(ka.agg + (int64_t)c * H)[i] = make_uint4(acc.v[4 * i], acc.v[4 * i + 1], acc.v[4 * i + 2], acc.v[4 * i + 3]);
-    }
+  if (wid == 0 && lane < H) {  // lane p walks state p through the CTA's tables (dependent byte lookups)
+    int st = lane;
+    for (int64_t b = B0; b < B1; ++b) st = c_tab[(b - B0) * H + st];
+    ka.agg[(int64_t)c * H + lane] = (unsigned char)st;
   }
   k3s_dbg(13);
   k3s_grid_sync(ka.sync, 2, G);
