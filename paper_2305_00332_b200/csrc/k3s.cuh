@@ -1141,6 +1141,13 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
   if (alt) *alt = -1;
   if (NWG == 1) k3s_dbg(16);
   if (r < lo || r >= hi) return false;
+  int2 gk[K3S_GCAP / 32] = {};  // group summaries, loaded with the first batch (they only depend on b)
+  if constexpr (NWG == 1) {
+    if (gm) {
+#pragma unroll
+      for (int i = 0; i < K3S_GCAP / 32; ++i) gk[i] = __ldcg(gm + lane + 32 * i);
+    }
+  }
   const double ax = to_f64(xs, prev), ay = to_f64(ys, prev);
   const double2 c = __ldcg(a.means + b);
   const double2 ce = __ldcg(a.merr + b);
@@ -1235,7 +1242,7 @@ __device__ __noinline__ bool grp_verify(const LttbArgs& a, const XT* xs, const Y
         bool sv = false;
         if (gi < gg.ng) {
           double y0, y1;
-          gkey_bounds<YT>(__ldcg(gm + gi), y0, y1);
+          gkey_bounds<YT>(gk[i], y0, y1);
           const int64_t v0g = w.vf + ((int64_t)gi << (gg.s + 5)), v1g = min((int64_t)w.vl, (int64_t)(v0g + (32LL << gg.s)));
           double xa = xr.x, xb = xr.y;
           if (xexact) {
@@ -1573,6 +1580,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   // repair walk of step 5 ----
   {
     const int nf = *(volatile int*)fcount;
+    if (nf == 0) return;  // (grid-uniform) every bucket verified: the output is final, no last-CTA step
     for (int q = c; q < nf; q += (int)G) {
       const int64_t f = __ldcg(a.flist + q);
       int64_t anc = __ldcg(a.best + f);
