@@ -1464,33 +1464,36 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   for (int i = t; i < c * (H / 16); i += NT)
     reinterpret_cast<uint4*>(s_agg)[i] = __ldcg(reinterpret_cast<const uint4*>(ka.agg) + i);
   __syncthreads();
-  if (wid == 0) {
-    const int per = (c + 31) / 32;
-    const int c0 = lane * per, c1 = min(c, c0 + per);
+  k3s_dbg(23);
+  // every thread walks 2 of the 32 x 32 (run, state) pairs through its run of maps;
+  // thread 0 then walks the <= 32 run maps and the CTA's own tables
+  const int per = (c + 31) / 32;
+  {
+    const int l = t >> 4, c0 = l * per, c1 = min(c, c0 + per);
     if (c0 < c1) {
-      unsigned char st[H];
 #pragma unroll
-      for (int p = 0; p < H; ++p) st[p] = (unsigned char)p;
-      for (int cc = c0; cc < c1; ++cc) {
-#pragma unroll
-        for (int p = 0; p < H; ++p) st[p] = s_agg[cc * H + st[p]];
-      }
-#pragma unroll
-      for (int p = 0; p < H; ++p) s_chk[lane * H + p] = st[p];
-    }
-    __syncwarp();
-    if (lane == 0) {
-      int e = 0;
-      for (int l = 0; l * per < c; ++l) e = s_chk[l * H + e];
-      s_e = e;
-      int ee = e;
-      for (int64_t b = B0; b < B1; ++b) {
-        ee = c_tab[(b - B0) * H + ee];
-        c_e[b - B0] = ee;
+      for (int q = 0; q < H / 16; ++q) {
+        const int p0 = (t & 15) * (H / 16) + q;
+        int st = p0;
+        for (int cc = c0; cc < c1; ++cc) st = s_agg[cc * H + st];
+        s_chk[l * H + p0] = (unsigned char)st;
       }
     }
   }
   __syncthreads();
+  k3s_dbg(24);
+  if (t == 0) {
+    int e = 0;
+    for (int l = 0; l * per < c; ++l) e = s_chk[l * H + e];
+    s_e = e;
+    int ee = e;
+    for (int64_t b = B0; b < B1; ++b) {
+      ee = c_tab[(b - B0) * H + ee];
+      c_e[b - B0] = ee;
+    }
+  }
+  __syncthreads();
+  k3s_dbg(25);
   for (int64_t i = t; i <= B1 - B0; i += NT) {
     int64_t p;
     if (i == 0) p = B0 == 0 ? 0 : __ldcg(a.cand + (B0 - 1) * H + s_e);
@@ -1499,6 +1502,7 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
     a.pos[B0 + i] = p;
   }
   if (t == 0 && B1 == k3) a.pos[k3 + 1] = m - 1;
+  k3s_dbg(26);
   __syncthreads();
   stamp(4);
   // ---- 4a: verification (L2), one warp per bucket; the chain's picks go to
