@@ -1431,6 +1431,20 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
   // ---- 2: candidates (L2) ----
   for (int64_t b = B0 + wid; b < B1; b += NW) k3s_cand<XT, YT>(a, ka, xs, ys, b, lbound(a, m, b), lbound(a, m, b + 1), s_glist[wid],
                                                          reinterpret_cast<float2*>(dsm) + wid * K3S_STAGE_LD);  // (dsm: free until phase 3)
+#ifndef K3S_NO_WARM
+  // The first warp without a bucket (C2 has 2-3 of them) runs the verification of the CTA's
+  // first bucket once, with an arbitrary anchor and guess, result discarded (the
+  // function has no side effects): phase 4a is once-through code bound by
+  // instruction fetch (ncu: 49 % of its samples `no_instruction`), and this brings
+  // its instructions to the SM while the other warps search candidates.
+  // (one warp, and only beside >= 12 searching warps: the discarded scan is a full one -- an arbitrary
+  // guess prunes nothing -- and must not outlast the candidate phase; A/B on one box: C2 93.6 vs 95.0 us,
+  // 8 buckets per CTA 79.3 vs 77.4 us without this condition)
+  if (wid == B1 - B0 && B1 - B0 >= 12 && ka.gmeta) {
+    const int64_t wlo = lbound(a, m, B0);
+    (void)grp_verify<1, XT, YT>(a, xs, ys, m, B0, wlo - 1, wlo, nullptr, nullptr, ka.gmeta + B0 * K3S_GCAP);
+  }
+#endif
   __syncthreads();
   stamp(2);
   // the tables of [B0, B1) need CTA c-1's last candidate set
