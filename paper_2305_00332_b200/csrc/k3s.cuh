@@ -1608,7 +1608,11 @@ __global__ void __launch_bounds__(K3S_NT, 1) k_lttb_k3s(LttbArgs a, K3sArgs ka) 
         if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1)] = gtimer();
         const int64_t guess = warp_cand_guess<XT, YT>(a, ka, xs, ys, b, anc);
         if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1) + 1] = gtimer();
-        const int64_t r = grp_pick<NW, XT, YT>(a, xs, ys, m, b, anc, guess, s_red, s_a, s_i);
+        // with group summaries every warp takes the pruned pick on its own (the same
+        // result, no CTA barrier: a few groups instead of the whole bucket by 512 threads)
+        const int64_t r = ka.gmeta ? grp_pick<1, XT, YT>(a, xs, ys, m, b, anc, guess, nullptr, nullptr, nullptr,
+                                                         ka.gmeta + b * K3S_GCAP)
+                                   : grp_pick<NW, XT, YT>(a, xs, ys, m, b, anc, guess, s_red, s_a, s_i);
         if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1) + 2] = gtimer();
         if (dbg) ka.prof[K3S_GMAX * 8 + 16 + 4 * (b - f - 1) + 3] = (unsigned long long)(r == guess);
         k3s_count(6);
