@@ -55,6 +55,9 @@ constexpr int K3S_GMAX = 1024;       // CTA bound for the workspace
 // few groups that can matter: on C2 ~5 of 79 groups per bucket for the
 // candidates and ~1.1 for the verification (a random walk without spikes: 5.1 / 1.14).
 constexpr int K3S_GCAP = 128;
+// K3s never runs beyond this many buckets (its repair state must fit shared memory:
+// 28 bytes per bucket), so the group summaries are not carved for larger calls
+constexpr int64_t K3S_K3MAX = 16384;
 // buckets of fewer groups are scanned whole: bounding 12 groups costs what scanning
 // them does (6e6 f32 points / n_out 4000, 1,500-point buckets: 122 vs 114 us)
 constexpr int K3S_PRUNE_MIN_GROUPS = 24;

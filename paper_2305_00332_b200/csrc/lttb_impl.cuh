@@ -171,8 +171,8 @@ int launch_lttb_large(LttbArgs a, cudaStream_t st) {
     fl.part = cv.take<unsigned char>(k3 * flat_cp_max(k3) * K3C_FLAT_PART);
     fl.ulist = cv.take<int>(k3);
     fl_c.part = fl.part;
-    int2* gmeta = cv.take<int2>(k3 * K3S_GCAP);
-    const int rk = launch_k3s<XT, YT>(a, fl.part, gmeta, st);
+    int2* gmeta = cv.take<int2>(std::min<int64_t>(k3, K3S_K3MAX) * K3S_GCAP);
+    const int rk = k3 <= K3S_K3MAX ? launch_k3s<XT, YT>(a, fl.part, gmeta, st) : MM_ENOTSUP;
     if (rk != MM_ENOTSUP) return rk;  // otherwise: the multi-kernel K3c below
     if (cudaMemsetAsync(fcnt, 0, (size_t)(3 * k3 + 3) * sizeof(unsigned), st) != cudaSuccess)
       return fail(MM_ECUDA, "memset");

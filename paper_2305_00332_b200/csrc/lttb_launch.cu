@@ -15,7 +15,7 @@ int64_t lttb_ws(int64_t B, int64_t n_out, int64_t s) {
          up(B * k3 * 8) + up(B * k3 * 4) + up(B * 4) + up(B * k3 * (int64_t)sizeof(double2)) +
          up(B * k3 * (int64_t)sizeof(XAff)) + up(B * k3 * (int64_t)sizeof(double2)) +
          (B == 1 ? up((3 * k3 + 3) * 4) + up(k3 * flat_cp_max(k3) * K3C_FLAT_PART) + up(k3 * 4) +
-                    up(k3 * (int64_t)mm::K3S_GCAP * 8) : 0);
+                    up(std::min<int64_t>(k3, mm::K3S_K3MAX) * (int64_t)mm::K3S_GCAP * 8) : 0);
 }
 
 int launch_lttb_f32(LttbArgs a, int ydt, int64_t s, cudaStream_t st);

@@ -66,6 +66,10 @@ def test_flat_k3c_workspace_is_bounded():
     a = L.mmlttb_workspace_bytes(_native.OP_LTTB, 1, 10_000_000, 2000, 0, _native.MM_F64)
     b = L.mmlttb_workspace_bytes(_native.OP_LTTB, 1, 1_000_000_000, 2000, 0, _native.MM_F64)
     assert 0 < a < 32 << 20 and a == b
+    # the K3s group summaries (1 KB per bucket) are carved only up to K3S_K3MAX buckets:
+    # a large n_out pays the K3c arrays (~1.5 KB per bucket) and no more
+    c = L.mmlttb_workspace_bytes(_native.OP_LTTB, 1, 100_000_000, 200_000, 0, _native.MM_F64)
+    assert c < 1700 * 200_000 + (32 << 20)
 
 
 def test_error_hierarchy_matches_reference_names():
