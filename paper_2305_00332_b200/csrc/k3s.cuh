@@ -1037,9 +1037,13 @@ __device__ __forceinline__ void warp_scan_area(const XT* xs, const YT* ys, int64
     long long k = __double_as_longlong(tt) & 0x7fffffffffffffffLL;
     bad |= (int)(k >> 32) >= 0x7ff00000;      // inf / NaN: no certification
     k = k > 0x7ff0000000000000LL ? -1LL : k;  // NaN never wins
-    if (k > k2) {
-      if (k > k1) { k2 = k1; k1 = k; il = j; }
-      else k2 = k;
+    // (a lane visits its head / tail element BEFORE its vector elements, so an exact tie
+    // with the running top must still resolve to the lower index: _kernels.py:114's strict
+    // `>` in ascending index order keeps the first of equal areas)
+    if (k > k1) { k2 = k1; k1 = k; il = j; }
+    else {
+      if (k > k2) k2 = k;
+      if (k == k1 && k >= 0 && j < il) il = j;
     }
   };
   const VWin w = vwin<YT>(lo, hi);

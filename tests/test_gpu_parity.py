@@ -753,3 +753,18 @@ def test_lttb_k3s_repeatable():
     for _ in range(30):
         assert torch.equal(mm.lttb(x, y, 2500), first)
     assert np.array_equal(first.cpu().numpy(), O.lttb(x.cpu().numpy(), y.cpu().numpy(), 2500))
+
+
+def test_lttb_tie_with_tail_element_regression():
+    """Found by tools/lttb_fuzz.py (seed 2, case 42): stepped float32 y over a repeating int64 x,
+    328-point buckets.  K3s's warp-level exact scan visits a lane's head / tail element before
+    its vector elements; an exact area tie between the tail and an earlier element of the same
+    lane kept the later index (78 of 6,429 picks off).  The scan now breaks ties by index."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, LTTB_FUZZ_ONLY="42")
+    r = subprocess.run([sys.executable, "tools/lttb_fuzz.py", "43", "2"], env=env, capture_output=True, text=True,
+                       cwd=str(GOLD.parent.parent), timeout=900)
+    assert r.returncode == 0 and "0 mismatches" in r.stdout, r.stdout[-800:] + r.stderr[-1500:]
